@@ -1,0 +1,161 @@
+"""ctypes binding of libcbessfm.so (the C ABI declared in include/cbessfm.h).
+
+The shared library is built in-tree by ``paper_2409_14489_b200/build.py``.
+There is no fallback: if the library is missing or fails to load, every
+entry point raises, so a GPU run can never silently go through host code.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "libcbessfm.so"
+
+CBESSFM_OK = 0
+CBESSFM_ERR_INVALID = 1
+CBESSFM_ERR_UNSUPPORTED = 2
+CBESSFM_ERR_CUDA = 3
+C64, C128 = 0, 1
+
+
+class Desc(C.Structure):
+    _fields_ = [("dtype", C.c_int32), ("n_subbands", C.c_int32),
+                ("block_size", C.c_int32), ("overlap", C.c_int32),
+                ("n_steps", C.c_int32), ("n_phasors", C.c_int32),
+                ("phasors", C.POINTER(C.c_double)),
+                ("phasor_index", C.POINTER(C.c_int32)),
+                ("mimo", C.POINTER(C.c_double)),
+                ("theta_scale", C.POINTER(C.c_double)),
+                ("device", C.c_int32)]
+
+
+class Io(C.Structure):
+    _fields_ = [("in_", C.c_void_p), ("in_batch_stride", C.c_int64),
+                ("in_pol_stride", C.c_int64), ("in_origin", C.c_int64),
+                ("out", C.c_void_p), ("out_batch_stride", C.c_int64),
+                ("out_pol_stride", C.c_int64), ("out_origin", C.c_int64),
+                ("n", C.c_int64), ("batch", C.c_int64),
+                ("block_begin", C.c_int64), ("block_end", C.c_int64)]
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [("threads_per_cta", C.c_int32), ("cluster_size", C.c_int32),
+                ("smem_per_cta", C.c_int64),
+                ("max_active_clusters", C.c_int32), ("q", C.c_int32)]
+
+
+# every symbol include/cbessfm.h declares: name -> (restype, argtypes)
+SIGNATURES = {
+    "cbessfm_version": (C.c_int32, []),
+    "cbessfm_num_blocks": (C.c_int64, [C.c_int64, C.c_int32, C.c_int32]),
+    "cbessfm_supported": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32]),
+    "cbessfm_plan_create": (C.c_int, [C.POINTER(Desc), C.POINTER(C.c_void_p)]),
+    "cbessfm_plan_info_get": (C.c_int, [C.c_void_p, C.POINTER(PlanInfo)]),
+    "cbessfm_run": (C.c_int, [C.c_void_p, C.POINTER(Io), C.c_void_p]),
+    "cbessfm_plan_destroy": (C.c_int, [C.c_void_p]),
+    "cbessfm_last_error": (C.c_char_p, []),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load() -> C.CDLL:
+    """Load (once) and return the library; raises if it is not built."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            path = os.environ.get("CBESSFM_LIB", str(LIB_PATH))
+            if not Path(path).exists():
+                raise RuntimeError(
+                    f"CUDA extension {path} is not built; run "
+                    "`python -c 'import __graft_entry__ as g; g.build()'` "
+                    "(the CB-ESSFM path has no CPU fallback)")
+            lib = C.CDLL(path)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def check(status: int, what: str) -> None:
+    if status == CBESSFM_OK:
+        return
+    msg = load().cbessfm_last_error().decode(errors="replace")
+    text = f"{what}: {msg}"
+    if status in (CBESSFM_ERR_INVALID, CBESSFM_ERR_UNSUPPORTED):
+        raise ValueError(text)
+    raise RuntimeError(text)
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+class NativePlan:
+    """Owns one cbessfm_plan (uploaded tables) on one device."""
+
+    def __init__(self, *, dtype: int, n_subbands: int, block_size: int,
+                 overlap: int, n_steps: int, phasors: np.ndarray,
+                 phasor_index: np.ndarray, mimo: np.ndarray | None,
+                 theta_scale: np.ndarray, device: int):
+        lib = load()
+        self._lib = lib
+        ph = np.ascontiguousarray(phasors, dtype=np.complex128)
+        idx = np.ascontiguousarray(phasor_index, dtype=np.int32)
+        th = np.ascontiguousarray(theta_scale, dtype=np.float64)
+        mi = None if mimo is None else np.ascontiguousarray(mimo, np.complex128)
+        d = Desc(dtype, n_subbands, block_size, overlap, n_steps, ph.shape[0],
+                 ph.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)),
+                 idx.ctypes.data_as(C.POINTER(C.c_int32)),
+                 None if mi is None else _dptr(mi.view(np.float64)),
+                 _dptr(th) if th.size else None, device)
+        handle = C.c_void_p()
+        check(lib.cbessfm_plan_create(C.byref(d), C.byref(handle)),
+              "cbessfm_plan_create")
+        self.handle = handle
+        self.dtype = dtype
+        self.device = device
+        self.block_size = block_size
+        self.overlap = overlap
+        self.n_subbands = n_subbands
+
+    def info(self) -> PlanInfo:
+        out = PlanInfo()
+        check(self._lib.cbessfm_plan_info_get(self.handle, C.byref(out)),
+              "cbessfm_plan_info_get")
+        return out
+
+    def run(self, *, in_ptr: int, in_batch_stride: int, in_pol_stride: int,
+            in_origin: int, out_ptr: int, out_batch_stride: int,
+            out_pol_stride: int, out_origin: int, n: int, batch: int,
+            block_begin: int, block_end: int, stream: int) -> None:
+        io = Io(in_ptr, in_batch_stride, in_pol_stride, in_origin, out_ptr,
+                out_batch_stride, out_pol_stride, out_origin, n, batch,
+                block_begin, block_end)
+        check(self._lib.cbessfm_run(self.handle, C.byref(io), C.c_void_p(stream)),
+              "cbessfm_run")
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self._lib.cbessfm_plan_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
+def num_blocks(n: int, block_size: int, overlap: int) -> int:
+    return int(load().cbessfm_num_blocks(n, block_size, overlap))
+
+
+def supported(dtype: int, n_subbands: int, block_size: int) -> bool:
+    return bool(load().cbessfm_supported(dtype, n_subbands, block_size))

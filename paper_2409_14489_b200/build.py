@@ -1,0 +1,89 @@
+"""Build libcbessfm.so in-tree for sm_100a (no JIT cache, no torch headers).
+
+One object per (real type, n_subbands) instantiation of the fused block
+kernel (csrc/cbessfm_inst.cu) plus the C ABI (csrc/cbessfm_api.cu), compiled
+in parallel with nvcc and linked into ``paper_2409_14489_b200/libcbessfm.so``.
+"""
+
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+BUILD = PKG.parent / "build" / "cbessfm"
+LIB = PKG / "libcbessfm.so"
+HEADERS = [CSRC / "cbessfm_kernel.cuh", CSRC / "cbessfm_launch.cuh",
+           PKG.parent / "include" / "cbessfm.h"]
+REALS = ("float", "double")
+SUBBANDS = tuple(range(1, 10))
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+         "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+
+
+def _nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), shutil.which("nvcc"),
+                 "/usr/local/cuda/bin/nvcc"):
+        if cand and Path(cand).exists():
+            return cand
+    raise RuntimeError("nvcc not found: cannot build the sm_100a extension")
+
+
+def _stale(target: Path, deps) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(Path(d).stat().st_mtime > t for d in deps)
+
+
+def _compile(args):
+    src, obj, defs, deps, log = args
+    if not _stale(obj, [src, *deps]):
+        return obj, None
+    cmd = [_nvcc(), *ARCH, *FLAGS, *defs, "-c", str(src), "-o", str(obj)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    log.write_text(res.stdout + res.stderr)
+    if res.returncode != 0:
+        return obj, f"{' '.join(cmd)}\n{res.stderr[-4000:]}"
+    return obj, None
+
+
+def build(jobs: int | None = None, verbose: bool = False) -> Path:
+    """Compile (incrementally) and link libcbessfm.so; returns its path."""
+    BUILD.mkdir(parents=True, exist_ok=True)
+    jobs = jobs or max(1, min(len(REALS) * len(SUBBANDS) + 1, os.cpu_count() or 1))
+    tasks = []
+    for real in REALS:
+        for p in SUBBANDS:
+            obj = BUILD / f"inst_{real}_{p}.o"
+            tasks.append((CSRC / "cbessfm_inst.cu", obj,
+                          [f"-DCB_REAL={real}", f"-DCB_P={p}"], HEADERS,
+                          BUILD / f"inst_{real}_{p}.log"))
+    tasks.append((CSRC / "cbessfm_api.cu", BUILD / "api.o", [], HEADERS,
+                  BUILD / "api.log"))
+    with ThreadPoolExecutor(jobs) as ex:
+        results = list(ex.map(_compile, tasks))
+    errors = [e for _, e in results if e]
+    if errors:
+        raise RuntimeError("nvcc failed:\n" + "\n\n".join(errors))
+    objs = [o for o, _ in results]
+    if _stale(LIB, objs):
+        cmd = [_nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs),
+               "-lcudart"]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"link failed:\n{res.stderr}")
+    if verbose:
+        print(f"built {LIB}")
+    return LIB
+
+
+if __name__ == "__main__":
+    build(verbose=True)
+    sys.exit(0)

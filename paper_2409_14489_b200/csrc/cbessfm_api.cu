@@ -1,0 +1,360 @@
+// C ABI of the CB-ESSFM hot path (include/cbessfm.h): plan creation
+// (coefficient and filter upload), kernel dispatch over (dtype, P, Q), and
+// error reporting. No torch types cross this boundary.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/cbessfm.h"
+#include "cbessfm_launch.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+cbessfm_status fail(cbessfm_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+cbessfm_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(CBESSFM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+constexpr int kMaxP = 9;
+
+int max_q(int dtype) { return dtype == CBESSFM_C64 ? 8192 : 4096; }
+
+// exp(-2 pi i m / n), m in [0, n), evaluated in long double and rounded once.
+std::vector<double> twiddles(int64_t n) {
+  std::vector<double> t(2 * n);
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (int64_t m = 0; m < n; ++m) {
+    const long double a = -2.0L * pi * (long double)m / (long double)n;
+    t[2 * m] = (double)cosl(a);
+    t[2 * m + 1] = (double)sinl(a);
+  }
+  if (n % 4 == 0) {  // exact values on the axes
+    const double c[4] = {1.0, 0.0, -1.0, 0.0}, sn[4] = {0.0, -1.0, 0.0, 1.0};
+    for (int q = 0; q < 4; ++q) {
+      t[2 * (q * n / 4)] = c[q];
+      t[2 * (q * n / 4) + 1] = sn[q];
+    }
+  }
+  return t;
+}
+
+}  // namespace
+
+struct cbessfm_plan {
+  int dtype, P, Q, N, overlap, n_steps, n_phasors, device;
+  void* phasor = nullptr;  // [n_phasors][P][Q]
+  int* ph_index = nullptr; // [n_steps + 1]
+  void* mimo = nullptr;    // [P][Q/2+1]
+  void* theta = nullptr;   // [n_steps]
+  void* twQ = nullptr;     // [Q]
+  void* twN = nullptr;     // [P*Q]
+};
+
+namespace {
+
+// Round a complex double of (near-)unit modulus, scaled by an exact power of
+// two, to a float pair. Among the +-1 ulp neighbours of the nearest pair we
+// keep the one whose modulus is closest to the exact one: twiddles and
+// dispersion phasors are applied to the same bins every step, so a
+// modulus error would act as a per-bin gain that accumulates coherently
+// over the steps (measured: 1.8e-5 rel L2 after 50 steps with plain
+// rounding), while their phase errors cancel between FFT and IFFT.
+void round_unit(double re, double im, float* ore, float* oim) {
+  const double mod = std::sqrt(re * re + im * im);
+  if (!(mod > 0) || !std::isfinite(mod)) {
+    *ore = (float)re;
+    *oim = (float)im;
+    return;
+  }
+  const int e = std::ilogb(mod);  // unit-modulus form: scale by 2^-e exactly
+  const double ur = std::ldexp(re, -e), ui = std::ldexp(im, -e);
+  const double target = std::ldexp(mod, -e);
+  const double t2 = target * target;
+  const float fr = (float)ur, fi = (float)ui;
+  float best_r = fr, best_i = fi;
+  double best = 1e300;
+  for (int a = -1; a <= 1; ++a) {
+    float cr = fr;
+    if (a < 0) cr = std::nextafter(fr, -INFINITY);
+    if (a > 0) cr = std::nextafter(fr, INFINITY);
+    for (int b = -1; b <= 1; ++b) {
+      float ci = fi;
+      if (b < 0) ci = std::nextafter(fi, -INFINITY);
+      if (b > 0) ci = std::nextafter(fi, INFINITY);
+      const double m2 = (double)cr * cr + (double)ci * ci;
+      const double ang = std::fabs(std::atan2((double)ci, (double)cr) - std::atan2(ui, ur));
+      const double score = std::fabs(m2 - t2) + 1e-3 * ang;
+      if (score < best) {
+        best = score;
+        best_r = cr;
+        best_i = ci;
+      }
+    }
+  }
+  *ore = std::ldexp(best_r, e);
+  *oim = std::ldexp(best_i, e);
+}
+
+template <typename R>
+cudaError_t upload_complex(const double* host, size_t count, void** dev, bool unit = false) {
+  const size_t bytes = count * 2 * sizeof(R);
+  cudaError_t e = cudaMalloc(dev, bytes ? bytes : sizeof(R) * 2);
+  if (e != cudaSuccess) return e;
+  if (!count) return cudaMemset(*dev, 0, sizeof(R) * 2);
+  if (sizeof(R) == sizeof(double)) return cudaMemcpy(*dev, host, bytes, cudaMemcpyHostToDevice);
+  std::vector<float> tmp(2 * count);
+  for (size_t i = 0; i < count; ++i) {
+    if (unit)
+      round_unit(host[2 * i], host[2 * i + 1], &tmp[2 * i], &tmp[2 * i + 1]);
+    else {
+      tmp[2 * i] = (float)host[2 * i];
+      tmp[2 * i + 1] = (float)host[2 * i + 1];
+    }
+  }
+  return cudaMemcpy(*dev, tmp.data(), bytes, cudaMemcpyHostToDevice);
+}
+
+template <typename R>
+cudaError_t upload_real(const double* host, size_t count, void** dev) {
+  const size_t bytes = count * sizeof(R);
+  cudaError_t e = cudaMalloc(dev, bytes ? bytes : sizeof(R));
+  if (e != cudaSuccess || !count) return e;
+  if (sizeof(R) == sizeof(double)) return cudaMemcpy(*dev, host, bytes, cudaMemcpyHostToDevice);
+  std::vector<float> tmp(count);
+  for (size_t i = 0; i < count; ++i) tmp[i] = (float)host[i];
+  return cudaMemcpy(*dev, tmp.data(), bytes, cudaMemcpyHostToDevice);
+}
+
+template <typename R>
+cbessfm_status upload_all(cbessfm_plan* p, const cbessfm_desc* d) {
+  const size_t PQ = (size_t)p->P * p->Q;
+  const size_t H1 = (size_t)p->Q / 2 + 1;
+  cudaError_t e;
+  if ((e = upload_complex<R>(d->phasors, (size_t)p->n_phasors * PQ, &p->phasor, true)) != cudaSuccess)
+    return cuda_fail(e, "upload phasors");
+  if ((e = cudaMalloc((void**)&p->ph_index, sizeof(int) * (p->n_steps + 1))) != cudaSuccess)
+    return cuda_fail(e, "alloc phasor index");
+  if ((e = cudaMemcpy(p->ph_index, d->phasor_index, sizeof(int) * (p->n_steps + 1),
+                      cudaMemcpyHostToDevice)) != cudaSuccess)
+    return cuda_fail(e, "upload phasor index");
+  std::vector<double> zeros;
+  const double* mimo = d->mimo;
+  if (!mimo) {
+    zeros.assign(2 * p->P * H1, 0.0);
+    mimo = zeros.data();
+  }
+  if ((e = upload_complex<R>(mimo, (size_t)p->P * H1, &p->mimo)) != cudaSuccess)
+    return cuda_fail(e, "upload MIMO spectra");
+  if ((e = upload_real<R>(d->theta_scale, (size_t)p->n_steps, &p->theta)) != cudaSuccess)
+    return cuda_fail(e, "upload theta scales");
+  const std::vector<double> tq = twiddles(p->Q), tn = twiddles((int64_t)p->P * p->Q);
+  if ((e = upload_complex<R>(tq.data(), (size_t)p->Q, &p->twQ, true)) != cudaSuccess)
+    return cuda_fail(e, "upload twiddles");
+  if ((e = upload_complex<R>(tn.data(), PQ, &p->twN, true)) != cudaSuccess)
+    return cuda_fail(e, "upload outer twiddles");
+  return CBESSFM_OK;
+}
+
+void free_plan(cbessfm_plan* p) {
+  if (!p) return;
+  cudaFree(p->phasor);
+  cudaFree(p->ph_index);
+  cudaFree(p->mimo);
+  cudaFree(p->theta);
+  cudaFree(p->twQ);
+  cudaFree(p->twN);
+  delete p;
+}
+
+template <typename R>
+cudaError_t dispatch(int P, const cbessfm::Params<R>& prm, int q, int64_t nclusters,
+                     cudaStream_t st, cbessfm::KernelInfo* info);
+
+#define CB_CASE(T, P) \
+  case P: return cbessfm::launch_##T##_##P(prm, q, nclusters, st, info);
+template <>
+cudaError_t dispatch<float>(int P, const cbessfm::Params<float>& prm, int q, int64_t nclusters,
+                            cudaStream_t st, cbessfm::KernelInfo* info) {
+  switch (P) {
+    CB_CASE(float, 1) CB_CASE(float, 2) CB_CASE(float, 3) CB_CASE(float, 4) CB_CASE(float, 5)
+    CB_CASE(float, 6) CB_CASE(float, 7) CB_CASE(float, 8) CB_CASE(float, 9)
+    default: return cudaErrorInvalidValue;
+  }
+}
+template <>
+cudaError_t dispatch<double>(int P, const cbessfm::Params<double>& prm, int q, int64_t nclusters,
+                             cudaStream_t st, cbessfm::KernelInfo* info) {
+  switch (P) {
+    CB_CASE(double, 1) CB_CASE(double, 2) CB_CASE(double, 3) CB_CASE(double, 4)
+    CB_CASE(double, 5) CB_CASE(double, 6) CB_CASE(double, 7) CB_CASE(double, 8)
+    CB_CASE(double, 9)
+    default: return cudaErrorInvalidValue;
+  }
+}
+#undef CB_CASE
+
+template <typename R>
+cbessfm::Params<R> make_params(const cbessfm_plan* p, const cbessfm_io* io) {
+  using C = cbessfm::Cx<R>;
+  cbessfm::Params<R> prm;
+  prm.in = reinterpret_cast<const C*>(io->in);
+  prm.out = reinterpret_cast<C*>(io->out);
+  prm.in_bstride = io->in_batch_stride;
+  prm.in_pstride = io->in_pol_stride;
+  prm.in_origin = io->in_origin;
+  prm.out_bstride = io->out_batch_stride;
+  prm.out_pstride = io->out_pol_stride;
+  prm.out_origin = io->out_origin;
+  prm.n = io->n;
+  prm.b0 = io->block_begin;
+  prm.nb = io->block_end - io->block_begin;
+  prm.keep = p->N - p->overlap;
+  prm.half = p->overlap / 2;
+  prm.phasor = reinterpret_cast<const C*>(p->phasor);
+  prm.ph_index = p->ph_index;
+  prm.mimo = reinterpret_cast<const C*>(p->mimo);
+  prm.theta_scale = reinterpret_cast<const R*>(p->theta);
+  prm.twQ = reinterpret_cast<const C*>(p->twQ);
+  prm.twN = reinterpret_cast<const C*>(p->twN);
+  prm.n_steps = p->n_steps;
+  prm.cid0 = 0;
+  return prm;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t cbessfm_version(void) { return CBESSFM_VERSION; }
+
+int64_t cbessfm_num_blocks(int64_t n, int32_t block_size, int32_t overlap) {
+  if (n <= 0 || block_size <= 0 || overlap < 0 || overlap >= block_size) return -1;
+  const int64_t keep = block_size - overlap;
+  return (n + keep - 1) / keep;
+}
+
+int32_t cbessfm_supported(int32_t dtype, int32_t n_subbands, int32_t block_size) {
+  if (dtype != CBESSFM_C64 && dtype != CBESSFM_C128) return 0;
+  if (n_subbands < 1 || n_subbands > kMaxP || block_size % n_subbands) return 0;
+  const int q = block_size / n_subbands;
+  return is_pow2(q) && q >= 256 && q <= max_q(dtype);
+}
+
+cbessfm_status cbessfm_plan_create(const cbessfm_desc* d, cbessfm_plan** out) {
+  g_err.clear();
+  if (!d || !out) return fail(CBESSFM_ERR_INVALID, "null descriptor or output pointer");
+  *out = nullptr;
+  if (d->dtype != CBESSFM_C64 && d->dtype != CBESSFM_C128)
+    return fail(CBESSFM_ERR_INVALID, "dtype must be CBESSFM_C64 or CBESSFM_C128");
+  if (d->n_subbands < 1) return fail(CBESSFM_ERR_INVALID, "n_subbands must be >= 1");
+  if (d->block_size <= d->overlap || d->overlap < 0)
+    return fail(CBESSFM_ERR_INVALID, "need block_size > overlap >= 0");
+  if (d->block_size % d->n_subbands)
+    return fail(CBESSFM_ERR_INVALID, "block_size must divide into n_subbands");
+  if (d->overlap % (2 * d->n_subbands))
+    return fail(CBESSFM_ERR_INVALID, "overlap must be a multiple of 2*n_subbands");
+  if (d->n_steps < 0) return fail(CBESSFM_ERR_INVALID, "n_steps must be >= 0");
+  if (d->n_phasors < 1 || !d->phasors || !d->phasor_index)
+    return fail(CBESSFM_ERR_INVALID, "phasor tables missing");
+  if (d->n_steps > 0 && !d->theta_scale)
+    return fail(CBESSFM_ERR_INVALID, "theta scales missing");
+  for (int s = 0; s <= d->n_steps; ++s)
+    if (d->phasor_index[s] < 0 || d->phasor_index[s] >= d->n_phasors)
+      return fail(CBESSFM_ERR_INVALID, "phasor index out of range");
+  if (!cbessfm_supported(d->dtype, d->n_subbands, d->block_size)) {
+    char buf[256];
+    snprintf(buf, sizeof buf,
+             "unsupported shape for the sm_100a kernel: n_subbands=%d (1..%d), "
+             "N'=block_size/n_subbands=%d (power of two in [256, %d])",
+             d->n_subbands, kMaxP, d->block_size / d->n_subbands, max_q(d->dtype));
+    return fail(CBESSFM_ERR_UNSUPPORTED, buf);
+  }
+  cbessfm_plan* p = new (std::nothrow) cbessfm_plan;
+  if (!p) return fail(CBESSFM_ERR_INVALID, "out of host memory");
+  p->dtype = d->dtype;
+  p->P = d->n_subbands;
+  p->Q = d->block_size / d->n_subbands;
+  p->N = d->block_size;
+  p->overlap = d->overlap;
+  p->n_steps = d->n_steps;
+  p->n_phasors = d->n_phasors;
+  p->device = d->device;
+  cudaError_t e = cudaSetDevice(d->device);
+  if (e != cudaSuccess) {
+    delete p;
+    return cuda_fail(e, "cudaSetDevice");
+  }
+  const cbessfm_status st =
+      p->dtype == CBESSFM_C64 ? upload_all<float>(p, d) : upload_all<double>(p, d);
+  if (st != CBESSFM_OK) {
+    free_plan(p);
+    return st;
+  }
+  *out = p;
+  return CBESSFM_OK;
+}
+
+cbessfm_status cbessfm_plan_info_get(const cbessfm_plan* p, cbessfm_plan_info* info) {
+  g_err.clear();
+  if (!p || !info) return fail(CBESSFM_ERR_INVALID, "null plan or info");
+  cbessfm::KernelInfo ki{};
+  cudaError_t e;
+  if (p->dtype == CBESSFM_C64) {
+    cbessfm::Params<float> prm{};
+    e = dispatch<float>(p->P, prm, p->Q, 0, nullptr, &ki);
+  } else {
+    cbessfm::Params<double> prm{};
+    e = dispatch<double>(p->P, prm, p->Q, 0, nullptr, &ki);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "kernel occupancy query");
+  info->threads_per_cta = ki.threads;
+  info->cluster_size = ki.cluster;
+  info->smem_per_cta = (int64_t)ki.smem;
+  info->max_active_clusters = ki.max_active_clusters;
+  info->q = p->Q;
+  return CBESSFM_OK;
+}
+
+cbessfm_status cbessfm_run(const cbessfm_plan* p, const cbessfm_io* io, void* stream) {
+  g_err.clear();
+  if (!p || !io) return fail(CBESSFM_ERR_INVALID, "null plan or io");
+  if (!io->in || !io->out) return fail(CBESSFM_ERR_INVALID, "null input or output buffer");
+  if (io->n < p->N) return fail(CBESSFM_ERR_INVALID, "block_size exceeds the sequence length");
+  if (io->batch < 0) return fail(CBESSFM_ERR_INVALID, "negative batch");
+  const int64_t nblk = cbessfm_num_blocks(io->n, p->N, p->overlap);
+  if (io->block_begin < 0 || io->block_end > nblk || io->block_begin > io->block_end)
+    return fail(CBESSFM_ERR_INVALID, "block range outside [0, n_blocks]");
+  if (io->in_origin < 0 || io->in_origin >= io->n || io->out_origin < 0)
+    return fail(CBESSFM_ERR_INVALID, "origins out of range");
+  const int64_t nclusters = io->batch * (io->block_end - io->block_begin);
+  if (nclusters == 0) return CBESSFM_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (p->dtype == CBESSFM_C64)
+    e = dispatch<float>(p->P, make_params<float>(p, io), p->Q, nclusters, st, nullptr);
+  else
+    e = dispatch<double>(p->P, make_params<double>(p, io), p->Q, nclusters, st, nullptr);
+  if (e != cudaSuccess) return cuda_fail(e, "cbessfm kernel launch");
+  return CBESSFM_OK;
+}
+
+cbessfm_status cbessfm_plan_destroy(cbessfm_plan* p) {
+  g_err.clear();
+  free_plan(p);
+  return CBESSFM_OK;
+}
+
+const char* cbessfm_last_error(void) { return g_err.c_str(); }
+
+}  // extern "C"

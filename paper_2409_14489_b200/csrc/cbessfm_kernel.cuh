@@ -1,0 +1,669 @@
+// Fused CB-ESSFM overlap-save block kernel for sm_100a.
+//
+// One thread-block cluster processes one overlap-save block of one waveform.
+// CTA r of a P-CTA cluster (P = n_subbands) owns subband r for both
+// polarisations; its fields stay resident in shared memory through every
+// step. Cross-subband data movement (the outer N = P*Q transform and the
+// per-step MIMO coupling of the intensity spectra) goes over distributed
+// shared memory (DSMEM) inside the cluster; nothing round-trips through HBM
+// between the block load and the store of the kept samples.
+//
+// Reference semantics (fiberdbp 0.1.0, /root/reference/pkg/src/fiberdbp):
+//   block framing ............ dbp.py:467-477  (circular window, keep/half)
+//   outer FFT + subband demux  dbp.py:387-389
+//   per-step dispersion ...... dbp.py:395, tables dbp.py:352-359
+//   subband IFFT / FFT ....... dbp.py:396, dbp.py:398
+//   NLPR (intensity, rfft, MIMO, irfft, rotation) dbp.py:185-208
+//   final phasor + merge ..... dbp.py:399-401
+//   discard .................. dbp.py:476-477
+//
+// Scaling conventions (all folded into host-built tables, see planner.py):
+//   * phasor tables carry 1/Q (the subband IFFT normalisation);
+//   * the forward outer exchange applies 1/P (dbp.py:388 "/ n_sb");
+//   * the merge "* n_sb" and the outer IFFT's 1/N combine to 1/Q, which the
+//     final phasor table already carries, so the inverse outer transform is
+//     an unnormalised sum;
+//   * theta_scale[st] = step_scales[st] / reference_power_w / Q (irfft 1/Q).
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cbessfm {
+
+namespace cg = cooperative_groups;
+
+template <typename R>
+struct alignas(2 * sizeof(R)) Cx {
+  R x, y;
+};
+
+template <typename R>
+__device__ __forceinline__ Cx<R> mk(R a, R b) {
+  Cx<R> c;
+  c.x = a;
+  c.y = b;
+  return c;
+}
+template <typename R>
+__device__ __forceinline__ Cx<R> operator+(Cx<R> a, Cx<R> b) {
+  return mk(a.x + b.x, a.y + b.y);
+}
+template <typename R>
+__device__ __forceinline__ Cx<R> operator-(Cx<R> a, Cx<R> b) {
+  return mk(a.x - b.x, a.y - b.y);
+}
+template <typename R>
+__device__ __forceinline__ Cx<R> cmul(Cx<R> a, Cx<R> b) {
+  return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a * conj(b)
+template <typename R>
+__device__ __forceinline__ Cx<R> cmulc(Cx<R> a, Cx<R> b) {
+  return mk(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+template <typename R>
+__device__ __forceinline__ Cx<R> conj(Cx<R> a) {
+  return mk(a.x, -a.y);
+}
+template <typename R>
+__device__ __forceinline__ Cx<R> scale(Cx<R> a, R s) {
+  return mk(a.x * s, a.y * s);
+}
+
+__device__ __forceinline__ Cx<float> ldg(const Cx<float>* p) {
+  const float2 v = __ldg(reinterpret_cast<const float2*>(p));
+  return mk(v.x, v.y);
+}
+__device__ __forceinline__ Cx<double> ldg(const Cx<double>* p) {
+  const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+  return mk(v.x, v.y);
+}
+
+// Twiddle loads inside the FFT passes go through the non-coherent L1 path
+// as volatile asm: the table is loop invariant, and letting the compiler
+// hoist every pass's twiddles out of the step loop exhausts the register
+// file (measured: ~900 B of spills per thread at 128 registers).
+__device__ __forceinline__ Cx<float> ldg_tw(const Cx<float>* p) {
+  float a, b;
+  asm volatile("ld.global.v2.f32 {%0, %1}, [%2];" : "=f"(a), "=f"(b) : "l"(p));
+  return mk(a, b);
+}
+__device__ __forceinline__ Cx<double> ldg_tw(const Cx<double>* p) {
+  double a, b;
+  asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "l"(p));
+  return mk(a, b);
+}
+
+// threadIdx.x read through volatile asm: keeps per-pass shared-memory
+// address arithmetic inside the step loop instead of letting loop-invariant
+// code motion hoist every pass's addresses into live registers.
+__device__ __forceinline__ int tid_opaque() {
+  int t;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t));
+  return t;
+}
+
+// Shared-memory index padding: one spare element every 16 complex entries
+// makes the radix-16 Stockham scatter (lane stride 16 elements) conflict-free.
+__device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int padded_len(int n) { return n + (n >> 4) + 1; }
+
+// ------------------------------------------------------------------------
+// Small DFTs in registers (radix 2..16), radix-2 DIF network with
+// compile-time twiddles; output is bit-reversed (callers index through
+// bitrev<RAD>).
+
+template <int RAD>
+__device__ __forceinline__ constexpr int bitrev(int r) {
+  int o = 0;
+  for (int b = 1; b < RAD; b <<= 1) {
+    o = (o << 1) | (r & 1);
+    r >>= 1;
+  }
+  return o;
+}
+
+// cos / sin of 2*pi*e/16, e = 0..15 (exact decimal expansions)
+__device__ __forceinline__ constexpr double c16(int e) {
+  constexpr double t[16] = {1.0,
+                            0.92387953251128675613,
+                            0.70710678118654752440,
+                            0.38268343236508977173,
+                            0.0,
+                            -0.38268343236508977173,
+                            -0.70710678118654752440,
+                            -0.92387953251128675613,
+                            -1.0,
+                            -0.92387953251128675613,
+                            -0.70710678118654752440,
+                            -0.38268343236508977173,
+                            0.0,
+                            0.38268343236508977173,
+                            0.70710678118654752440,
+                            0.92387953251128675613};
+  return t[e & 15];
+}
+__device__ __forceinline__ constexpr double s16(int e) { return c16(e - 4); }
+
+// d * W_16^{e16} (forward: exp(-2 pi i e16 / 16); inverse: conjugate),
+// e16 in [0, 8) and known at compile time after unrolling.
+// a * sqrt(1/2) with a two-term constant in float: the one-term float
+// constant is 1.7e-8 low, a systematic gain that would repeat in every
+// FFT of every step.
+template <typename R>
+__device__ __forceinline__ R mul_rsqrt2(R a) {
+  if constexpr (sizeof(R) == 4) {
+    return __fmaf_rn(a, 0.707106769084930419921875f, a * 1.21016175e-08f);
+  } else {
+    return a * 0.70710678118654752440;
+  }
+}
+
+// d * W_16^{e16} (forward: exp(-2 pi i e16 / 16); inverse: conjugate),
+// e16 in [0, 8) and known at compile time after unrolling.
+template <typename R, bool INV>
+__device__ __forceinline__ Cx<R> tw16(Cx<R> d, int e16) {
+  if (e16 == 0) return d;
+  if (e16 == 4) return INV ? mk(-d.y, d.x) : mk(d.y, -d.x);  // +i / -i
+  if (e16 == 2)  // (1 -+ i)/sqrt2
+    return INV ? mk(mul_rsqrt2(d.x - d.y), mul_rsqrt2(d.x + d.y))
+               : mk(mul_rsqrt2(d.x + d.y), mul_rsqrt2(d.y - d.x));
+  if (e16 == 6)  // (-1 -+ i)/sqrt2
+    return INV ? mk(-mul_rsqrt2(d.x + d.y), mul_rsqrt2(d.x - d.y))
+               : mk(mul_rsqrt2(d.y - d.x), -mul_rsqrt2(d.x + d.y));
+  const R c = (R)c16(e16);
+  const R s = INV ? (R)s16(e16) : (R)-s16(e16);
+  return mk(d.x * c - d.y * s, d.x * s + d.y * c);
+}
+
+template <typename R, int RAD, bool INV>
+__device__ __forceinline__ void dft_reg(Cx<R>* v) {
+#pragma unroll
+  for (int span = RAD / 2; span >= 1; span >>= 1) {
+#pragma unroll
+    for (int start = 0; start < RAD; start += 2 * span) {
+#pragma unroll
+      for (int i = 0; i < span; ++i) {
+        const Cx<R> a = v[start + i];
+        const Cx<R> b = v[start + i + span];
+        v[start + i] = a + b;
+        v[start + i + span] = tw16<R, INV>(a - b, i * (16 / (2 * span)));
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------
+// Stockham radix-RAD pass over NA arrays of length L stored at stride
+// padded_len(L) in shared memory, register staged (load all, barrier, store
+// all, barrier). twQ is the length-Q table exp(-2 pi i m / Q).
+
+template <int L, int MAXRAD, int NS>
+struct PassRadix {
+  static constexpr int rem = L / NS;
+  static constexpr int value = rem >= MAXRAD ? MAXRAD : rem;
+};
+
+// Addressing: with one pad slot per 16 entries, pad(a + b) == pad(a) + pad(b)
+// for every (read, write) index pair a Stockham pass forms (checked
+// exhaustively in tests/test_host_logic.py), so each pass needs one read and
+// one write base register plus compile-time offsets. `zero` is a shared
+// memory word holding 0: reading it after the barrier makes every pass's
+// addressing loop-variant, which stops ptxas from hoisting all passes'
+// address registers out of the step loop (it otherwise spills).
+__device__ __forceinline__ void bar_named(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <typename R, int Q, int L, int NA, int RAD, int NS, bool INV>
+__device__ __forceinline__ void butterfly_load(const Cx<R>* __restrict__ buf,
+                                               const Cx<R>* __restrict__ twQ, int jj,
+                                               Cx<R>* v) {
+  constexpr int STRIDE = padded_len(L);
+  constexpr int TWM = Q / (NS * RAD);  // twiddle index multiplier
+  constexpr int LR = L / RAD;
+  const int a = jj / LR;
+  const int j = jj % LR;
+  const Cx<R>* base = buf + a * STRIDE + pad(j);
+#pragma unroll
+  for (int r = 0; r < RAD; ++r) v[r] = base[pad(r * LR)];
+  if (NS > 1) {
+    const int k = j % NS;
+    const Cx<R>* tw = twQ + k * TWM;
+    const int step = k * TWM;
+#pragma unroll
+    for (int r = 1; r < RAD; ++r) {
+      const Cx<R> w = ldg_tw(tw + (r - 1) * step);
+      v[r] = INV ? cmulc(v[r], w) : cmul(v[r], w);
+    }
+  }
+  dft_reg<R, RAD, INV>(v);
+}
+
+template <typename R, int L, int NA, int RAD, int NS>
+__device__ __forceinline__ void butterfly_store(Cx<R>* __restrict__ buf, int jj,
+                                                const Cx<R>* v) {
+  constexpr int STRIDE = padded_len(L);
+  constexpr int LR = L / RAD;
+  const int a = jj / LR;
+  const int j = jj % LR;
+  const int k = j % NS;
+  Cx<R>* base = buf + a * STRIDE + pad((j / NS) * NS * RAD + k);
+#pragma unroll
+  for (int r = 0; r < RAD; ++r) base[pad(r * NS)] = v[bitrev<RAD>(r)];
+}
+
+// Addressing: with one pad slot per 16 entries, pad(a + b) == pad(a) + pad(b)
+// for every (read, write) index pair a Stockham pass forms (checked
+// exhaustively in tests/test_host_logic.py), so each pass needs one read and
+// one write base register plus compile-time offsets. `zero` is a shared
+// memory word holding 0: reading it after the barrier makes every pass's
+// addressing loop-variant, which stops ptxas from hoisting all passes'
+// address registers out of the step loop (it otherwise spills).
+// Passes with fewer butterflies than threads run on the leading whole warps
+// only; those synchronise between load and store with a named barrier, so
+// the staged registers never have to live across a divergent region.
+template <typename R, int Q, int L, int NA, int NT, int RAD, int NS, bool INV>
+__device__ __forceinline__ void fft_pass(Cx<R>* __restrict__ buf,
+                                         const Cx<R>* __restrict__ twQ,
+                                         const volatile int* zero) {
+  constexpr int NB = NA * L / RAD;  // butterflies in this pass
+  const int tid = threadIdx.x + *zero;
+  if constexpr (NB >= NT) {
+    static_assert(NB % NT == 0, "butterflies must tile the block");
+    constexpr int PER = NB / NT;
+    Cx<R> v[PER][RAD];
+#pragma unroll
+    for (int p = 0; p < PER; ++p)
+      butterfly_load<R, Q, L, NA, RAD, NS, INV>(buf, twQ, tid + p * NT, v[p]);
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < PER; ++p) butterfly_store<R, L, NA, RAD, NS>(buf, tid + p * NT, v[p]);
+    __syncthreads();
+  } else {
+    constexpr int ACT = (NB + 31) / 32 * 32;  // active threads, whole warps
+    if (tid < ACT) {
+      Cx<R> v[RAD];
+      const bool on = (NB % 32 == 0) || tid < NB;
+      if (on) butterfly_load<R, Q, L, NA, RAD, NS, INV>(buf, twQ, tid, v);
+      bar_named(1, ACT);
+      if (on) butterfly_store<R, L, NA, RAD, NS>(buf, tid, v);
+    }
+    // full barrier: no warp may run ahead into a later pass whose named
+    // barrier expects a different thread count
+    __syncthreads();
+  }
+}
+
+template <typename R, int Q, int L, int NA, int NT, int MAXRAD, int NS, bool INV>
+struct FftRun {
+  static __device__ __forceinline__ void run(Cx<R>* buf, const Cx<R>* twQ, const volatile int* z) {
+    constexpr int RAD = PassRadix<L, MAXRAD, NS>::value;
+    fft_pass<R, Q, L, NA, NT, RAD, NS, INV>(buf, twQ, z);
+    FftRun<R, Q, L, NA, NT, MAXRAD, NS * RAD, INV>::run(buf, twQ, z);
+  }
+};
+template <typename R, int Q, int L, int NA, int NT, int MAXRAD, bool INV>
+struct FftRun<R, Q, L, NA, NT, MAXRAD, L, INV> {
+  static __device__ __forceinline__ void run(Cx<R>*, const Cx<R>*, const volatile int*) {}
+};
+
+// Unnormalised FFT (forward: exp(-), inverse: exp(+)) of NA arrays of
+// length L in place, natural order in and out. Ends with a barrier.
+template <typename R, int Q, int L, int NA, int NT, int MAXRAD, bool INV>
+__device__ __forceinline__ void fft(Cx<R>* buf, const Cx<R>* twQ, const volatile int* z) {
+  FftRun<R, Q, L, NA, NT, MAXRAD, 1, INV>::run(buf, twQ, z);
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------------
+
+template <typename R>
+struct Params {
+  const Cx<R>* in;
+  Cx<R>* out;
+  int64_t in_bstride, in_pstride, in_origin;
+  int64_t out_bstride, out_pstride, out_origin;
+  int64_t n;        // circular period of the waveform
+  int64_t b0;       // first global block index of this launch
+  int64_t nb;       // blocks per waveform in this launch
+  int64_t keep;     // block_size - overlap
+  int64_t half;     // overlap / 2
+  const Cx<R>* phasor;     // [n_tab][P][Q], carries 1/Q
+  const int* ph_index;     // [n_steps + 1]
+  const Cx<R>* mimo;       // [P][Q/2+1], S_h with the 3/2 XPM weight folded
+  const R* theta_scale;    // [n_steps], carries 1/Q
+  const Cx<R>* twQ;        // [Q]   exp(-2 pi i m / Q)
+  const Cx<R>* twN;        // [P*Q] exp(-2 pi i m / (P Q))
+  int n_steps;
+  int64_t cid0;     // first cluster index of this launch chunk
+};
+
+template <typename R>
+__device__ __forceinline__ void sincos_acc(R a, R* s, R* c);
+template <>
+__device__ __forceinline__ void sincos_acc<float>(float a, float* s, float* c) {
+  sincosf(a, s, c);
+}
+template <>
+__device__ __forceinline__ void sincos_acc<double>(double a, double* s, double* c) {
+  sincos(a, s, c);
+}
+
+template <typename R>
+struct Cfg {
+  // max radix of the register-staged Stockham passes
+  static constexpr int MAXRAD = 8;
+};
+
+// One radix-8 butterfly per thread on the two-polarisation field FFTs;
+// capped so double-precision blocks stay within 128 registers.
+template <typename R, int Q>
+__host__ __device__ constexpr int threads_for() {
+  return (Q / 4) > (sizeof(R) == 4 ? 1024 : 512) ? (sizeof(R) == 4 ? 1024 : 512) : Q / 4;
+}
+
+// Resident CTAs per SM the register budget is sized for: 1024 threads at
+// <= 64 registers (float) or 512 threads at <= 128 registers (double).
+template <typename R, int Q>
+__host__ __device__ constexpr int min_blocks() {
+  return (sizeof(R) == 4 ? 1024 : 512) / threads_for<R, Q>() > 1
+             ? (sizeof(R) == 4 ? 1024 : 512) / threads_for<R, Q>()
+             : 1;
+}
+
+template <typename R, int Q>
+__host__ __device__ constexpr size_t smem_bytes(int P) {
+  // F: 2 padded polarisation arrays; IS, TS: padded spectra (Q/2+1 bins)
+  return sizeof(Cx<R>) * (size_t)(2 * padded_len(Q) + (P > 1 ? 2 : 1) * padded_len(Q / 2 + 1));
+}
+
+// Position of global FFT bin g (of N = P*Q) in the subband layout:
+// shifted s = (g + N/2) mod N, subband i = s / Q, local j = s mod Q,
+// ifftshift'd storage m = (j + Q/2) mod Q   (dbp.py:387-389).
+template <int P, int Q>
+__device__ __forceinline__ void bin_home(int g, int& i, int& m) {
+  constexpr int N = P * Q;
+  int s = g + N / 2;
+  if (s >= N) s -= N;
+  i = s / Q;
+  m = (s % Q + Q / 2) % Q;
+}
+
+template <typename R, int P, int Q>
+__global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
+    cbessfm_block_kernel(const Params<R> prm) {
+  constexpr int NT = threads_for<R, Q>();
+  constexpr int N = P * Q;
+  constexpr int H = Q / 2;
+  constexpr int SF = padded_len(Q);      // stride between x and y in F
+  constexpr int MAXRAD = Cfg<R>::MAXRAD;
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Cx<R>* F = reinterpret_cast<Cx<R>*>(smem_raw);
+  Cx<R>* IS = F + 2 * SF;
+  Cx<R>* TS = (P > 1) ? IS + padded_len(H + 1) : IS;
+
+  __shared__ int s_zero;
+  if (threadIdx.x == 0) s_zero = 0;
+  const int tid = threadIdx.x;
+  const int rank = (P > 1) ? (int)(blockIdx.x % P) : 0;
+  const int64_t cid = prm.cid0 + blockIdx.x / P;
+  const int64_t wv = cid / prm.nb;
+  const int64_t b = prm.b0 + cid % prm.nb;
+  const int64_t n = prm.n;
+
+  const Cx<R>* __restrict__ twQ = prm.twQ;
+  const Cx<R>* __restrict__ twN = prm.twN;
+
+  // ---- 1. load the polyphase component u[rank + P*t2] of the circular
+  //         window starting at (b*keep - half) mod n (dbp.py:473-475)
+  {
+    int64_t start = (b * prm.keep - prm.half) % n;
+    if (start < 0) start += n;
+    start -= prm.in_origin;
+    if (start < 0) start += n;
+    const Cx<R>* src = prm.in + wv * prm.in_bstride;
+    for (int t2 = tid; t2 < Q; t2 += NT) {
+      int64_t idx = start + rank + (int64_t)P * t2;
+      if (idx >= n) idx -= n;
+      F[pad(t2)] = src[idx];
+      F[SF + pad(t2)] = src[prm.in_pstride + idx];
+    }
+  }
+  __syncthreads();
+
+  // ---- 2. outer transform, polyphase part: FFT_Q of both polarisations
+  fft<R, Q, Q, 2, NT, MAXRAD, false>(F, twQ, &s_zero);
+
+  const Cx<R>* ph = prm.phasor + (size_t)rank * Q;  // this CTA's subband rows
+  const size_t ph_tab = (size_t)P * Q;
+
+  if constexpr (P > 1) {
+    // ---- 3. cross-subband radix-P stage over DSMEM: CTA c produces bins
+    //         Q*k1 + k2 for k2 in its slice and every k1, and writes each to
+    //         the CTA that owns it in the fftshift'd subband layout. Results
+    //         are staged in the owner's idle IS/TS region (one polarisation
+    //         at a time), so no CTA overwrites fields another CTA still reads.
+    cg::cluster_group cluster = cg::this_cluster();
+    const int lo = (rank * Q) / P, hi = ((rank + 1) * Q) / P;
+    const R invP = (R)1 / (R)P;
+    const Cx<R>* ph0 = prm.phasor + (size_t)prm.ph_index[0] * ph_tab;
+    Cx<R>* S = IS;  // staging: padded_len(Q) entries fit in IS + TS
+    cluster.sync();
+    for (int pol = 0; pol < 2; ++pol) {
+      for (int k2 = lo + tid; k2 < hi; k2 += NT) {
+        Cx<R> bv[P];
+#pragma unroll
+        for (int r = 0; r < P; ++r) {
+          const Cx<R>* rf = cluster.map_shared_rank(F, r);
+          Cx<R> v = rf[pol * SF + pad(k2)];
+          if (r) v = cmul(v, ldg(twN + r * k2));
+          bv[r] = v;
+        }
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) {
+          Cx<R> s = bv[0];
+#pragma unroll
+          for (int r = 1; r < P; ++r) s = s + cmul(bv[r], ldg(twN + ((r * k1) % P) * Q));
+          int i, m;
+          bin_home<P, Q>(Q * k1 + k2, i, m);
+          const Cx<R> w = ldg(ph0 + (size_t)i * Q + m);
+          Cx<R>* dst = cluster.map_shared_rank(S, i);
+          dst[pad(m)] = cmul(scale(s, invP), w);
+        }
+      }
+      cluster.sync();
+      for (int t = tid; t < Q; t += NT) F[pol * SF + pad(t)] = S[pad(t)];
+      cluster.sync();
+    }
+  } else {
+    // P == 1: the subband layout is the natural FFT order (bin_home is the
+    // identity); apply the first phasor in place.
+    const Cx<R>* w0 = ph + (size_t)prm.ph_index[0] * ph_tab;
+    for (int t = tid; t < Q; t += NT) {
+      const Cx<R> w = ldg(w0 + t);
+      F[pad(t)] = cmul(F[pad(t)], w);
+      F[SF + pad(t)] = cmul(F[SF + pad(t)], w);
+    }
+    __syncthreads();
+  }
+
+  // ---- 4. nonlinear steps (dbp.py:394-398)
+  for (int st = 0; st < prm.n_steps; ++st) {
+    // subband IFFT (normalisation folded into the phasor)
+    fft<R, Q, Q, 2, NT, MAXRAD, true>(F, twQ, &s_zero);
+
+    // intensity I = |x|^2 + |y|^2 packed as H complex z[t] = I[2t] + i I[2t+1]
+    for (int t = tid; t < H; t += NT) {
+      const Cx<R> x0 = F[pad(2 * t)], x1 = F[pad(2 * t + 1)];
+      const Cx<R> y0 = F[SF + pad(2 * t)], y1 = F[SF + pad(2 * t + 1)];
+      const R i0 = x0.x * x0.x + x0.y * x0.y + (y0.x * y0.x + y0.y * y0.y);
+      const R i1 = x1.x * x1.x + x1.y * x1.y + (y1.x * y1.x + y1.y * y1.y);
+      IS[pad(t)] = mk(i0, i1);
+    }
+    __syncthreads();
+    fft<R, Q, H, 1, NT, MAXRAD, false>(IS, twQ, &s_zero);
+
+    // r2c untangle in place: I_hat[k], k = 0..H  (numpy rfft, dbp.py:194)
+    for (int k = tid; k <= H / 2; k += NT) {
+      if (k == 0) {
+        const Cx<R> z = IS[pad(0)];
+        IS[pad(0)] = mk(z.x + z.y, (R)0);
+        IS[pad(H)] = mk(z.x - z.y, (R)0);
+      } else {
+        const Cx<R> a = IS[pad(k)];
+        const Cx<R> bq = conj(IS[pad(H - k)]);
+        const Cx<R> e = scale(a + bq, (R)0.5);
+        const Cx<R> dd = a - bq;                           // 2i * O[k]
+        const Cx<R> o = mk(dd.y * (R)0.5, -dd.x * (R)0.5); // O[k]
+        const Cx<R> wo = cmul(o, ldg(twQ + k));
+        IS[pad(k)] = e + wo;
+        if (k != H - k) IS[pad(H - k)] = conj(e - wo);
+      }
+    }
+
+    // MIMO coupling (dbp.py:195): theta_hat_i[k] = sum_l T[i,l,k] I_hat_l[k]
+    if constexpr (P > 1) {
+      cg::cluster_group cluster = cg::this_cluster();
+      cluster.sync();
+      const int lo = (rank * (H + 1)) / P, hi = ((rank + 1) * (H + 1)) / P;
+      for (int k = lo + tid; k < hi; k += NT) {
+        Cx<R> iv[P], sv[P];
+#pragma unroll
+        for (int l = 0; l < P; ++l) {
+          const Cx<R>* ri = cluster.map_shared_rank(IS, l);
+          iv[l] = ri[pad(k)];
+          sv[l] = ldg(prm.mimo + (size_t)l * (H + 1) + k);
+        }
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          Cx<R> s = mk((R)0, (R)0);
+#pragma unroll
+          for (int l = 0; l < P; ++l) {
+            s = s + (l >= i ? cmul(sv[l - i], iv[l]) : cmul(conj(sv[i - l]), iv[l]));
+          }
+          Cx<R>* dst = cluster.map_shared_rank(TS, i);
+          dst[pad(k)] = s;
+        }
+      }
+      cluster.sync();
+    } else {
+      __syncthreads();
+      for (int k = tid; k <= H; k += NT) TS[pad(k)] = cmul(ldg(prm.mimo + k), IS[pad(k)]);
+      __syncthreads();
+    }
+
+    // c2r pre-twist in place (numpy irfft ignores Im of bins 0 and H)
+    for (int k = tid; k <= H / 2; k += NT) {
+      if (k == 0) {
+        const R x0 = TS[pad(0)].x, xh = TS[pad(H)].x;
+        TS[pad(0)] = mk(x0 + xh, x0 - xh);
+      } else {
+        const Cx<R> a = TS[pad(k)];                 // X[k]
+        const Cx<R> c = conj(TS[pad(H - k)]);       // X[k + H]
+        const Cx<R> wk = ldg(twQ + k);            // W^k, we need W^-k
+        const Cx<R> s = a + c;
+        const Cx<R> dd = cmulc(a - c, wk);          // W^-k (a - c)
+        TS[pad(k)] = mk(s.x - dd.y, s.y + dd.x);    // s + i dd
+        if (k != H - k) {
+          // Z[H-k] = (X[H-k] + X[Q-k]) + i W^{-(H-k)} (X[H-k] - X[Q-k])
+          //        = conj(s) + i * (conj(dd) * -1)... computed directly:
+          const Cx<R> a2 = conj(c);                 // X[H-k]
+          const Cx<R> c2 = conj(a);                 // X[Q-k]
+          const Cx<R> s2 = a2 + c2;
+          const Cx<R> w2 = mk(-wk.x, wk.y);         // W^{H-k} = -conj(W^k)
+          const Cx<R> d2 = cmulc(a2 - c2, w2);
+          TS[pad(H - k)] = mk(s2.x - d2.y, s2.y + d2.x);
+        }
+      }
+    }
+    __syncthreads();
+    fft<R, Q, H, 1, NT, MAXRAD, true>(TS, twQ, &s_zero);
+
+    // rotation exp(-i theta) of both polarisations (dbp.py:208)
+    {
+      const R tsc = prm.theta_scale[st];
+      for (int t = tid; t < H; t += NT) {
+        const Cx<R> z = TS[pad(t)];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const R th = (e ? z.y : z.x) * tsc;
+          R s, c;
+          sincos_acc<R>(th, &s, &c);
+          const Cx<R> rot = mk(c, -s);
+          const int ti = pad(2 * t + e);
+          F[ti] = cmul(F[ti], rot);
+          F[SF + ti] = cmul(F[SF + ti], rot);
+        }
+      }
+    }
+    __syncthreads();
+
+    // subband FFT, then the next dispersion stage (dbp.py:398, :395 / :399)
+    fft<R, Q, Q, 2, NT, MAXRAD, false>(F, twQ, &s_zero);
+    {
+      const Cx<R>* w1 = ph + (size_t)prm.ph_index[st + 1] * ph_tab;
+      for (int t = tid; t < Q; t += NT) {
+        const Cx<R> w = ldg(w1 + t);
+        F[pad(t)] = cmul(F[pad(t)], w);
+        F[SF + pad(t)] = cmul(F[SF + pad(t)], w);
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- 5. merge + outer IFFT (dbp.py:400-401): CTA c gathers, for k2 in
+  //         its slice, the P bins Q*k1 + k2 from their owners, applies the
+  //         inverse radix-P stage and the twiddle, and hands polyphase
+  //         component n1 to CTA n1 (staged as in step 3).
+  if constexpr (P > 1) {
+    cg::cluster_group cluster = cg::this_cluster();
+    const int lo = (rank * Q) / P, hi = ((rank + 1) * Q) / P;
+    Cx<R>* S = IS;
+    cluster.sync();
+    for (int pol = 0; pol < 2; ++pol) {
+      for (int k2 = lo + tid; k2 < hi; k2 += NT) {
+        Cx<R> xv[P];
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) {
+          int i, m;
+          bin_home<P, Q>(Q * k1 + k2, i, m);
+          const Cx<R>* rf = cluster.map_shared_rank(F, i);
+          xv[k1] = rf[pol * SF + pad(m)];
+        }
+#pragma unroll
+        for (int n1 = 0; n1 < P; ++n1) {
+          Cx<R> s = xv[0];
+#pragma unroll
+          for (int k1 = 1; k1 < P; ++k1) s = s + cmulc(xv[k1], ldg(twN + ((n1 * k1) % P) * Q));
+          if (n1) s = cmulc(s, ldg(twN + n1 * k2));
+          Cx<R>* dst = cluster.map_shared_rank(S, n1);
+          dst[pad(k2)] = s;
+        }
+      }
+      cluster.sync();
+      for (int t = tid; t < Q; t += NT) F[pol * SF + pad(t)] = S[pad(t)];
+      cluster.sync();
+    }
+  }
+  fft<R, Q, Q, 2, NT, MAXRAD, true>(F, twQ, &s_zero);
+
+  // ---- 6. keep proc[half : half + span] (dbp.py:476-477)
+  {
+    const int64_t span = min(prm.keep, n - b * prm.keep);
+    Cx<R>* dst = prm.out + wv * prm.out_bstride;
+    const int64_t obase = b * prm.keep - prm.half - prm.out_origin;
+    for (int t2 = tid; t2 < Q; t2 += NT) {
+      const int64_t t = rank + (int64_t)P * t2;
+      if (t >= prm.half && t < prm.half + span) {
+        dst[obase + t] = F[pad(t2)];
+        dst[prm.out_pstride + obase + t] = F[SF + pad(t2)];
+      }
+    }
+  }
+}
+
+}  // namespace cbessfm

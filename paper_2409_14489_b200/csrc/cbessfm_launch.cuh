@@ -1,0 +1,113 @@
+// Host-side launch helpers for the fused block kernel (cluster launch via
+// cudaLaunchKernelEx, dynamic shared memory opt-in, non-portable clusters).
+#pragma once
+
+#include "cbessfm_kernel.cuh"
+
+namespace cbessfm {
+
+struct KernelInfo {
+  int threads;
+  int cluster;
+  size_t smem;
+  int max_active_clusters;
+};
+
+template <typename R>
+constexpr int max_q() {
+  return sizeof(R) == 4 ? 8192 : 4096;
+}
+
+template <typename R, int P, int Q>
+cudaError_t launch_one(const Params<R>& prm, int64_t nclusters, cudaStream_t stream,
+                       KernelInfo* info) {
+  auto kern = cbessfm_block_kernel<R, P, Q>;
+  constexpr int NT = threads_for<R, Q>();
+  const size_t smem = smem_bytes<R, Q>(P);
+  // function attributes are per device; set them once per device
+  static unsigned long long configured = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(__atomic_load_n(&configured, __ATOMIC_ACQUIRE) & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    if (P > 8) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    __atomic_fetch_or(&configured, bit, __ATOMIC_RELEASE);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(NT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = P;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = P > 1 ? 1 : 0;
+  if (info) {
+    info->threads = NT;
+    info->cluster = P;
+    info->smem = smem;
+    cfg.gridDim = dim3(P, 1, 1);
+    int nc = 0;
+    if (P > 1) {
+      cudaError_t e = cudaOccupancyMaxActiveClusters(&nc, kern, &cfg);
+      if (e != cudaSuccess) return e;
+    } else {
+      int per_sm = 0;
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
+      if (e != cudaSuccess) return e;
+      int sms = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      nc = per_sm * sms;
+    }
+    info->max_active_clusters = nc;
+    if (nclusters == 0) return cudaSuccess;
+  }
+  // grid.x is limited to 2^31-1 CTAs: launch in chunks of whole clusters
+  const int64_t max_clusters = (int64_t)(0x7fffffff / P);
+  Params<R> p = prm;
+  for (int64_t c0 = 0; c0 < nclusters; c0 += max_clusters) {
+    const int64_t nc = nclusters - c0 < max_clusters ? nclusters - c0 : max_clusters;
+    p.cid0 = prm.cid0 + c0;
+    cfg.gridDim = dim3((unsigned)(nc * P), 1, 1);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+template <typename R, int P>
+cudaError_t launch_q(const Params<R>& prm, int q, int64_t nclusters, cudaStream_t stream,
+                     KernelInfo* info) {
+  switch (q) {
+    case 256: return launch_one<R, P, 256>(prm, nclusters, stream, info);
+    case 512: return launch_one<R, P, 512>(prm, nclusters, stream, info);
+    case 1024: return launch_one<R, P, 1024>(prm, nclusters, stream, info);
+    case 2048: return launch_one<R, P, 2048>(prm, nclusters, stream, info);
+    case 4096: return launch_one<R, P, 4096>(prm, nclusters, stream, info);
+    case 8192:
+      if constexpr (max_q<R>() >= 8192) return launch_one<R, P, 8192>(prm, nclusters, stream, info);
+      return cudaErrorInvalidValue;
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+#define CB_DECLARE(T, P)                                                                 \
+  cudaError_t launch_##T##_##P(const Params<T>& prm, int q, int64_t nclusters, cudaStream_t, \
+                               KernelInfo* info);
+#define CB_FOR_P(T) \
+  CB_DECLARE(T, 1) CB_DECLARE(T, 2) CB_DECLARE(T, 3) CB_DECLARE(T, 4) CB_DECLARE(T, 5) \
+  CB_DECLARE(T, 6) CB_DECLARE(T, 7) CB_DECLARE(T, 8) CB_DECLARE(T, 9)
+CB_FOR_P(float)
+CB_FOR_P(double)
+#undef CB_FOR_P
+#undef CB_DECLARE
+
+}  // namespace cbessfm

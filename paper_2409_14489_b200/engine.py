@@ -1,0 +1,269 @@
+"""Drop-in DBP entry points backed by the sm_100a kernel.
+
+``run_dbp`` keeps the reference signature and semantics
+(dbp.py:437-478): same validation and errors, same RuntimeWarning, same
+counter hooks, a fresh waveform of the input's class. The math runs in one
+fused kernel per launch (csrc/cbessfm_kernel.cuh) through the C ABI
+(include/cbessfm.h); torch only provides device memory and streams.
+
+``run_dbp_tensor`` is the device-resident entry: [B, 2, n] complex tensors
+in HBM in, [B, 2, n] out, optionally over a block range (time shards).
+"""
+
+from __future__ import annotations
+
+import threading
+import warnings
+from collections import OrderedDict
+
+import numpy as np
+
+from . import _native
+from .complexity import record_cb_blocks, record_time_domain_blocks
+from .config import DualPolWaveform, validate_config
+from .planner import BlockSchedule, EngineTables, build_tables, mimo_spectra
+
+_DTYPES = {"c64": _native.C64, "complex64": _native.C64,
+           "c128": _native.C128, "complex128": _native.C128}
+
+_plan_cache: "OrderedDict[tuple, _native.NativePlan]" = OrderedDict()
+_plan_lock = threading.Lock()
+_PLAN_CACHE_SIZE = 32
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def channel_memory_samples(link, bandwidth_hz: float, sample_rate_hz: float) -> int:
+    """Dispersive response length in samples (dbp.py:105-114)."""
+    spread = (2 * np.pi * abs(link.beta2_s2_km) * link.total_length_km
+              * bandwidth_hz)
+    return int(np.ceil(spread * sample_rate_hz))
+
+
+def gvd_step(spectrum: np.ndarray, freqs_hz: np.ndarray, delta_z_km: float,
+             beta2_ps2_km: float) -> np.ndarray:
+    """Dispersion-compensation phasor on a spectrum (dbp.py:117-125).
+    A host helper of the public API; the kernel applies the same phasor
+    from the uploaded tables."""
+    phase = 2 * np.pi ** 2 * beta2_ps2_km * 1e-24 * delta_z_km * freqs_hz ** 2
+    return spectrum * np.exp(1j * phase)
+
+
+class MimoTransfer:
+    """Per-bin coupling matrices of the nonlinear-phase filter
+    (dbp.py:128-149); ``matrix`` is (n_sb, n_sb, block_len//2 + 1)."""
+
+    def __init__(self, matrix: np.ndarray, block_len: int):
+        self.matrix = matrix
+        self.block_len = block_len
+
+    def validate(self):
+        n_sb = self.matrix.shape[0]
+        if self.matrix.shape != (n_sb, n_sb, self.block_len // 2 + 1):
+            raise ValueError("matrix shape inconsistent with block_len")
+        diag = self.matrix[np.arange(n_sb), np.arange(n_sb)]
+        peak = np.max(np.abs(diag)) or 1.0
+        if np.max(np.abs(diag.imag)) > 1e-10 * peak:
+            raise ValueError("diagonal transfer entries must be real")
+
+
+def build_mimo_transfer(coeffs, block_len: int) -> MimoTransfer:
+    """Full (n_sb, n_sb, bins) matrix from the kernel's spectra layout
+    (dbp.py:152-182)."""
+    spectra = mimo_spectra(coeffs, block_len)
+    n_sb = coeffs.n_sb
+    present = {int(h) for h in coeffs.coeffs}
+    m = np.zeros((n_sb, n_sb, block_len // 2 + 1), dtype=complex)
+    for i in range(n_sb):
+        for ell in range(n_sb):
+            h = ell - i
+            if abs(h) not in present:
+                continue
+            m[i, ell] = spectra[h] if h >= 0 else spectra[-h].conj()
+    out = MimoTransfer(m, block_len)
+    out.validate()
+    return out
+
+
+# ------------------------------------------------------------------ plans
+
+def _variant_geometry(cfg, coeffs):
+    """Map a variant onto the coupled-band pipeline: EDC is N_sb = 1 with
+    no steps and ESSFM/OSSFM are N_sb = 1 with the same taps
+    (pkg/tests/test_dbp.py:60-81 pins both identities to 1e-12)."""
+    if cfg.variant == "CB_ESSFM":
+        return cfg.n_subbands
+    if cfg.variant in ("EDC", "ESSFM", "OSSFM"):
+        return 1
+    raise NotImplementedError(
+        f"variant {cfg.variant!r} has no B200 path (the fine-step IDEAL_SSFM "
+        "oracle is out of the hot path's scope, SURVEY.md 2.1)")
+
+
+def get_plan(cfg, rate: float, coeffs, dtype: str = "c128",
+             device: int | None = None) -> _native.NativePlan:
+    """Build (or fetch from the cache) the uploaded plan for a config."""
+    if dtype not in _DTYPES:
+        raise ValueError(f"dtype must be one of {sorted(_DTYPES)}")
+    torch = _torch()
+    if device is None:
+        device = torch.cuda.current_device()
+    n_sb = _variant_geometry(cfg, coeffs)
+    tables = build_tables(cfg, rate, coeffs if cfg.n_steps else None, n_sb)
+    if not _native.supported(_DTYPES[dtype], n_sb, cfg.block_size):
+        raise ValueError(
+            f"no sm_100a kernel for n_subbands={n_sb}, "
+            f"N'={cfg.block_size // n_sb} ({dtype}); this build supports "
+            "1..9 subbands and power-of-two N' in [256, 4096] (c128) or "
+            "[256, 8192] (c64)")
+    key = (_DTYPES[dtype], int(device), tables.digest())
+    with _plan_lock:
+        plan = _plan_cache.get(key)
+        if plan is not None:
+            _plan_cache.move_to_end(key)
+            return plan
+    with torch.cuda.device(device):
+        plan = _native.NativePlan(
+            dtype=_DTYPES[dtype], n_subbands=n_sb, block_size=cfg.block_size,
+            overlap=cfg.overlap, n_steps=cfg.n_steps, phasors=tables.phasors,
+            phasor_index=tables.phasor_index, mimo=tables.mimo,
+            theta_scale=tables.theta_scale, device=int(device))
+    plan.tables = tables
+    with _plan_lock:
+        _plan_cache[key] = plan
+        while len(_plan_cache) > _PLAN_CACHE_SIZE:
+            _plan_cache.popitem(last=False)
+    return plan
+
+
+def launch(plan: _native.NativePlan, x, out, *, n: int | None = None,
+           block_range: tuple[int, int] | None = None, in_origin: int = 0,
+           out_origin: int = 0, stream=None) -> None:
+    """Enqueue the fused kernel on device tensors.
+
+    x: [B, 2, L_in] and out: [B, 2, L_out] complex tensors of the plan's
+    dtype on the plan's device; the last dim must be contiguous. n is the
+    circular period (default L_in)."""
+    torch = _torch()
+    want = torch.complex64 if plan.dtype == _native.C64 else torch.complex128
+    for name, t in (("input", x), ("output", out)):
+        if not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor")
+        if t.dtype != want:
+            raise ValueError(f"{name} dtype {t.dtype} does not match the plan ({want})")
+        if t.dim() != 3 or t.shape[1] != 2 or t.stride(2) != 1:
+            raise ValueError(f"{name} must be [B, 2, n] with a contiguous last dim")
+    if x.shape[0] != out.shape[0]:
+        raise ValueError("input and output batch differ")
+    n = x.shape[2] if n is None else n
+    sched = BlockSchedule(n, plan.block_size, plan.overlap)
+    b0, b1 = (0, sched.n_blocks) if block_range is None else block_range
+    if stream is None:
+        stream = torch.cuda.current_stream(x.device)
+    plan.run(in_ptr=x.data_ptr(), in_batch_stride=x.stride(0),
+             in_pol_stride=x.stride(1), in_origin=in_origin,
+             out_ptr=out.data_ptr(), out_batch_stride=out.stride(0),
+             out_pol_stride=out.stride(1), out_origin=out_origin, n=n,
+             batch=x.shape[0], block_begin=b0, block_end=b1,
+             stream=stream.cuda_stream)
+
+
+def run_dbp_tensor(x, cfg, coeffs, sample_rate: float, out=None,
+                   block_range: tuple[int, int] | None = None, stream=None):
+    """Device-resident CB-ESSFM over a batch: x [B, 2, n] complex64/128 CUDA
+    tensor (HBM), returns out [B, 2, n] (kept samples of block_range)."""
+    torch = _torch()
+    validate_config(cfg)
+    if x.dim() == 2:
+        x = x.unsqueeze(0)
+    dtype = "c64" if x.dtype == torch.complex64 else "c128"
+    if x.dtype not in (torch.complex64, torch.complex128):
+        raise ValueError("x must be complex64 or complex128")
+    n = x.shape[-1]
+    if cfg.block_size > n:
+        raise ValueError("block_size exceeds the sequence length")
+    plan = get_plan(cfg, sample_rate, coeffs, dtype, x.device.index)
+    if out is None:
+        out = torch.empty_like(x)
+    launch(plan, x, out, block_range=block_range, stream=stream)
+    return out
+
+
+def run_dbp(w, cfg, coeffs=None, counter=None, *, dtype: str = "c128",
+            device: int | None = None) -> DualPolWaveform:
+    """Backpropagate a waveform (drop-in for dbp.py:437-478).
+
+    Blockwise overlap-and-save on the GPU: blocks of block_size samples
+    advance by block_size - overlap, overlap/2 samples are discarded on each
+    side, the input is treated as circular. dtype "c128" (default) matches
+    the reference to ~1e-15; "c64" runs the FP32 kernel (tables still built
+    in FP64). Returns a new waveform of the input's class."""
+    torch = _torch()
+    w.require_finite()
+    validate_config(cfg)
+    n_sb = _variant_geometry(cfg, coeffs)
+    n = w.num_samples
+    if cfg.block_size > n:
+        raise ValueError("block_size exceeds the sequence length")
+    mem = channel_memory_samples(cfg.link, w.sample_rate, w.sample_rate)
+    if cfg.overlap < mem and cfg.block_size < n:
+        warnings.warn(
+            f"overlap {cfg.overlap} is below the channel memory (~{mem} "
+            "samples); blocks will leak dispersion across the discard zone",
+            RuntimeWarning)
+    plan = get_plan(cfg, w.sample_rate, coeffs if cfg.n_steps else None,
+                    dtype, device)
+    n_blocks = BlockSchedule(n, cfg.block_size, cfg.overlap).n_blocks
+    if cfg.variant == "CB_ESSFM":
+        record_cb_blocks(counter, cfg.block_size, cfg.n_steps, n_sb, n_blocks)
+    else:
+        taps = 1 if not cfg.n_steps else coeffs.coeffs[0].size
+        record_time_domain_blocks(counter, cfg.block_size, cfg.n_steps, taps,
+                                  cfg.variant == "EDC", n_blocks)
+    cdt = torch.complex64 if dtype in ("c64", "complex64") else torch.complex128
+    host = torch.from_numpy(np.stack([np.asarray(w.x), np.asarray(w.y)])[None])
+    dev = torch.device("cuda", plan.device)
+    x = host.to(dev, non_blocking=False).to(cdt)
+    out = torch.empty_like(x)
+    with torch.cuda.device(dev):
+        launch(plan, x, out)
+        res = out[0].to(torch.complex128).cpu().numpy()
+    return type(w)(res[0], res[1], w.sample_rate, w.center_freq)
+
+
+def nlpr_step(subbands, mimo: MimoTransfer, step_power_scale: float,
+              reference_power_w: float, counter=None):
+    """Nonlinear phase rotation across subband waveforms (dbp.py:211-230).
+
+    A host-side helper of the public API (the reference's tests call it on
+    256-sample lists); the hot path runs the same rotation inside the fused
+    kernel. Numpy FP64, identical formula (dbp.py:185-208)."""
+    n_prime = subbands[0].num_samples
+    if any(s.num_samples != n_prime for s in subbands):
+        raise ValueError("subbands must share their length")
+    if len(subbands) != mimo.matrix.shape[0] or n_prime != mimo.block_len:
+        raise ValueError("transfer matrix does not match the subband set")
+    fields = np.stack([[s.x for s in subbands], [s.y for s in subbands]])
+    scale = step_power_scale / reference_power_w
+    power = np.abs(fields[0]) ** 2 + np.abs(fields[1]) ** 2
+    theta = np.fft.irfft(np.einsum("ilk,lk->ik", mimo.matrix,
+                                   np.fft.rfft(power, axis=-1)),
+                         n=n_prime, axis=-1) * scale
+    if counter is not None:
+        n_sb = len(subbands)
+        total = n_sb * n_prime
+        counter.rmul(4 * total, "intensity")
+        counter.radd(3 * total, "intensity")
+        counter.rfft(n_prime, 2 * n_sb, "mimo")
+        counter.fixed_cmul(n_sb * (n_sb - 1) * n_prime / 2, "mimo")
+        counter.real_scale(n_sb * n_prime / 2, "mimo")
+        counter.cadd(n_sb * (n_sb - 1) * n_prime / 2, "mimo")
+        counter.lut_exp(total)
+        counter.pair_shared_cmul(total, "rotation")
+    fields = fields * np.exp(-1j * theta)[None]
+    cls = type(subbands[0])
+    return [cls(fields[0, i], fields[1, i], s.sample_rate, s.center_freq)
+            for i, s in enumerate(subbands)]

@@ -1,0 +1,105 @@
+"""Shared fixtures: golden-fixture loading and the parity metric.
+
+Markers: ``gpu`` tests need a B200 (run with ``-m gpu``); everything else runs
+on the CPU build container.
+"""
+
+from __future__ import annotations
+
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+GOLDEN = Path(__file__).resolve().parent / "golden"
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+from paper_2409_14489_b200 import (CoefficientSet, DbpConfig,  # noqa: E402
+                                   DualPolWaveform, LinkConfig)
+
+CASES = ("cfg1_nsb1", "cfg1_nsb3_st2", "cfg1_nsb9_st3", "cfg1_nsb2_frac",
+         "cfg1_nst0", "cfg2_nsb5", "cfg4_nsb5_st50")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA (B200) device")
+
+
+def rel_rms(a, b) -> float:
+    """pkg/tests/conftest.py:25-28 -- relative RMS deviation (= rel L2)."""
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return float(np.sqrt(np.mean(np.abs(a - b) ** 2) / np.mean(np.abs(b) ** 2)))
+
+
+class Golden:
+    """One reference run: input waveform, config, coefficients, output."""
+
+    def __init__(self, name: str):
+        d = np.load(GOLDEN / f"{name}.npz", allow_pickle=False)
+        self.name = name
+        self.data = d
+        wv = np.load(GOLDEN / f"wave_{str(d['wave'])}.npz")
+        self.wave = DualPolWaveform(wv["x"], wv["y"], float(wv["sample_rate"]),
+                                    float(wv["center_freq"]))
+        c = json.loads(str(d["cfg_json"]))
+        link = LinkConfig(num_spans=c["num_spans"],
+                          span_length_km=c["span_length_km"],
+                          alpha_db_per_km=c["alpha_db_per_km"],
+                          dispersion_d_ps_nm_km=c["dispersion_d_ps_nm_km"],
+                          gamma_w_km=c["gamma_w_km"])
+        fr = c["step_fractions"]
+        self.cfg = DbpConfig(link=link, variant=c["variant"],
+                             n_steps=c["n_steps"], n_subbands=c["n_subbands"],
+                             splitting_ratio=c["splitting_ratio"],
+                             block_size=c["block_size"], overlap=c["overlap"],
+                             oversampling=c["oversampling"],
+                             step_fractions=None if fr is None else tuple(fr))
+        self.coeffs = load_coeffs(d)
+        self.out = np.vstack([d["out_x"], d["out_y"]])
+
+    def extra(self, key):
+        return self.data[key]
+
+
+def load_coeffs(d):
+    if "c_n_sb" not in d.files:
+        return None
+    hs = [int(h) for h in d["c_hs"]]
+    return CoefficientSet(
+        n_sb=int(d["c_n_sb"]), subband_rate=float(d["c_subband_rate"]),
+        subband_spacing=float(d["c_subband_spacing"]),
+        reference_power_w=float(d["c_reference_power_w"]),
+        phase_norm_rad=float(d["c_phase_norm_rad"]),
+        step_scales=d["c_step_scales"],
+        geometry_hash=str(d["c_geometry_hash"]),
+        coeffs={h: d[f"c_tap_{h}"] for h in hs})
+
+
+_cache = {}
+
+
+def golden(name: str) -> Golden:
+    if name not in _cache:
+        _cache[name] = Golden(name)
+    return _cache[name]
+
+
+def gpu_available() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+@pytest.fixture(scope="session")
+def cuda():
+    if not gpu_available():
+        pytest.fail("GPU test selected but no CUDA device is visible")
+    import torch
+    return torch.device("cuda", 0)

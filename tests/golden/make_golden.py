@@ -1,0 +1,239 @@
+"""Generate the golden fixtures for the CB-ESSFM hot path from the REAL reference.
+
+Run in the build container (where /root/reference exists):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Each case stores the seeded, forward-propagated input waveform, the
+coefficient set the reference built for it, the DbpConfig fields and the
+reference ``run_dbp`` output (complex128). The GPU box has no reference tree,
+so these files are how parity is pinned there; ``tests/test_oracle_golden.py``
+checks the numpy restatement in ``oracle/`` against them and
+``tests/test_gpu_parity.py`` checks the CUDA path against them.
+
+Reference calls used (``/root/reference/pkg/src/fiberdbp``): generate_wdm
+(signals.py:204-257), propagate_link (channel.py:211-235),
+make_dbp_coefficient_set (dbp.py:239-269), run_dbp (dbp.py:437-478),
+prepare/symbols/snr (metrics.py:54-153).
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+import warnings
+from pathlib import Path
+
+import numpy as np
+
+import fiberdbp as fd
+
+HERE = Path(__file__).resolve().parent
+SSFM = fd.SimSettings(step_km=0.8, noise_enabled=False)  # 100 steps / span
+
+
+def link(spans):
+    return fd.LinkConfig(num_spans=spans, span_length_km=80.0,
+                         alpha_db_per_km=0.2, dispersion_d_ps_nm_km=17.0,
+                         gamma_w_km=1.3)
+
+
+def wave_single(nsym, seed=9, spans=15):
+    """BASELINE.json configs[0] layout at a small symbol count."""
+    wdm = fd.WdmConfig(64e9, 1, 0.0, 0.05, "16-qam", 2.0)
+    tx, rec = fd.generate_wdm(wdm, nsym, sim_rate=128e9, seed=seed)
+    rx = fd.propagate_link(tx, link(spans), SSFM)
+    return wdm, rx, rec
+
+
+def wave_wdm5(nsym, seed=11, spans=15, dbm=1.0):
+    """BASELINE.json configs[1] layout (5 x 64 GBd, 100 GHz, 512 GS/s)."""
+    wdm = fd.WdmConfig(64e9, 5, 100e9, 0.05, "16-qam", dbm)
+    tx, rec = fd.generate_wdm(wdm, nsym, sim_rate=512e9, seed=seed)
+    rx = fd.propagate_link(tx, link(spans), SSFM)
+    return wdm, rx, rec
+
+
+def coeff_arrays(c):
+    if c is None:
+        return {}
+    d = {"c_n_sb": c.n_sb, "c_subband_rate": c.subband_rate,
+         "c_subband_spacing": c.subband_spacing,
+         "c_reference_power_w": c.reference_power_w,
+         "c_phase_norm_rad": c.phase_norm_rad,
+         "c_step_scales": c.step_scales,
+         "c_geometry_hash": c.geometry_hash,
+         "c_hs": np.array(sorted(c.coeffs))}
+    for h, v in c.coeffs.items():
+        d[f"c_tap_{h}"] = v
+    return d
+
+
+_WAVES = {}
+
+
+def save_wave(tag, w):
+    """Inputs are stored once per waveform and shared by the cases."""
+    if tag not in _WAVES:
+        np.savez_compressed(HERE / f"wave_{tag}.npz", x=w.x, y=w.y,
+                            sample_rate=w.sample_rate,
+                            center_freq=w.center_freq)
+        _WAVES[tag] = True
+        print(f"  wrote wave_{tag}.npz", flush=True)
+    return tag
+
+
+def save_case(name, w, cfg, coeffs, out, extra=None, wave=None):
+    cfgd = dict(num_spans=cfg.link.num_spans,
+                span_length_km=cfg.link.span_length_km,
+                alpha_db_per_km=cfg.link.alpha_db_per_km,
+                dispersion_d_ps_nm_km=cfg.link.dispersion_d_ps_nm_km,
+                gamma_w_km=cfg.link.gamma_w_km,
+                variant=cfg.variant, n_steps=cfg.n_steps,
+                n_subbands=cfg.n_subbands,
+                splitting_ratio=cfg.splitting_ratio,
+                block_size=cfg.block_size, overlap=cfg.overlap,
+                oversampling=cfg.oversampling,
+                step_fractions=(None if cfg.step_fractions is None
+                                else list(cfg.step_fractions)))
+    arrays = dict(wave=save_wave(wave, w), sample_rate=w.sample_rate,
+                  out_x=out.x, out_y=out.y,
+                  cfg_json=json.dumps(cfgd))
+    arrays.update(coeff_arrays(coeffs))
+    if extra:
+        arrays.update(extra)
+    np.savez_compressed(HERE / f"{name}.npz", **arrays)
+    print(f"  wrote {name}.npz", flush=True)
+
+
+def run(w, cfg, coeffs):
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        return fd.run_dbp(w, cfg, coeffs)
+
+
+def coeffs_for(cfg, rate, p_ref, memory):
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        return fd.make_dbp_coefficient_set(cfg, rate, p_ref, memory=memory)
+
+
+def main():
+    t0 = time.time()
+    only = set(sys.argv[1:])
+
+    def want(name):
+        return not only or name in only
+
+    # --- config-1 layout (single channel, 2 sps, 15 x 80 km), n = 8192
+    wdm1, w1, rec1 = wave_single(4096)
+    rate1 = w1.sample_rate
+    p1 = wdm1.launch_power_w
+
+    if want("cfg1_nsb1"):
+        cfg = fd.DbpConfig(link=link(15), variant="CB_ESSFM", n_steps=1,
+                           n_subbands=1, splitting_ratio=0.5, block_size=4096,
+                           overlap=2680, oversampling=2.0)
+        c = coeffs_for(cfg, rate1, p1, 255)
+        out = run(w1, cfg, c)
+        es_cfg = fd.DbpConfig(link=link(15), variant="ESSFM", n_steps=1,
+                              n_subbands=1, splitting_ratio=0.5,
+                              block_size=4096, overlap=2680, oversampling=2.0)
+        es = run(w1, es_cfg, c)
+        sym = fd.symbols_from_dbp_output(out, wdm1)
+        s = fd.snr(sym, rec1.channel(0)).snr_db
+        save_case("cfg1_nsb1", w1, cfg, c, out, wave="cfg1", extra=dict(
+            essfm_x=es.x, essfm_y=es.y, tx_symbols=rec1.channel(0),
+            snr_db=s, baud=wdm1.baud_rate, rolloff=wdm1.rolloff,
+            launch_power_w=p1, channel_freq=0.0, channel_bw=0.0))
+
+    if want("cfg1_nsb3_st2"):
+        cfg = fd.DbpConfig(link=link(15), variant="CB_ESSFM", n_steps=2,
+                           n_subbands=3, splitting_ratio=0.7, block_size=1536,
+                           overlap=1344, oversampling=2.0)
+        c = coeffs_for(cfg, rate1, p1, 15)
+        save_case("cfg1_nsb3_st2", w1, cfg, c, run(w1, cfg, c), wave="cfg1")
+
+    if want("cfg1_nsb9_st3"):
+        cfg = fd.DbpConfig(link=link(15), variant="CB_ESSFM", n_steps=3,
+                           n_subbands=9, splitting_ratio=1.0, block_size=4608,
+                           overlap=900, oversampling=2.0)
+        c = coeffs_for(cfg, rate1, p1, 7)
+        save_case("cfg1_nsb9_st3", w1, cfg, c, run(w1, cfg, c), wave="cfg1")
+
+    if want("cfg1_nsb2_frac"):
+        cfg = fd.DbpConfig(link=link(15), variant="CB_ESSFM", n_steps=3,
+                           n_subbands=2, splitting_ratio=0.0, block_size=2048,
+                           overlap=1000, oversampling=2.0,
+                           step_fractions=(0.5, 0.3, 0.2))
+        c = coeffs_for(cfg, rate1, p1, 20)
+        save_case("cfg1_nsb2_frac", w1, cfg, c, run(w1, cfg, c), wave="cfg1")
+
+    if want("cfg1_nst0"):
+        cfg = fd.DbpConfig(link=link(15), variant="CB_ESSFM", n_steps=0,
+                           n_subbands=2, splitting_ratio=0.5, block_size=4096,
+                           overlap=2680, oversampling=2.0)
+        out = run(w1, cfg, None)
+        edc = run(w1, fd.DbpConfig(link=link(15), variant="EDC", n_steps=0,
+                                   block_size=4096, overlap=2680,
+                                   oversampling=2.0), None)
+        save_case("cfg1_nst0", w1, cfg, None, out, wave="cfg1",
+                  extra=dict(edc_x=edc.x, edc_y=edc.y))
+
+    # --- config-2 layout (5 x 64 GBd, 512 GS/s), n = 16384
+    if want("cfg2_nsb5"):
+        wdm2, w2, rec2 = wave_wdm5(2048)
+        rate2 = w2.sample_rate
+        cfg = fd.DbpConfig(link=link(15), variant="CB_ESSFM", n_steps=15,
+                           n_subbands=5, splitting_ratio=0.12,
+                           block_size=10240, overlap=2860, oversampling=1.6)
+        c = coeffs_for(cfg, rate2, wdm2.launch_power_w, 15)
+        out = run(w2, cfg, c)
+        # centre-channel SNR after whole-band DBP
+        ch = fd.demux_channel(out, 0.0, 100e9)
+        sym = fd.symbols_from_dbp_output(ch, wdm2)
+        s = fd.snr(sym, rec2.channel(2)).snr_db
+        save_case("cfg2_nsb5", w2, cfg, c, out, wave="cfg2", extra=dict(
+            tx_symbols=rec2.channel(2), snr_db=s, baud=wdm2.baud_rate,
+            rolloff=wdm2.rolloff, launch_power_w=wdm2.launch_power_w,
+            channel_freq=0.0, channel_bw=100e9))
+
+    # --- config-4 layout (50 x 80 km), N' = 4096, 50 steps, n = 32768
+    if want("cfg4_nsb5_st50"):
+        wdm4, w4, _ = wave_wdm5(4096, seed=13, spans=50)
+        cfg = fd.DbpConfig(link=link(50), variant="CB_ESSFM", n_steps=50,
+                           n_subbands=5, splitting_ratio=0.12,
+                           block_size=20480, overlap=2860, oversampling=1.6)
+        c = coeffs_for(cfg, w4.sample_rate, wdm4.launch_power_w, 15)
+        save_case("cfg4_nsb5_st50", w4, cfg, c, run(w4, cfg, c),
+                  wave="cfg4")
+
+    # --- reference KAT inputs: nlpr direct formula (test_dbp.py:143-169)
+    if want("nlpr_kat"):
+        lk = fd.LinkConfig(num_spans=3, span_length_km=80.0)
+        cfg = fd.DbpConfig(link=lk, n_steps=3, block_size=4096, overlap=1024,
+                           oversampling=2.0, variant="CB_ESSFM", n_subbands=2)
+        c = fd.make_dbp_coefficient_set(cfg, 64e9, 1e-3)
+        rng = np.random.default_rng(5)
+        n_prime = 256
+        subs = [fd.DualPolWaveform(rng.normal(size=n_prime) * 0.03 + 0j,
+                                   rng.normal(size=n_prime) * 0.03 + 0j,
+                                   32e9, 0.0) for _ in range(2)]
+        got = fd.nlpr_step(subs, fd.build_mimo_transfer(c, n_prime), 1.0,
+                           1e-3)
+        arr = coeff_arrays(c)
+        arr.update(sx=np.stack([s.x for s in subs]),
+                   sy=np.stack([s.y for s in subs]),
+                   gx=np.stack([g.x for g in got]),
+                   gy=np.stack([g.y for g in got]),
+                   mimo=fd.build_mimo_transfer(c, n_prime).matrix)
+        np.savez_compressed(HERE / "nlpr_kat.npz", **arr)
+        print("  wrote nlpr_kat.npz")
+
+    print(f"done in {time.time() - t0:.1f} s")
+
+
+if __name__ == "__main__":
+    main()

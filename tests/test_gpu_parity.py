@@ -1,0 +1,164 @@
+"""Parity of the sm_100a path (through the C ABI) with the reference.
+
+Bars (BASELINE.json north_star): relative L2 <= 1e-12 in complex128 and
+<= 1e-5 in complex64, both against the reference's complex128 output, and
+post-DBP SNR within 0.01 dB. Fixed cases come from the real reference
+(tests/golden); larger seeded cases are checked against the numpy oracle.
+"""
+
+import warnings
+
+import numpy as np
+import pytest
+
+from conftest import CASES, golden, rel_rms
+from oracle import cbessfm_oracle as orc
+
+import paper_2409_14489_b200 as pb
+from paper_2409_14489_b200.synth import gaussian_wdm
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"c128": 1e-12, "c64": 1e-5}
+
+
+def _run(g, dtype, **kw):
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        out = pb.run_dbp(g.wave, g.cfg, g.coeffs, dtype=dtype, **kw)
+    return np.vstack([out.x, out.y])
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("name", CASES)
+def test_golden_parity(cuda, name, dtype):
+    g = golden(name)
+    err = rel_rms(_run(g, dtype), g.out)
+    assert err < TOL[dtype], f"{name} {dtype}: rel L2 {err:.3e}"
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_single_band_equals_essfm(cuda, dtype):
+    # pkg/tests/test_dbp.py:60-64, against the reference ESSFM output
+    g = golden("cfg1_nsb1")
+    es = np.vstack([g.extra("essfm_x"), g.extra("essfm_y")])
+    assert rel_rms(_run(g, dtype), es) < TOL[dtype]
+
+
+def test_essfm_and_edc_variants_run_on_gpu(cuda):
+    from dataclasses import replace
+    g = golden("cfg1_nsb1")
+    es = np.vstack([g.extra("essfm_x"), g.extra("essfm_y")])
+    cfg = replace(g.cfg, variant="ESSFM")
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        out = pb.run_dbp(g.wave, cfg, g.coeffs)
+    assert rel_rms(np.vstack([out.x, out.y]), es) < 1e-12
+    g0 = golden("cfg1_nst0")
+    edc = np.vstack([g0.extra("edc_x"), g0.extra("edc_y")])
+    ecfg = replace(g0.cfg, variant="EDC", n_subbands=1)
+    out = pb.run_dbp(g0.wave, ecfg, None)
+    assert rel_rms(np.vstack([out.x, out.y]), edc) < 1e-12
+    # zero-step CB with 2 subbands == EDC (test_dbp.py:75-81)
+    assert rel_rms(_run(g0, "c128"), edc) < 1e-12
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("name", ["cfg1_nsb1", "cfg2_nsb5"])
+def test_post_dbp_snr_within_0p01_db(cuda, name, dtype):
+    g = golden(name)
+    out = _run(g, dtype)
+    rate = g.wave.sample_rate
+    if float(g.extra("channel_bw")) > 0:
+        out, rate = orc.demux(out, rate, float(g.extra("channel_freq")),
+                              float(g.extra("channel_bw")))
+    sym = orc.symbols_from_output(out, rate, float(g.extra("baud")),
+                                  float(g.extra("rolloff")),
+                                  float(g.extra("launch_power_w")))
+    s = orc.snr_db(sym, g.extra("tx_symbols"))
+    assert abs(s - float(g.extra("snr_db"))) < 0.01
+
+
+def test_full_size_config2_against_oracle(cuda):
+    # BASELINE.json configs[1] sizes: n = 2^20, N' = 2048, 5 subbands, 15 steps
+    import torch
+    g = golden("cfg2_nsb5")      # reuse its coefficient set (same geometry)
+    rate = g.wave.sample_rate
+    field = gaussian_wdm(1 << 20, rate, seed=7)
+    ref = orc.run_cb_blocks(field, g.cfg, rate, g.coeffs)
+    for dtype, ct in (("c128", torch.complex128), ("c64", torch.complex64)):
+        x = torch.from_numpy(field[None]).to(cuda).to(ct)
+        out = pb.run_dbp_tensor(x, g.cfg, g.coeffs, rate)
+        got = out[0].to(torch.complex128).cpu().numpy()
+        assert rel_rms(got, ref) < TOL[dtype], dtype
+
+
+def test_batch_and_block_ranges_are_independent(cuda):
+    import torch
+    g = golden("cfg1_nsb3_st2")
+    rate = g.wave.sample_rate
+    f0 = np.vstack([g.wave.x, g.wave.y])
+    f1 = gaussian_wdm(f0.shape[-1], rate, n_channels=1, spacing=0.0, seed=3)
+    x = torch.from_numpy(np.stack([f0, f1])).to(cuda)
+    whole = pb.run_dbp_tensor(x, g.cfg, g.coeffs, rate)
+    sched = pb.BlockSchedule(f0.shape[-1], g.cfg.block_size, g.cfg.overlap)
+    parts = torch.zeros_like(x)
+    cut = sched.n_blocks // 3
+    for rng in ((0, cut), (cut, sched.n_blocks)):
+        pb.run_dbp_tensor(x, g.cfg, g.coeffs, rate, out=parts, block_range=rng)
+    assert torch.equal(parts, whole)
+    for b, f in enumerate((f0, f1)):
+        ref = orc.run_cb_blocks(f, g.cfg, rate, g.coeffs)
+        assert rel_rms(whole[b].cpu().numpy(), ref) < 1e-12
+
+
+def test_time_shard_with_halo_slice(cuda):
+    # a shard uploads only its halo'd input slice
+    import torch
+    from paper_2409_14489_b200.planner import gather_slice
+    g = golden("cfg2_nsb5")
+    rate = g.wave.sample_rate
+    field = np.vstack([g.wave.x, g.wave.y])
+    n = field.shape[-1]
+    sched = pb.BlockSchedule(n, g.cfg.block_size, g.cfg.overlap)
+    plan = pb.get_plan(g.cfg, rate, g.coeffs, "c128")
+    out = np.zeros_like(field)
+    for b0, b1 in ((0, 1), (1, sched.n_blocks)):
+        origin, length = sched.input_range(b0, b1)
+        sl = torch.from_numpy(gather_slice(field, origin, length)[None]).to(cuda)
+        o0, o1 = sched.output_range(b0, b1)
+        dst = torch.zeros((1, 2, o1 - o0), dtype=torch.complex128, device=cuda)
+        pb.launch(plan, sl, dst, n=n, block_range=(b0, b1), in_origin=origin,
+                  out_origin=o0)
+        out[:, o0:o1] = dst[0].cpu().numpy()
+    assert rel_rms(out, g.out) < 1e-12
+
+
+def test_errors_match_reference(cuda):
+    g = golden("cfg1_nsb1")
+    from dataclasses import replace
+    with pytest.raises(ValueError):          # dbp.py:458-459
+        pb.run_dbp(g.wave, replace(g.cfg, block_size=16384, overlap=0), g.coeffs)
+    with pytest.raises(ValueError):          # dbp.py:339-340
+        pb.run_dbp(g.wave, g.cfg, None)
+    with pytest.warns(RuntimeWarning):       # dbp.py:461-465
+        pb.run_dbp(g.wave, replace(g.cfg, overlap=16), g.coeffs)
+    bad = pb.DualPolWaveform(g.wave.x.copy(), g.wave.y, g.wave.sample_rate)
+    bad.x[3] = np.nan
+    with pytest.raises(ValueError):          # dbp.py:449
+        pb.run_dbp(bad, g.cfg, g.coeffs)
+    with pytest.raises(ValueError):          # unsupported N' is loud, no fallback
+        pb.run_dbp(g.wave, replace(g.cfg, block_size=3000, overlap=0), g.coeffs)
+
+
+def test_counter_hook_matches_reference_cost(cuda):
+    # pkg/tests/test_complexity.py:111-121: partial-tile overshoot < 1 %
+    g = golden("cfg2_nsb5")
+    c = pb.CostCounter()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        pb.run_dbp(g.wave, g.cfg, g.coeffs, counter=c)
+    rep = c.as_report(g.wave.num_samples, g.cfg.oversampling)
+    closed = pb.cb_essfm_cost(g.cfg.block_size, g.cfg.overlap,
+                              g.cfg.oversampling, g.cfg.n_steps, 5)
+    assert rep.rm_per_2d >= closed.rm_per_2d

@@ -1,0 +1,198 @@
+"""Host-side logic that needs no GPU: config invariants, block scheduler,
+engine tables, shard planner, cost model, kernel addressing identity, and
+the C ABI library (loads, exports every symbol include/cbessfm.h declares)."""
+
+import re
+import warnings
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import CASES, ROOT, golden
+from oracle import cbessfm_oracle as orc
+from paper_2409_14489_b200 import (BlockSchedule, CostCounter, DbpConfig,
+                                   LinkConfig, build_mimo_transfer,
+                                   build_tables, cb_essfm_cost,
+                                   channel_memory_samples,
+                                   essfm_time_domain_cost, plan_shards)
+from paper_2409_14489_b200 import _native
+from paper_2409_14489_b200.complexity import record_cb_blocks
+from paper_2409_14489_b200.planner import gather_slice, subband_frequencies
+
+LINK = LinkConfig(num_spans=3, span_length_km=80.0)
+
+
+def test_config_invariants():
+    # pkg/tests/test_dbp.py:45-57
+    with pytest.raises(ValueError):
+        DbpConfig(link=LINK, variant="EDC", n_steps=2)
+    with pytest.raises(ValueError):
+        DbpConfig(link=LINK, variant="OSSFM", n_subbands=2)
+    with pytest.raises(ValueError):
+        DbpConfig(link=LINK, block_size=1024, overlap=1024)
+    with pytest.raises(ValueError):
+        DbpConfig(link=LINK, n_subbands=3, block_size=1024)
+    with pytest.raises(ValueError):
+        DbpConfig(link=LINK, n_subbands=2, block_size=1024, overlap=30)
+    with pytest.raises(ValueError):
+        DbpConfig(link=LINK, splitting_ratio=1.5)
+    with pytest.raises(ValueError):
+        DbpConfig(link=LINK, n_steps=2, step_fractions=(0.5, 0.6))
+
+
+def test_link_beta2_bit_identical_to_oracle():
+    for d in (16.0, 17.0, 21.3):
+        lk = LinkConfig(num_spans=2, span_length_km=50.0, dispersion_d_ps_nm_km=d)
+        assert lk.beta2_ps2_km == orc.beta2_ps2_km(d)
+
+
+def test_channel_memory():
+    # pkg/tests/test_dbp.py:200-205 and SURVEY Appendix A values
+    m1 = channel_memory_samples(LINK, 36e9, 64e9)
+    m2 = channel_memory_samples(LinkConfig(num_spans=6, span_length_km=80.0), 36e9, 64e9)
+    assert abs(m2 - 2 * m1) <= 1 and m1 > 0
+    l15 = LinkConfig(num_spans=15, span_length_km=80.0, gamma_w_km=1.3)
+    assert channel_memory_samples(l15, 128e9, 128e9) == 2679
+    assert channel_memory_samples(l15, 512e9, 512e9) == 42857
+
+
+@pytest.mark.parametrize("n,N,ov", [(8192, 4096, 2680), (16384, 10240, 2860),
+                                    (1 << 20, 10240, 2860), (1000, 1000, 0),
+                                    (4096, 1024, 512)])
+def test_block_schedule_matches_reference_framing(n, N, ov):
+    s = BlockSchedule(n, N, ov)
+    keep, half, nb = orc.block_schedule(n, N, ov)
+    assert (s.keep, s.half, s.n_blocks) == (keep, half, nb)
+    assert s.n_blocks == _native.num_blocks(n, N, ov)
+    covered = np.zeros(n, int)
+    for b in range(nb):
+        assert s.window_start(b) == (b * keep - half) % n
+        covered[b * keep: b * keep + s.span(b)] += 1
+    assert np.all(covered == 1)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_tables_bit_identical_to_oracle(name):
+    g = golden(name)
+    t = build_tables(g.cfg, g.wave.sample_rate, g.coeffs)
+    proc = orc.BlockProcessor(g.cfg, g.wave.sample_rate, g.coeffs)
+    stages = proc.before + [proc.final]
+    assert t.stage_lengths_km == stages
+    for a, dz in enumerate(stages):
+        # the kernel table is the reference phasor scaled by the exact 1/Q
+        assert np.array_equal(t.phasors[t.phasor_index[a]] * t.q, proc.ph[dz])
+    if g.cfg.n_steps:
+        T = orc.mimo_matrix(g.coeffs, t.q)
+        n_sb = g.cfg.n_subbands
+        for i in range(n_sb):
+            for ell in range(n_sb):
+                h = ell - i
+                want = t.mimo[h] if h >= 0 else t.mimo[-h].conj()
+                assert np.array_equal(want, T[i, ell])
+        assert np.allclose(t.theta_scale * t.q, proc.scales, rtol=1e-15)
+
+
+def test_build_mimo_transfer_structure():
+    g = golden("cfg1_nsb2_frac")
+    m = build_mimo_transfer(g.coeffs, 128)
+    assert m.matrix.shape == (2, 2, 65)
+    assert np.allclose(m.matrix[0, 1], np.conj(m.matrix[1, 0]))
+    assert np.abs(m.matrix[0, 0].imag).max() < 1e-12 * np.abs(m.matrix[0, 0]).max()
+
+
+def test_subband_frequency_layout():
+    # subband i, stored bin m <-> global bin (i Q + (m + Q/2) mod Q - N/2) mod N
+    rate, n_sb, q = 512e9, 5, 64
+    n = n_sb * q
+    f = subband_frequencies(rate, n_sb, q)
+    g_freq = np.fft.fftfreq(n, 1.0 / rate)
+    for i in range(n_sb):
+        for m in range(q):
+            g = (i * q + (m + q // 2) % q - n // 2) % n
+            assert abs(f[i, m] - g_freq[g]) < 1e-3
+
+
+def test_pad_identity_used_by_kernel_addressing():
+    # csrc/cbessfm_kernel.cuh: pad(a + b) == pad(a) + pad(b) for every index
+    # pair a Stockham pass forms (one pad slot per 16 complex entries)
+    pad = lambda i: i + (i >> 4)
+    for L in (128, 256, 512, 1024, 2048, 4096, 8192):
+        ns = 1
+        while ns < L:
+            R = min(8, L // ns)
+            j = np.arange(L // R)
+            k = j % ns
+            d0 = (j // ns) * ns * R + k
+            for r in range(R):
+                assert np.all(pad(d0 + r * ns) == pad(d0) + pad(r * ns))
+                assert np.all(pad(j + r * (L // R)) == pad(j) + pad(r * (L // R)))
+            ns *= R
+
+
+@pytest.mark.parametrize("batch,nblk,world", [(1, 143, 8), (64, 1137, 8),
+                                              (3, 10, 8), (8, 5, 8), (2, 7, 2),
+                                              (1, 1, 4), (5, 3, 3)])
+def test_shard_planner_covers_schedule_once(batch, nblk, world):
+    shards = plan_shards(batch, nblk, world)
+    cover = np.zeros((batch, nblk), int)
+    for s in shards:
+        w0, w1 = s.waveforms
+        b0, b1 = s.blocks
+        cover[w0:w1, b0:b1] += 1
+    assert np.all(cover == 1)
+
+
+def test_shard_input_slice_contains_every_window():
+    s = BlockSchedule(16384, 10240, 2860)
+    x = np.arange(16384)
+    for b0, b1 in ((0, 1), (1, 3), (0, s.n_blocks), (2, 3)):
+        origin, length = s.input_range(b0, b1)
+        sl = gather_slice(x, origin, length)
+        for b in range(b0, b1):
+            win = (s.window_start(b) + np.arange(10240)) % 16384
+            loc = (win - origin) % 16384
+            assert np.all(loc < length)
+            assert np.array_equal(sl[loc], x[win])
+
+
+def test_cost_golden_values():
+    # pkg/tests/test_complexity.py:15-18
+    assert round(cb_essfm_cost(16384, 1800, 1.125, 15, 2).rm_per_2d) == 681
+    assert round(cb_essfm_cost(16384, 1800, 1.125, 1, 2).rm_per_2d) == 75
+    assert round(essfm_time_domain_cost(16384, 1800, 1.125, 0).rm_per_2d) == 32
+    assert cb_essfm_cost(10240, 2860, 1.6, 15, 5).rm_per_2d == pytest.approx(1101.6, abs=0.1)
+
+
+def test_counter_matches_closed_form_on_exact_tiling():
+    # pkg/tests/test_complexity.py:90-108: whole-block tiling
+    N, ov, st, sb = 4096, 1024, 3, 2
+    nblk = 8
+    c = CostCounter()
+    record_cb_blocks(c, N, st, sb, nblk)
+    rep = c.as_report(nblk * (N - ov), 2.0)
+    ref = cb_essfm_cost(N, ov, 2.0, st, sb)
+    assert rep.rm_per_2d == pytest.approx(ref.rm_per_2d, rel=1e-12)
+    assert rep.ra_per_2d == pytest.approx(ref.ra_per_2d, rel=1e-12)
+    assert list(rep.breakdown) == ["outer_fft", "gvd", "subband_fft",
+                                   "intensity", "mimo", "exp_lut", "rotation"]
+
+
+def test_native_library_exports_every_header_symbol():
+    header = (ROOT / "include" / "cbessfm.h").read_text()
+    declared = set(re.findall(r"\b(cbessfm_[a-z_]+)\s*\(", header))
+    lib = _native.load()
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(_native.SIGNATURES)
+    assert lib.cbessfm_version() == 1
+    assert lib.cbessfm_supported(0, 5, 10240) == 1
+    assert lib.cbessfm_supported(1, 5, 10240 * 4) == 0
+    assert lib.cbessfm_supported(0, 3, 3000) == 0
+
+
+def test_oracle_is_not_imported_by_the_product():
+    pkg = ROOT / "paper_2409_14489_b200"
+    for f in pkg.rglob("*.py"):
+        assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)",
+                                          f.read_text(), re.M), f
