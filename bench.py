@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""CB-ESSFM DBP throughput benchmark (BASELINE.json metric, configs[1]).
+
+Workload (per GPU, weak scaling): BASELINE.json configs[1] -- one 5-channel
+WDM waveform at 512 GS/s, 2^17 symbols per channel (n = 2^20 samples per
+polarisation), CB-ESSFM with 5 subbands, 15 steps, rho = 0.12, N' = 2048
+(N = 10240, N_ov = 2860), 31-tap filters (coefficient set built by the
+reference for exactly this geometry, tests/golden/cfg2_nsb5.npz). Input is
+seeded band-limited Gaussian WDM (synthetic, same shape and spectrum as the
+forward-propagated config; throughput does not depend on content). One step
+= one backpropagation of every waveform on this rank.
+
+  python bench.py [--gpus N --steps K --warmup W --dtype c64|c128 --batch B]
+  python bench.py --impl reference ...   (reference CPU path: the oracle port)
+
+Prints one JSON line (rank 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "CB-ESSFM DBP throughput (2D symbols/s) at 1/2/4/8 B200; % of roofline"
+UNIT = "2D symbols/s"
+RATE = 512e9
+N_SAMPLES = 1 << 20
+SYMBOLS_PER_WAVE = 5 * 2 * (1 << 17)      # channels x polarisations x symbols
+SPS_EFF = RATE / (5 * 64e9)               # samples per 2D symbol per pol = 1.6
+
+
+def workload_cfg():
+    from paper_2409_14489_b200 import DbpConfig, LinkConfig
+    from paper_2409_14489_b200.config import load_coefficients_npz
+    link = LinkConfig(num_spans=15, span_length_km=80.0, alpha_db_per_km=0.2,
+                      dispersion_d_ps_nm_km=17.0, gamma_w_km=1.3)
+    cfg = DbpConfig(link=link, variant="CB_ESSFM", n_steps=15, n_subbands=5,
+                    splitting_ratio=0.12, block_size=10240, overlap=2860,
+                    oversampling=SPS_EFF)
+    coeffs = load_coefficients_npz(ROOT / "tests" / "golden" / "cfg2_nsb5.npz")
+    return cfg, coeffs
+
+
+def config_block(args, world):
+    return {"workload": "BASELINE configs[1]: 5x64 GBd WDM @ 512 GS/s, 2^17 sym/ch, "
+                        "CB-ESSFM N_sb=5, N_st=15, rho=0.12, N'=2048 (N=10240, N_ov=2860), "
+                        "31-tap MIMO",
+            "n_samples_per_pol": N_SAMPLES, "waveforms_per_gpu": args.batch,
+            "two_d_symbols_per_waveform": SYMBOLS_PER_WAVE,
+            "parallelism": f"waveform-parallel x{world} (no collective in the step loop)",
+            "l2": "flushed (256 MiB write) between timed steps"}
+
+
+# ------------------------------------------------------------ CPU legs
+
+def _oracle_worker(args):
+    """One process: the numpy oracle over blocks [b0, b1) of a waveform."""
+    os.environ["OMP_NUM_THREADS"] = "1"
+    b0, b1, seed = args
+    import numpy as np
+    from oracle import cbessfm_oracle as orc        # checker / CPU baseline only
+    from paper_2409_14489_b200.synth import gaussian_wdm
+    cfg, coeffs = workload_cfg()
+    field = gaussian_wdm(N_SAMPLES, RATE, seed=seed)
+    t0 = time.perf_counter()
+    orc.run_cb_blocks(field, cfg, RATE, coeffs, b0, b1)
+    return time.perf_counter() - t0
+
+
+def _cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(max_procs: int | None = None) -> dict:
+    """The oracle port on the host cores: P concurrent processes, each one
+    full configs[1] waveform (143 blocks); aggregate 2D symbols/s."""
+    import multiprocessing as mp
+    from paper_2409_14489_b200.planner import BlockSchedule
+    cores = _cores() if max_procs is None else min(max_procs, _cores())
+    nb = BlockSchedule(N_SAMPLES, 10240, 2860).n_blocks
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(cores) as pool:
+        pool.map(_oracle_worker, [(0, 1, 0)] * cores)           # warm imports
+        t0 = time.perf_counter()
+        pool.map(_oracle_worker, [(0, nb, i) for i in range(cores)])
+        wall = time.perf_counter() - t0
+    return {"value": cores * SYMBOLS_PER_WAVE / wall, "unit": UNIT,
+            "cores": cores, "kind": "port",
+            "sample": f"{cores} concurrent processes x one configs[1] waveform "
+                      f"({nb} blocks, complex128 numpy oracle), wall {wall:.2f} s"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU algorithm (oracle port) on all
+    host cores, one configs[1] waveform per step split by block ranges."""
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    from paper_2409_14489_b200.planner import BlockSchedule
+    cores = _cores()
+    nb = BlockSchedule(N_SAMPLES, 10240, 2860).n_blocks
+    parts = min(cores, nb)
+    ranges = [(nb * i // parts, nb * (i + 1) // parts, 0) for i in range(parts)]
+    ctx = mp.get_context("spawn")
+    times = []
+    with ctx.Pool(parts) as pool:
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            pool.map(_oracle_worker, ranges)
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
+    per = sum(times) / len(times)
+    value = SYMBOLS_PER_WAVE / per
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "c128 (f64)", "data": "synthetic (seeded band-limited Gaussian WDM)",
+            "impl": "reference",
+            "config": dict(config_block(args, world), waveforms_per_gpu=1),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": parts, "kind": "port",
+                             "sample": f"one configs[1] waveform per step, {nb} blocks "
+                                       f"split over {parts} processes"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------ GPU leg
+
+def roofline_numbers(dtype: str):
+    from paper_2409_14489_b200 import cb_essfm_cost
+    rm = cb_essfm_cost(10240, 2860, SPS_EFF, 15, 5).rm_per_2d
+    sample_bytes = 8 if dtype == "c64" else 16
+    byt = SPS_EFF * sample_bytes * (10240 / (10240 - 2860) + 1)
+    return rm, byt
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()), "measured"
+        except Exception:
+            pass
+    return {"hbm_gbs": 6650.0}, "fallback"
+
+
+def ncu_traffic(dtype: str):
+    """dram read+write bytes per launch of the fused kernel from the
+    committed ncu --set full summary (profiles/), or None."""
+    for p in sorted((ROOT / "profiles").glob("ncu_summary_*.json"), reverse=True):
+        try:
+            d = json.loads(p.read_text())
+            v = d.get(dtype, {}).get("dram_bytes_per_launch")
+            if v:
+                return float(v), p.name
+        except Exception:
+            continue
+    return None, None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--dtype", default="c64", choices=("c64", "c128"))
+    ap.add_argument("--batch", type=int, default=1,
+                    help="configs[1] waveforms per GPU per step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="minimal run for ncu (no sampler, no CPU legs)")
+    args = ap.parse_args()
+    if args.warmup < 3 and not args.profile:
+        args.warmup = 3
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    cpu = None
+    if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.profile):
+        cpu = cpu_baseline()
+
+    import numpy as np
+    import torch
+    import paper_2409_14489_b200 as pb
+    from paper_2409_14489_b200 import _native
+    from paper_2409_14489_b200.synth import gaussian_wdm
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg, coeffs = workload_cfg()
+    eng = pb.DbpEngine(cfg, coeffs, RATE, dtype=args.dtype, device=local)
+    ct = torch.complex64 if args.dtype == "c64" else torch.complex128
+    host = np.stack([gaussian_wdm(N_SAMPLES, RATE, seed=1000 * rank + b)
+                     for b in range(args.batch)])
+    x = torch.from_numpy(host).to(dev).to(ct)
+    out = torch.empty_like(x)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    sampler = ClockSampler(local) if not args.profile else None
+    if sampler:                      # nvidia-smi needs ~0.3 s to start sampling
+        sampler.__enter__()
+        time.sleep(0.5)
+    for _ in range(args.warmup):
+        eng.run_device(x, out)
+    barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)                    # evict the waveform from L2
+        evs[i][0].record(stream)
+        eng.run_device(x, out)
+        evs[i][1].record(stream)
+    barrier()
+    if sampler:
+        sampler.__exit__()
+    t_ms = sum(a.elapsed_time(b) for a, b in evs)
+    if dist is not None:
+        tt = torch.tensor([t_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    per_step_ms = t_ms / args.steps
+    sym_per_step = world * args.batch * SYMBOLS_PER_WAVE
+    value = sym_per_step / (per_step_ms * 1e-3)
+
+    # end to end through the public API with pinned host buffers
+    e2e = None
+    if not (args.no_e2e or args.profile):
+        hx = torch.from_numpy(host).to(ct).pin_memory()
+        hout = torch.empty_like(hx).pin_memory()
+        for _ in range(3):
+            eng.run_host(hx, hout)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            eng.run_host(hx, hout)
+        e1.record(stream)
+        barrier()
+        te = e0.elapsed_time(e1)
+        if dist is not None:
+            tt = torch.tensor([te], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": sym_per_step / (te / args.steps * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(hx.numel() * hx.element_size()),
+               "d2h_bytes_per_step": int(hout.numel() * hout.element_size()),
+               "path": "DbpEngine.run_host: pinned host -> H2D -> fused kernel -> D2H"}
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    peaks, peak_src = measured_peaks()
+    rm_2d, b_2d = roofline_numbers(args.dtype)
+    launch_s = per_step_ms * 1e-3                 # one kernel launch per step
+    sym_launch = args.batch * SYMBOLS_PER_WAVE
+    fma_kinds = (0, 1) if args.dtype == "c64" else (2,)
+    fma_peak = max(_native.fma_peak(k) for k in fma_kinds)
+    achieved_rm = rm_2d * sym_launch / launch_s
+    achieved_gbs = b_2d * sym_launch / launch_s / 1e9
+    t_fma = rm_2d / fma_peak
+    t_hbm = b_2d / (peaks["hbm_gbs"] * 1e9)
+    traffic, traffic_src = ncu_traffic(args.dtype)
+    if t_fma >= t_hbm:
+        roof = {"bound": "fma", "achieved": achieved_rm / 1e12, "peak": fma_peak / 1e12,
+                "unit": "TFLOP/s", "frac": achieved_rm / fma_peak,
+                "flop": "paper RM (real multiplications) per 2D symbol x symbols per launch",
+                "rm_per_2d": rm_2d,
+                "peak_source": "measured on this GPU: max(FFMA, FFMA2) lane-ops/s"
+                               if args.dtype == "c64" else "measured DFMA lane-ops/s"}
+    else:
+        roof = {"bound": "hbm"}
+    roof.update({"traffic": traffic, "traffic_source": traffic_src,
+                 "hbm": {"achieved": achieved_gbs, "peak": peaks["hbm_gbs"],
+                         "unit": "GB/s", "frac": achieved_gbs / peaks["hbm_gbs"],
+                         "bytes_per_2d": b_2d, "peak_source": peak_src}})
+    if roof["bound"] == "hbm":
+        roof.update({"achieved": achieved_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved_gbs / peaks["hbm_gbs"]})
+    clocks = sampler.summary() if sampler else None
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step_ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "c64 (f32)" if args.dtype == "c64" else "c128 (f64)",
+            "data": "synthetic (seeded band-limited Gaussian WDM, configs[1] grid)",
+            "config": config_block(args, world), "impl": "ours",
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": args.steps, "clocks": clocks,
+            "kernel": {"name": "cbessfm_block_kernel<float,5,2048>" if args.dtype == "c64"
+                       else "cbessfm_block_kernel<double,5,2048>",
+                       "plan": {k: getattr(eng.plan.info(), k) for k in
+                                ("threads_per_cta", "cluster_size", "smem_per_cta",
+                                 "max_active_clusters", "q")}}}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -14,7 +14,7 @@ from .complexity import (CostCounter, CostReport, cb_essfm_cost,
                          count_runtime_multiplies, essfm_time_domain_cost)
 from .config import (VARIANTS, CoefficientSet, DbpConfig, DualPolWaveform,
                      LinkConfig)
-from .engine import (MimoTransfer, build_mimo_transfer,
+from .engine import (DbpEngine, MimoTransfer, build_mimo_transfer,
                      channel_memory_samples, get_plan, gvd_step, launch,
                      nlpr_step, run_dbp, run_dbp_tensor)
 from .planner import (BlockSchedule, EngineTables, Shard, build_tables,

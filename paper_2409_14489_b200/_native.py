@@ -59,6 +59,8 @@ SIGNATURES = {
     "cbessfm_run": (C.c_int, [C.c_void_p, C.POINTER(Io), C.c_void_p]),
     "cbessfm_plan_destroy": (C.c_int, [C.c_void_p]),
     "cbessfm_last_error": (C.c_char_p, []),
+    # include/cbessfm_peaks.h
+    "cbessfm_fma_peak": (C.c_double, [C.c_int32, C.c_double]),
 }
 
 _lib = None
@@ -151,6 +153,11 @@ class NativePlan:
             except Exception:
                 pass
             self.handle = None
+
+
+def fma_peak(kind: int, ms: float = 200.0) -> float:
+    """Measured FMA lane-ops/s: kind 0 FFMA, 1 FFMA2, 2 DFMA."""
+    return float(load().cbessfm_fma_peak(kind, ms))
 
 
 def num_blocks(n: int, block_size: int, overlap: int) -> int:

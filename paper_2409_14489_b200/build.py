@@ -19,7 +19,8 @@ CSRC = PKG / "csrc"
 BUILD = PKG.parent / "build" / "cbessfm"
 LIB = PKG / "libcbessfm.so"
 HEADERS = [CSRC / "cbessfm_kernel.cuh", CSRC / "cbessfm_launch.cuh",
-           PKG.parent / "include" / "cbessfm.h"]
+           PKG.parent / "include" / "cbessfm.h",
+           PKG.parent / "include" / "cbessfm_peaks.h"]
 REALS = ("float", "double")
 SUBBANDS = tuple(range(1, 10))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -67,6 +68,8 @@ def build(jobs: int | None = None, verbose: bool = False) -> Path:
                           BUILD / f"inst_{real}_{p}.log"))
     tasks.append((CSRC / "cbessfm_api.cu", BUILD / "api.o", [], HEADERS,
                   BUILD / "api.log"))
+    tasks.append((CSRC / "cbessfm_peaks.cu", BUILD / "peaks.o", [], HEADERS,
+                  BUILD / "peaks.log"))
     with ThreadPoolExecutor(jobs) as ex:
         results = list(ex.map(_compile, tasks))
     errors = [e for _, e in results if e]

@@ -230,3 +230,17 @@ class DualPolWaveform:
     def copy(self) -> "DualPolWaveform":
         return DualPolWaveform(self.x.copy(), self.y.copy(),
                                self.sample_rate, self.center_freq)
+
+
+def load_coefficients_npz(path) -> CoefficientSet:
+    """Read a CoefficientSet saved by tests/golden/make_golden.py (keys
+    c_n_sb, c_subband_rate, ..., c_tap_<h>)."""
+    d = np.load(path, allow_pickle=False)
+    hs = [int(h) for h in d["c_hs"]]
+    return CoefficientSet(
+        n_sb=int(d["c_n_sb"]), subband_rate=float(d["c_subband_rate"]),
+        subband_spacing=float(d["c_subband_spacing"]),
+        reference_power_w=float(d["c_reference_power_w"]),
+        phase_norm_rad=float(d["c_phase_norm_rad"]),
+        step_scales=d["c_step_scales"], geometry_hash=str(d["c_geometry_hash"]),
+        coeffs={h: d[f"c_tap_{h}"] for h in hs})

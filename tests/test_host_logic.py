@@ -179,8 +179,9 @@ def test_counter_matches_closed_form_on_exact_tiling():
 
 
 def test_native_library_exports_every_header_symbol():
-    header = (ROOT / "include" / "cbessfm.h").read_text()
-    declared = set(re.findall(r"\b(cbessfm_[a-z_]+)\s*\(", header))
+    declared = set()
+    for h in (ROOT / "include").glob("*.h"):
+        declared |= set(re.findall(r"\b(cbessfm_[a-z_]+)\s*\(", h.read_text()))
     lib = _native.load()
     for name in declared:
         assert hasattr(lib, name), name
