@@ -49,6 +49,32 @@ std::vector<double> twiddles(int64_t n) {
   return t;
 }
 
+// Per-pass twiddle rows of the length-Q and length-Q/2 Stockham FFTs, in
+// the layout cbessfm_kernel.cuh reads (twp_offset / pass_radix): row k of
+// the pass with sub-transform size ns holds W_Q^(r*k*Q/(ns*R)), r < R.
+std::vector<double> pass_tables(int Q, const std::vector<double>& tq) {
+  using cbessfm::pass_radix;
+  using cbessfm::twp_offset;
+  using cbessfm::twp_size;
+  std::vector<double> out(2 * (size_t)(twp_size(Q) + twp_size(Q / 2)), 0.0);
+  auto fill = [&](int L, size_t base) {
+    for (int ns = 1; ns < L; ns *= pass_radix(L, ns)) {
+      const int R = pass_radix(L, ns);
+      if (ns == 1) continue;
+      const size_t off = base + twp_offset(L, ns);
+      for (int k = 0; k < ns; ++k)
+        for (int r = 0; r < R; ++r) {
+          const int64_t e = ((int64_t)r * k * (Q / (ns * R))) % Q;
+          out[2 * (off + (size_t)k * R + r)] = tq[2 * e];
+          out[2 * (off + (size_t)k * R + r) + 1] = tq[2 * e + 1];
+        }
+    }
+  };
+  fill(Q, 0);
+  fill(Q / 2, twp_size(Q));
+  return out;
+}
+
 }  // namespace
 
 struct cbessfm_plan {
@@ -59,6 +85,7 @@ struct cbessfm_plan {
   void* theta = nullptr;   // [n_steps]
   void* twQ = nullptr;     // [Q]
   void* twN = nullptr;     // [P*Q]
+  void* twp = nullptr;     // per-pass twiddle rows
 };
 
 namespace {
@@ -163,6 +190,9 @@ cbessfm_status upload_all(cbessfm_plan* p, const cbessfm_desc* d) {
     return cuda_fail(e, "upload twiddles");
   if ((e = upload_complex<R>(tn.data(), PQ, &p->twN, true)) != cudaSuccess)
     return cuda_fail(e, "upload outer twiddles");
+  const std::vector<double> tp = pass_tables(p->Q, tq);
+  if ((e = upload_complex<R>(tp.data(), tp.size() / 2, &p->twp, true)) != cudaSuccess)
+    return cuda_fail(e, "upload pass twiddles");
   return CBESSFM_OK;
 }
 
@@ -174,6 +204,7 @@ void free_plan(cbessfm_plan* p) {
   cudaFree(p->theta);
   cudaFree(p->twQ);
   cudaFree(p->twN);
+  cudaFree(p->twp);
   delete p;
 }
 
@@ -227,6 +258,7 @@ cbessfm::Params<R> make_params(const cbessfm_plan* p, const cbessfm_io* io) {
   prm.theta_scale = reinterpret_cast<const R*>(p->theta);
   prm.twQ = reinterpret_cast<const C*>(p->twQ);
   prm.twN = reinterpret_cast<const C*>(p->twN);
+  prm.twp = reinterpret_cast<const C*>(p->twp);
   prm.n_steps = p->n_steps;
   prm.cid0 = 0;
   return prm;

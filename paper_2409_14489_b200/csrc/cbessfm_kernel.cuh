@@ -24,6 +24,12 @@
 //     final phasor table already carries, so the inverse outer transform is
 //     an unnormalised sum;
 //   * theta_scale[st] = step_scales[st] / reference_power_w / Q (irfft 1/Q).
+//
+// Per step a CTA runs: subband IFFT (last pass writes the intensity),
+// half-length FFT + r2c untangle, DSMEM MIMO, c2r twist + half-length IFFT,
+// subband FFT (first pass applies the rotation, last pass the next
+// dispersion phasor) -- four shared-memory FFTs and no other full-field
+// passes.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -79,30 +85,6 @@ __device__ __forceinline__ Cx<float> ldg(const Cx<float>* p) {
 __device__ __forceinline__ Cx<double> ldg(const Cx<double>* p) {
   const double2 v = __ldg(reinterpret_cast<const double2*>(p));
   return mk(v.x, v.y);
-}
-
-// Twiddle loads inside the FFT passes go through the non-coherent L1 path
-// as volatile asm: the table is loop invariant, and letting the compiler
-// hoist every pass's twiddles out of the step loop exhausts the register
-// file (measured: ~900 B of spills per thread at 128 registers).
-__device__ __forceinline__ Cx<float> ldg_tw(const Cx<float>* p) {
-  float a, b;
-  asm volatile("ld.global.v2.f32 {%0, %1}, [%2];" : "=f"(a), "=f"(b) : "l"(p));
-  return mk(a, b);
-}
-__device__ __forceinline__ Cx<double> ldg_tw(const Cx<double>* p) {
-  double a, b;
-  asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "l"(p));
-  return mk(a, b);
-}
-
-// threadIdx.x read through volatile asm: keeps per-pass shared-memory
-// address arithmetic inside the step loop instead of letting loop-invariant
-// code motion hoist every pass's addresses into live registers.
-__device__ __forceinline__ int tid_opaque() {
-  int t;
-  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t));
-  return t;
 }
 
 // Shared-memory index padding: one spare element every 16 complex entries
@@ -196,126 +178,294 @@ __device__ __forceinline__ void dft_reg(Cx<R>* v) {
 }
 
 // ------------------------------------------------------------------------
-// Stockham radix-RAD pass over NA arrays of length L stored at stride
-// padded_len(L) in shared memory, register staged (load all, barrier, store
-// all, barrier). twQ is the length-Q table exp(-2 pi i m / Q).
+// Radix schedule and per-pass twiddle tables.
+//
+// An FFT of length L runs Stockham passes with sub-transform size NS = 1,
+// R1, R1*R2, ... and radix R = min(MAXRAD, L / NS). A pass with NS > 1
+// twiddles element r of butterfly j by W_Q^(r*k*Q/(NS*R)), k = j mod NS.
+// Those factors are stored per pass as NS rows of R entries (row k, entry
+// r), so the R-1 twiddles of a butterfly are one contiguous row: lanes with
+// consecutive k read consecutive rows with 16-byte vector loads (fully
+// coalesced), instead of R-1 scattered 8-byte loads.
 
-template <int L, int MAXRAD, int NS>
-struct PassRadix {
-  static constexpr int rem = L / NS;
-  static constexpr int value = rem >= MAXRAD ? MAXRAD : rem;
-};
+constexpr int kMaxRad = 8;
 
-// Addressing: with one pad slot per 16 entries, pad(a + b) == pad(a) + pad(b)
-// for every (read, write) index pair a Stockham pass forms (checked
-// exhaustively in tests/test_host_logic.py), so each pass needs one read and
-// one write base register plus compile-time offsets. `zero` is a shared
-// memory word holding 0: reading it after the barrier makes every pass's
-// addressing loop-variant, which stops ptxas from hoisting all passes'
-// address registers out of the step loop (it otherwise spills).
+__host__ __device__ constexpr int pass_radix(int L, int ns) {
+  return L / ns >= kMaxRad ? kMaxRad : L / ns;
+}
+__host__ __device__ constexpr int twp_offset(int L, int NS) {
+  int s = 0;
+  for (int ns = 1; ns < NS; ns *= pass_radix(L, ns))
+    if (ns > 1) s += ns * pass_radix(L, ns);
+  return s;
+}
+__host__ __device__ constexpr int twp_size(int L) { return twp_offset(L, L); }
+
+// Load the twiddle row of butterfly k (RAD entries, entry 0 unused).
+template <int RAD>
+__device__ __forceinline__ void load_row(const Cx<float>* row, Cx<float>* w) {
+#pragma unroll
+  for (int q = 0; q < RAD / 2; ++q) {
+    float a, b, c, d;
+    asm volatile("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(a), "=f"(b), "=f"(c), "=f"(d)
+                 : "l"(row + 2 * q));
+    w[2 * q] = mk(a, b);
+    w[2 * q + 1] = mk(c, d);
+  }
+}
+template <int RAD>
+__device__ __forceinline__ void load_row(const Cx<double>* row, Cx<double>* w) {
+#pragma unroll
+  for (int q = 0; q < RAD; ++q) {
+    double a, b;
+    asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "l"(row + q));
+    w[q] = mk(a, b);
+  }
+}
+
 __device__ __forceinline__ void bar_named(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-template <typename R, int Q, int L, int NA, int RAD, int NS, bool INV>
-__device__ __forceinline__ void butterfly_load(const Cx<R>* __restrict__ buf,
-                                               const Cx<R>* __restrict__ twQ, int jj,
-                                               Cx<R>* v) {
-  constexpr int STRIDE = padded_len(L);
-  constexpr int TWM = Q / (NS * RAD);  // twiddle index multiplier
-  constexpr int LR = L / RAD;
-  const int a = jj / LR;
-  const int j = jj % LR;
-  const Cx<R>* base = buf + a * STRIDE + pad(j);
+// Float index of real sample p in a complex-packed array z[t] = (v[2t], v[2t+1])
+// stored with the complex padding.
+__device__ __forceinline__ int fpos(int p) { return 2 * pad(p >> 1) + (p & 1); }
+
+// ------------------------------------------------------------------------
+// Hooks fused into the first (pre: after the loads) or last (post: before
+// the stores) pass of a two-polarisation FFT. Element r of butterfly j sits
+// at position j + r*LR on load; natural output r sits at d0 + r*NS on store
+// and lives in v[bitrev(r)].
+
+struct NoHook {
+  template <typename R, int RAD, int LR>
+  __device__ __forceinline__ void pre(int, Cx<R>*, Cx<R>*) {}
+  template <typename R, int RAD, int NS>
+  __device__ __forceinline__ void post(int, Cx<R>*, Cx<R>*) {}
+};
+
+// Multiply by a dispersion phasor row (dbp.py:395 / :399); ph is indexed by
+// the subband-local bin.
+template <typename R>
+struct PhasorHook : NoHook {
+  const Cx<R>* ph;
+  template <typename, int RAD, int NS>
+  __device__ __forceinline__ void post(int d0, Cx<R>* vx, Cx<R>* vy) {
 #pragma unroll
-  for (int r = 0; r < RAD; ++r) v[r] = base[pad(r * LR)];
-  if (NS > 1) {
-    const int k = j % NS;
-    const Cx<R>* tw = twQ + k * TWM;
-    const int step = k * TWM;
-#pragma unroll
-    for (int r = 1; r < RAD; ++r) {
-      const Cx<R> w = ldg_tw(tw + (r - 1) * step);
-      v[r] = INV ? cmulc(v[r], w) : cmul(v[r], w);
+    for (int r = 0; r < RAD; ++r) {
+      const Cx<R> w = ldg(ph + d0 + r * NS);
+      vx[bitrev<RAD>(r)] = cmul(vx[bitrev<RAD>(r)], w);
+      vy[bitrev<RAD>(r)] = cmul(vy[bitrev<RAD>(r)], w);
     }
   }
-  dft_reg<R, RAD, INV>(v);
-}
+};
 
-template <typename R, int L, int NA, int RAD, int NS>
-__device__ __forceinline__ void butterfly_store(Cx<R>* __restrict__ buf, int jj,
-                                                const Cx<R>* v) {
-  constexpr int STRIDE = padded_len(L);
-  constexpr int LR = L / RAD;
-  const int a = jj / LR;
-  const int j = jj % LR;
-  const int k = j % NS;
-  Cx<R>* base = buf + a * STRIDE + pad((j / NS) * NS * RAD + k);
+// Write the intensity |x|^2 + |y|^2 (dbp.py:193) of the just-computed time
+// samples into the packed real array I (float view of IS).
+template <typename R>
+struct IntensityHook : NoHook {
+  R* I;
+  template <typename, int RAD, int NS>
+  __device__ __forceinline__ void post(int d0, Cx<R>* vx, Cx<R>* vy) {
+    R* base = I + fpos(d0);
 #pragma unroll
-  for (int r = 0; r < RAD; ++r) base[pad(r * NS)] = v[bitrev<RAD>(r)];
+    for (int r = 0; r < RAD; ++r) {
+      const Cx<R> a = vx[bitrev<RAD>(r)], b = vy[bitrev<RAD>(r)];
+      base[2 * pad(r * NS / 2)] = a.x * a.x + a.y * a.y + (b.x * b.x + b.y * b.y);
+    }
+  }
+};
+
+template <typename R>
+__device__ __forceinline__ void sincos_acc(R a, R* s, R* c);
+template <>
+__device__ __forceinline__ void sincos_acc<float>(float a, float* s, float* c) {
+  sincosf(a, s, c);
+}
+template <>
+__device__ __forceinline__ void sincos_acc<double>(double a, double* s, double* c) {
+  sincos(a, s, c);
 }
 
-// Addressing: with one pad slot per 16 entries, pad(a + b) == pad(a) + pad(b)
-// for every (read, write) index pair a Stockham pass forms (checked
-// exhaustively in tests/test_host_logic.py), so each pass needs one read and
-// one write base register plus compile-time offsets. `zero` is a shared
-// memory word holding 0: reading it after the barrier makes every pass's
-// addressing loop-variant, which stops ptxas from hoisting all passes'
-// address registers out of the step loop (it otherwise spills).
-// Passes with fewer butterflies than threads run on the leading whole warps
-// only; those synchronise between load and store with a named barrier, so
-// the staged registers never have to live across a divergent region.
-template <typename R, int Q, int L, int NA, int NT, int RAD, int NS, bool INV>
-__device__ __forceinline__ void fft_pass(Cx<R>* __restrict__ buf,
-                                         const Cx<R>* __restrict__ twQ,
-                                         const volatile int* zero) {
-  constexpr int NB = NA * L / RAD;  // butterflies in this pass
+// Rotate both polarisations by exp(-i theta), theta = scale * th[p]
+// (dbp.py:196, :208); th is the float view of the packed irfft output.
+template <typename R>
+struct RotationHook : NoHook {
+  const R* th;
+  R scale;
+  template <typename, int RAD, int LR>
+  __device__ __forceinline__ void pre(int j, Cx<R>* vx, Cx<R>* vy) {
+    const R* base = th + fpos(j);
+#pragma unroll
+    for (int r = 0; r < RAD; ++r) {
+      R s, c;
+      sincos_acc<R>(base[2 * pad(r * LR / 2)] * scale, &s, &c);
+      const Cx<R> rot = mk(c, -s);
+      vx[r] = cmul(vx[r], rot);
+      vy[r] = cmul(vy[r], rot);
+    }
+  }
+};
+
+// ------------------------------------------------------------------------
+// Stockham passes. Addressing: with one pad slot per 16 entries,
+// pad(a + b) == pad(a) + pad(b) for every (read, write) index pair a pass
+// forms (checked exhaustively in tests/test_host_logic.py), so a pass needs
+// one read and one write base register plus compile-time offsets. `zero`
+// is a shared word holding 0: reading it after the barrier keeps each
+// pass's addressing inside the step loop (ptxas otherwise hoists every
+// pass's address registers out of the loop and spills).
+
+// Two-polarisation pass: thread j runs butterfly j of x AND of y, sharing
+// the index arithmetic and the twiddle row.
+template <typename R, int Q, int NT, int NS, bool INV, bool FIRST, bool LAST, class Hook>
+__device__ __forceinline__ void fft2_pass(Cx<R>* __restrict__ F, const Cx<R>* __restrict__ twp,
+                                          const volatile int* zero, Hook& hook) {
+  constexpr int RAD = pass_radix(Q, NS);
+  constexpr int LR = Q / RAD;
+  constexpr int NB = Q / RAD;
+  static_assert(NB % NT == 0, "butterflies must tile the block");
+  constexpr int PER = NB / NT;
+  constexpr int SF = padded_len(Q);
+  const Cx<R>* tw = twp + twp_offset(Q, NS);
+  Cx<R> vx[PER][RAD], vy[PER][RAD];
   const int tid = threadIdx.x + *zero;
+#pragma unroll
+  for (int p = 0; p < PER; ++p) {
+    const int j = tid + p * NT;
+    const Cx<R>* bx = F + pad(j);
+#pragma unroll
+    for (int r = 0; r < RAD; ++r) {
+      vx[p][r] = bx[pad(r * LR)];
+      vy[p][r] = bx[SF + pad(r * LR)];
+    }
+    if constexpr (FIRST) hook.template pre<R, RAD, LR>(j, vx[p], vy[p]);
+    if constexpr (NS > 1) {
+      Cx<R> w[RAD];
+      load_row<RAD>(tw + (j % NS) * RAD, w);
+#pragma unroll
+      for (int r = 1; r < RAD; ++r) {
+        vx[p][r] = INV ? cmulc(vx[p][r], w[r]) : cmul(vx[p][r], w[r]);
+        vy[p][r] = INV ? cmulc(vy[p][r], w[r]) : cmul(vy[p][r], w[r]);
+      }
+    }
+    dft_reg<R, RAD, INV>(vx[p]);
+    dft_reg<R, RAD, INV>(vy[p]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int p = 0; p < PER; ++p) {
+    const int j = tid + p * NT;
+    const int d0 = (j / NS) * NS * RAD + j % NS;
+    if constexpr (LAST) hook.template post<R, RAD, NS>(d0, vx[p], vy[p]);
+    Cx<R>* bx = F + pad(d0);
+#pragma unroll
+    for (int r = 0; r < RAD; ++r) {
+      bx[pad(r * NS)] = vx[p][bitrev<RAD>(r)];
+      bx[SF + pad(r * NS)] = vy[p][bitrev<RAD>(r)];
+    }
+  }
+  __syncthreads();
+}
+
+template <typename R, int Q, int NT, int NS, bool INV, class Pre, class Post>
+struct Fft2Run {
+  static __device__ __forceinline__ void run(Cx<R>* F, const Cx<R>* twp, const volatile int* z,
+                                             Pre& pre, Post& post) {
+    constexpr int RAD = pass_radix(Q, NS);
+    constexpr bool FIRST = NS == 1, LAST = NS * RAD == Q;
+    if constexpr (FIRST && LAST) {
+      static_assert(!(FIRST && LAST), "single-pass transforms are not used");
+    } else if constexpr (FIRST) {
+      fft2_pass<R, Q, NT, NS, INV, true, false>(F, twp, z, pre);
+    } else if constexpr (LAST) {
+      fft2_pass<R, Q, NT, NS, INV, false, true>(F, twp, z, post);
+    } else {
+      NoHook none;
+      fft2_pass<R, Q, NT, NS, INV, false, false>(F, twp, z, none);
+    }
+    if constexpr (!LAST) Fft2Run<R, Q, NT, NS * RAD, INV, Pre, Post>::run(F, twp, z, pre, post);
+  }
+};
+
+// Unnormalised length-Q FFT of both polarisation rows of F (forward:
+// exp(-), inverse: exp(+)), natural order in and out, with fused hooks.
+// Ends with a barrier.
+template <typename R, int Q, int NT, bool INV, class Pre = NoHook, class Post = NoHook>
+__device__ __forceinline__ void fft2(Cx<R>* F, const Cx<R>* twp, const volatile int* z,
+                                     Pre pre = Pre(), Post post = Post()) {
+  Fft2Run<R, Q, NT, 1, INV, Pre, Post>::run(F, twp, z, pre, post);
+}
+
+// Single-array pass for the half-length real-transform FFTs. Passes with
+// fewer butterflies than threads run on the leading whole warps only; those
+// synchronise between load and store with a named barrier, and a full
+// barrier ends the pass so no warp runs ahead into a later pass whose named
+// barrier expects a different thread count.
+template <typename R, int Q, int L, int NT, int NS, bool INV>
+__device__ __forceinline__ void fft1_pass(Cx<R>* __restrict__ buf, const Cx<R>* __restrict__ twp,
+                                          const volatile int* zero) {
+  constexpr int RAD = pass_radix(L, NS);
+  constexpr int LR = L / RAD;
+  constexpr int NB = L / RAD;
+  const Cx<R>* tw = twp + twp_offset(L, NS);
+  const int tid = threadIdx.x + *zero;
+  auto body_load = [&](int j, Cx<R>* v) {
+    const Cx<R>* b = buf + pad(j);
+#pragma unroll
+    for (int r = 0; r < RAD; ++r) v[r] = b[pad(r * LR)];
+    if constexpr (NS > 1) {
+      Cx<R> w[RAD];
+      load_row<RAD>(tw + (j % NS) * RAD, w);
+#pragma unroll
+      for (int r = 1; r < RAD; ++r) v[r] = INV ? cmulc(v[r], w[r]) : cmul(v[r], w[r]);
+    }
+    dft_reg<R, RAD, INV>(v);
+  };
+  auto body_store = [&](int j, const Cx<R>* v) {
+    Cx<R>* b = buf + pad((j / NS) * NS * RAD + j % NS);
+#pragma unroll
+    for (int r = 0; r < RAD; ++r) b[pad(r * NS)] = v[bitrev<RAD>(r)];
+  };
   if constexpr (NB >= NT) {
     static_assert(NB % NT == 0, "butterflies must tile the block");
     constexpr int PER = NB / NT;
     Cx<R> v[PER][RAD];
 #pragma unroll
-    for (int p = 0; p < PER; ++p)
-      butterfly_load<R, Q, L, NA, RAD, NS, INV>(buf, twQ, tid + p * NT, v[p]);
+    for (int p = 0; p < PER; ++p) body_load(tid + p * NT, v[p]);
     __syncthreads();
 #pragma unroll
-    for (int p = 0; p < PER; ++p) butterfly_store<R, L, NA, RAD, NS>(buf, tid + p * NT, v[p]);
+    for (int p = 0; p < PER; ++p) body_store(tid + p * NT, v[p]);
     __syncthreads();
   } else {
     constexpr int ACT = (NB + 31) / 32 * 32;  // active threads, whole warps
     if (tid < ACT) {
       Cx<R> v[RAD];
       const bool on = (NB % 32 == 0) || tid < NB;
-      if (on) butterfly_load<R, Q, L, NA, RAD, NS, INV>(buf, twQ, tid, v);
+      if (on) body_load(tid, v);
       bar_named(1, ACT);
-      if (on) butterfly_store<R, L, NA, RAD, NS>(buf, tid, v);
+      if (on) body_store(tid, v);
     }
-    // full barrier: no warp may run ahead into a later pass whose named
-    // barrier expects a different thread count
     __syncthreads();
   }
 }
 
-template <typename R, int Q, int L, int NA, int NT, int MAXRAD, int NS, bool INV>
-struct FftRun {
-  static __device__ __forceinline__ void run(Cx<R>* buf, const Cx<R>* twQ, const volatile int* z) {
-    constexpr int RAD = PassRadix<L, MAXRAD, NS>::value;
-    fft_pass<R, Q, L, NA, NT, RAD, NS, INV>(buf, twQ, z);
-    FftRun<R, Q, L, NA, NT, MAXRAD, NS * RAD, INV>::run(buf, twQ, z);
+template <typename R, int Q, int L, int NT, int NS, bool INV>
+struct Fft1Run {
+  static __device__ __forceinline__ void run(Cx<R>* buf, const Cx<R>* twp, const volatile int* z) {
+    fft1_pass<R, Q, L, NT, NS, INV>(buf, twp, z);
+    Fft1Run<R, Q, L, NT, NS * pass_radix(L, NS), INV>::run(buf, twp, z);
   }
 };
-template <typename R, int Q, int L, int NA, int NT, int MAXRAD, bool INV>
-struct FftRun<R, Q, L, NA, NT, MAXRAD, L, INV> {
+template <typename R, int Q, int L, int NT, bool INV>
+struct Fft1Run<R, Q, L, NT, L, INV> {
   static __device__ __forceinline__ void run(Cx<R>*, const Cx<R>*, const volatile int*) {}
 };
 
-// Unnormalised FFT (forward: exp(-), inverse: exp(+)) of NA arrays of
-// length L in place, natural order in and out. Ends with a barrier.
-template <typename R, int Q, int L, int NA, int NT, int MAXRAD, bool INV>
-__device__ __forceinline__ void fft(Cx<R>* buf, const Cx<R>* twQ, const volatile int* z) {
-  FftRun<R, Q, L, NA, NT, MAXRAD, 1, INV>::run(buf, twQ, z);
-  __syncthreads();
+template <typename R, int Q, int L, int NT, bool INV>
+__device__ __forceinline__ void fft1(Cx<R>* buf, const Cx<R>* twp, const volatile int* z) {
+  Fft1Run<R, Q, L, NT, 1, INV>::run(buf, twp, z);
 }
 
 // ------------------------------------------------------------------------
@@ -337,46 +487,29 @@ struct Params {
   const R* theta_scale;    // [n_steps], carries 1/Q
   const Cx<R>* twQ;        // [Q]   exp(-2 pi i m / Q)
   const Cx<R>* twN;        // [P*Q] exp(-2 pi i m / (P Q))
+  const Cx<R>* twp;        // per-pass rows: [twp_size(Q)] then [twp_size(Q/2)]
   int n_steps;
-  int64_t cid0;     // first cluster index of this launch chunk
+  int64_t cid0;            // first cluster index of this launch chunk
 };
 
-template <typename R>
-__device__ __forceinline__ void sincos_acc(R a, R* s, R* c);
-template <>
-__device__ __forceinline__ void sincos_acc<float>(float a, float* s, float* c) {
-  sincosf(a, s, c);
-}
-template <>
-__device__ __forceinline__ void sincos_acc<double>(double a, double* s, double* c) {
-  sincos(a, s, c);
-}
-
-template <typename R>
-struct Cfg {
-  // max radix of the register-staged Stockham passes
-  static constexpr int MAXRAD = 8;
-};
-
-// One radix-8 butterfly per thread on the two-polarisation field FFTs;
-// capped so double-precision blocks stay within 128 registers.
+// One radix-8 butterfly of each polarisation per thread on the length-Q
+// field FFTs.
 template <typename R, int Q>
 __host__ __device__ constexpr int threads_for() {
-  return (Q / 4) > (sizeof(R) == 4 ? 1024 : 512) ? (sizeof(R) == 4 ? 1024 : 512) : Q / 4;
+  return Q / 8;
 }
 
-// Resident CTAs per SM the register budget is sized for: 1024 threads at
-// <= 64 registers (float) or 512 threads at <= 128 registers (double).
+// Resident CTAs per SM the register budget is sized for.
 template <typename R, int Q>
 __host__ __device__ constexpr int min_blocks() {
-  return (sizeof(R) == 4 ? 1024 : 512) / threads_for<R, Q>() > 1
-             ? (sizeof(R) == 4 ? 1024 : 512) / threads_for<R, Q>()
+  return (sizeof(R) == 4 ? (Q <= 2048 ? 768 : 1024) : 512) / threads_for<R, Q>() > 1
+             ? (sizeof(R) == 4 ? (Q <= 2048 ? 768 : 1024) : 512) / threads_for<R, Q>()
              : 1;
 }
 
 template <typename R, int Q>
 __host__ __device__ constexpr size_t smem_bytes(int P) {
-  // F: 2 padded polarisation arrays; IS, TS: padded spectra (Q/2+1 bins)
+  // F: 2 padded polarisation rows; IS, TS: padded spectra (Q/2+1 bins)
   return sizeof(Cx<R>) * (size_t)(2 * padded_len(Q) + (P > 1 ? 2 : 1) * padded_len(Q / 2 + 1));
 }
 
@@ -396,10 +529,8 @@ template <typename R, int P, int Q>
 __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
     cbessfm_block_kernel(const Params<R> prm) {
   constexpr int NT = threads_for<R, Q>();
-  constexpr int N = P * Q;
   constexpr int H = Q / 2;
   constexpr int SF = padded_len(Q);      // stride between x and y in F
-  constexpr int MAXRAD = Cfg<R>::MAXRAD;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Cx<R>* F = reinterpret_cast<Cx<R>*>(smem_raw);
@@ -417,6 +548,8 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
 
   const Cx<R>* __restrict__ twQ = prm.twQ;
   const Cx<R>* __restrict__ twN = prm.twN;
+  const Cx<R>* __restrict__ twpQ = prm.twp;                  // length-Q passes
+  const Cx<R>* __restrict__ twpH = prm.twp + twp_size(Q);    // length-Q/2 passes
 
   // ---- 1. load the polyphase component u[rank + P*t2] of the circular
   //         window starting at (b*keep - half) mod n (dbp.py:473-475)
@@ -435,13 +568,17 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
   }
   __syncthreads();
 
-  // ---- 2. outer transform, polyphase part: FFT_Q of both polarisations
-  fft<R, Q, Q, 2, NT, MAXRAD, false>(F, twQ, &s_zero);
-
-  const Cx<R>* ph = prm.phasor + (size_t)rank * Q;  // this CTA's subband rows
   const size_t ph_tab = (size_t)P * Q;
 
-  if constexpr (P > 1) {
+  // ---- 2. outer transform, polyphase part: FFT_Q of both polarisations.
+  //         For P == 1 the subband layout is the natural FFT order
+  //         (bin_home is the identity) and the first phasor is fused in.
+  if constexpr (P == 1) {
+    PhasorHook<R> ph0;
+    ph0.ph = prm.phasor + (size_t)prm.ph_index[0] * ph_tab;
+    fft2<R, Q, NT, false, NoHook, PhasorHook<R>>(F, twpQ, &s_zero, NoHook(), ph0);
+  } else {
+    fft2<R, Q, NT, false>(F, twpQ, &s_zero);
     // ---- 3. cross-subband radix-P stage over DSMEM: CTA c produces bins
     //         Q*k1 + k2 for k2 in its slice and every k1, and writes each to
     //         the CTA that owns it in the fftshift'd subband layout. Results
@@ -479,33 +616,20 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
       for (int t = tid; t < Q; t += NT) F[pol * SF + pad(t)] = S[pad(t)];
       cluster.sync();
     }
-  } else {
-    // P == 1: the subband layout is the natural FFT order (bin_home is the
-    // identity); apply the first phasor in place.
-    const Cx<R>* w0 = ph + (size_t)prm.ph_index[0] * ph_tab;
-    for (int t = tid; t < Q; t += NT) {
-      const Cx<R> w = ldg(w0 + t);
-      F[pad(t)] = cmul(F[pad(t)], w);
-      F[SF + pad(t)] = cmul(F[SF + pad(t)], w);
-    }
-    __syncthreads();
   }
+
+  const Cx<R>* ph_rank = prm.phasor + (size_t)rank * Q;  // this CTA's subband rows
+  R* Ireal = reinterpret_cast<R*>(IS);
+  const R* Treal = reinterpret_cast<const R*>(TS);
 
   // ---- 4. nonlinear steps (dbp.py:394-398)
   for (int st = 0; st < prm.n_steps; ++st) {
-    // subband IFFT (normalisation folded into the phasor)
-    fft<R, Q, Q, 2, NT, MAXRAD, true>(F, twQ, &s_zero);
-
-    // intensity I = |x|^2 + |y|^2 packed as H complex z[t] = I[2t] + i I[2t+1]
-    for (int t = tid; t < H; t += NT) {
-      const Cx<R> x0 = F[pad(2 * t)], x1 = F[pad(2 * t + 1)];
-      const Cx<R> y0 = F[SF + pad(2 * t)], y1 = F[SF + pad(2 * t + 1)];
-      const R i0 = x0.x * x0.x + x0.y * x0.y + (y0.x * y0.x + y0.y * y0.y);
-      const R i1 = x1.x * x1.x + x1.y * x1.y + (y1.x * y1.x + y1.y * y1.y);
-      IS[pad(t)] = mk(i0, i1);
-    }
-    __syncthreads();
-    fft<R, Q, H, 1, NT, MAXRAD, false>(IS, twQ, &s_zero);
+    // subband IFFT (normalisation folded into the phasor); its last pass
+    // also writes I = |x|^2 + |y|^2 packed as z[t] = I[2t] + i I[2t+1]
+    IntensityHook<R> ih;
+    ih.I = Ireal;
+    fft2<R, Q, NT, true, NoHook, IntensityHook<R>>(F, twpQ, &s_zero, NoHook(), ih);
+    fft1<R, Q, H, NT, false>(IS, twpH, &s_zero);
 
     // r2c untangle in place: I_hat[k], k = 0..H  (numpy rfft, dbp.py:194)
     for (int k = tid; k <= H / 2; k += NT) {
@@ -564,55 +688,33 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
       } else {
         const Cx<R> a = TS[pad(k)];                 // X[k]
         const Cx<R> c = conj(TS[pad(H - k)]);       // X[k + H]
-        const Cx<R> wk = ldg(twQ + k);            // W^k, we need W^-k
+        const Cx<R> wk = ldg(twQ + k);              // W^k
         const Cx<R> s = a + c;
         const Cx<R> dd = cmulc(a - c, wk);          // W^-k (a - c)
         TS[pad(k)] = mk(s.x - dd.y, s.y + dd.x);    // s + i dd
         if (k != H - k) {
-          // Z[H-k] = (X[H-k] + X[Q-k]) + i W^{-(H-k)} (X[H-k] - X[Q-k])
-          //        = conj(s) + i * (conj(dd) * -1)... computed directly:
+          // Z[H-k] = (X[H-k] + X[Q-k]) + i W^-(H-k) (X[H-k] - X[Q-k])
           const Cx<R> a2 = conj(c);                 // X[H-k]
           const Cx<R> c2 = conj(a);                 // X[Q-k]
           const Cx<R> s2 = a2 + c2;
-          const Cx<R> w2 = mk(-wk.x, wk.y);         // W^{H-k} = -conj(W^k)
+          const Cx<R> w2 = mk(-wk.x, wk.y);         // W^(H-k) = -conj(W^k)
           const Cx<R> d2 = cmulc(a2 - c2, w2);
           TS[pad(H - k)] = mk(s2.x - d2.y, s2.y + d2.x);
         }
       }
     }
     __syncthreads();
-    fft<R, Q, H, 1, NT, MAXRAD, true>(TS, twQ, &s_zero);
+    fft1<R, Q, H, NT, true>(TS, twpH, &s_zero);
 
-    // rotation exp(-i theta) of both polarisations (dbp.py:208)
-    {
-      const R tsc = prm.theta_scale[st];
-      for (int t = tid; t < H; t += NT) {
-        const Cx<R> z = TS[pad(t)];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const R th = (e ? z.y : z.x) * tsc;
-          R s, c;
-          sincos_acc<R>(th, &s, &c);
-          const Cx<R> rot = mk(c, -s);
-          const int ti = pad(2 * t + e);
-          F[ti] = cmul(F[ti], rot);
-          F[SF + ti] = cmul(F[SF + ti], rot);
-        }
-      }
-    }
-    __syncthreads();
-
-    // subband FFT, then the next dispersion stage (dbp.py:398, :395 / :399)
-    fft<R, Q, Q, 2, NT, MAXRAD, false>(F, twQ, &s_zero);
-    {
-      const Cx<R>* w1 = ph + (size_t)prm.ph_index[st + 1] * ph_tab;
-      for (int t = tid; t < Q; t += NT) {
-        const Cx<R> w = ldg(w1 + t);
-        F[pad(t)] = cmul(F[pad(t)], w);
-        F[SF + pad(t)] = cmul(F[SF + pad(t)], w);
-      }
-    }
-    __syncthreads();
+    // rotation exp(-i theta) fused into the first pass and the next
+    // dispersion stage into the last pass of the subband FFT
+    // (dbp.py:208, :398, then :395 or :399)
+    RotationHook<R> rot;
+    rot.th = Treal;
+    rot.scale = prm.theta_scale[st];
+    PhasorHook<R> ph1;
+    ph1.ph = ph_rank + (size_t)prm.ph_index[st + 1] * ph_tab;
+    fft2<R, Q, NT, false, RotationHook<R>, PhasorHook<R>>(F, twpQ, &s_zero, rot, ph1);
   }
 
   // ---- 5. merge + outer IFFT (dbp.py:400-401): CTA c gathers, for k2 in
@@ -649,7 +751,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
       cluster.sync();
     }
   }
-  fft<R, Q, Q, 2, NT, MAXRAD, true>(F, twQ, &s_zero);
+  fft2<R, Q, NT, true>(F, twpQ, &s_zero);
 
   // ---- 6. keep proc[half : half + span] (dbp.py:476-477)
   {

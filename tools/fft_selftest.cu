@@ -1,5 +1,6 @@
-// Standalone check of the shared-memory Stockham FFT used by the fused
-// kernel: forward/inverse, float/double, NA = 1/2, against a long-double DFT.
+// Standalone check of the shared-memory Stockham FFTs used by the fused
+// kernel (two-polarisation fft2 with per-pass twiddle rows, and the
+// half-length fft1), forward/inverse, float/double, against a long-double DFT.
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -7,9 +8,11 @@
 #include "../paper_2409_14489_b200/csrc/cbessfm_kernel.cuh"
 using namespace cbessfm;
 
-template <typename R, int Q, int L, int NA, bool INV>
-__global__ void __launch_bounds__(threads_for<R, Q>()) kfft(const Cx<R>* tw, Cx<R>* data) {
+template <typename R, int Q, bool HALF, bool INV>
+__global__ void __launch_bounds__(threads_for<R, Q>()) kfft(const Cx<R>* twp, Cx<R>* data) {
   constexpr int NT = threads_for<R, Q>();
+  constexpr int L = HALF ? Q / 2 : Q;
+  constexpr int NA = HALF ? 1 : 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int z;
   if (threadIdx.x == 0) z = 0;
@@ -17,38 +20,58 @@ __global__ void __launch_bounds__(threads_for<R, Q>()) kfft(const Cx<R>* tw, Cx<
   for (int a = 0; a < NA; ++a)
     for (int i = threadIdx.x; i < L; i += NT) buf[a * padded_len(L) + pad(i)] = data[a * L + i];
   __syncthreads();
-  fft<R, Q, L, NA, NT, Cfg<R>::MAXRAD, INV>(buf, tw, &z);
+  if constexpr (HALF)
+    fft1<R, Q, L, NT, INV>(buf, twp + twp_size(Q), &z);
+  else
+    fft2<R, Q, NT, INV>(buf, twp, &z);
   for (int a = 0; a < NA; ++a)
     for (int i = threadIdx.x; i < L; i += NT) data[a * L + i] = buf[a * padded_len(L) + pad(i)];
 }
 
-template <typename R, int Q, int L, int NA, bool INV>
+template <typename R>
+std::vector<Cx<R>> tables(int Q) {
+  const long double pi = 3.141592653589793238462643383279502884L;
+  std::vector<Cx<R>> out(twp_size(Q) + twp_size(Q / 2));
+  auto fill = [&](int L, int base) {
+    for (int ns = 1; ns < L; ns *= pass_radix(L, ns)) {
+      const int Rr = pass_radix(L, ns);
+      if (ns == 1) continue;
+      for (int k = 0; k < ns; ++k)
+        for (int r = 0; r < Rr; ++r) {
+          const long long e = (long long)r * k * (Q / (ns * Rr)) % Q;
+          out[base + twp_offset(L, ns) + k * Rr + r].x = (R)cosl(-2 * pi * e / Q);
+          out[base + twp_offset(L, ns) + k * Rr + r].y = (R)sinl(-2 * pi * e / Q);
+        }
+    }
+  };
+  fill(Q, 0);
+  fill(Q / 2, twp_size(Q));
+  return out;
+}
+
+template <typename R, int Q, bool HALF, bool INV>
 double run() {
+  constexpr int L = HALF ? Q / 2 : Q;
+  constexpr int NA = HALF ? 1 : 2;
   const int n = NA * L;
-  std::vector<Cx<R>> h(n), tw(Q);
+  std::vector<Cx<R>> h(n);
   std::vector<long double> re(n), im(n);
   srand(1);
   for (int i = 0; i < n; ++i) {
-    re[i] = rand() / (long double)RAND_MAX - 0.5L;
-    im[i] = rand() / (long double)RAND_MAX - 0.5L;
-    h[i].x = (R)re[i];
-    h[i].y = (R)im[i];
+    h[i].x = (R)(rand() / (double)RAND_MAX - 0.5);
+    h[i].y = (R)(rand() / (double)RAND_MAX - 0.5);
     re[i] = h[i].x;
     im[i] = h[i].y;
   }
-  const long double pi = 3.141592653589793238462643383279502884L;
-  for (int m = 0; m < Q; ++m) {
-    tw[m].x = (R)cosl(-2 * pi * m / Q);
-    tw[m].y = (R)sinl(-2 * pi * m / Q);
-  }
+  const std::vector<Cx<R>> tw = tables<R>(Q);
   Cx<R>*dd, *dt;
   cudaMalloc(&dd, n * sizeof(Cx<R>));
-  cudaMalloc(&dt, Q * sizeof(Cx<R>));
+  cudaMalloc(&dt, tw.size() * sizeof(Cx<R>));
   cudaMemcpy(dd, h.data(), n * sizeof(Cx<R>), cudaMemcpyHostToDevice);
-  cudaMemcpy(dt, tw.data(), Q * sizeof(Cx<R>), cudaMemcpyHostToDevice);
-  const size_t smem = NA * padded_len(L) * sizeof(Cx<R>);
-  cudaFuncSetAttribute(kfft<R, Q, L, NA, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kfft<R, Q, L, NA, INV><<<1, threads_for<R, Q>(), smem>>>(dt, dd);
+  cudaMemcpy(dt, tw.data(), tw.size() * sizeof(Cx<R>), cudaMemcpyHostToDevice);
+  const size_t smem = 2 * padded_len(Q) * sizeof(Cx<R>);
+  cudaFuncSetAttribute(kfft<R, Q, HALF, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kfft<R, Q, HALF, INV><<<1, threads_for<R, Q>(), smem>>>(dt, dd);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     printf("CUDA error %s\n", cudaGetErrorString(e));
@@ -56,6 +79,7 @@ double run() {
   }
   std::vector<Cx<R>> o(n);
   cudaMemcpy(o.data(), dd, n * sizeof(Cx<R>), cudaMemcpyDeviceToHost);
+  const long double pi = 3.141592653589793238462643383279502884L;
   long double num = 0, den = 0;
   const long double sg = INV ? 1 : -1;
   for (int a = 0; a < NA; ++a)
@@ -76,15 +100,16 @@ double run() {
   return (double)sqrtl(num / den);
 }
 
-#define T(R, Q, L, NA, INV) \
-  printf("%-6s Q=%5d L=%5d NA=%d inv=%d relL2=%.3e\n", #R, Q, L, NA, INV, run<R, Q, L, NA, INV>());
+#define T(R, Q, HALF, INV) \
+  printf("%-6s Q=%5d half=%d inv=%d relL2=%.3e\n", #R, Q, HALF, INV, run<R, Q, HALF, INV>());
 
 int main() {
-  T(float, 512, 512, 2, false) T(float, 512, 256, 1, false) T(float, 2048, 2048, 2, false)
-  T(float, 2048, 2048, 2, true) T(float, 2048, 1024, 1, false) T(float, 2048, 1024, 1, true)
-  T(float, 4096, 4096, 2, false) T(float, 4096, 2048, 1, true) T(float, 1024, 1024, 2, false)
-  T(float, 1024, 512, 1, false) T(float, 256, 256, 2, false) T(float, 256, 128, 1, false)
-  T(double, 2048, 2048, 2, false) T(double, 2048, 1024, 1, true) T(double, 4096, 4096, 2, true)
-  T(double, 4096, 2048, 1, false) T(double, 512, 512, 2, false) T(double, 256, 128, 1, true)
+  T(float, 256, false, false) T(float, 256, true, false) T(float, 512, false, true)
+  T(float, 512, true, true) T(float, 1024, false, false) T(float, 1024, true, true)
+  T(float, 2048, false, false) T(float, 2048, false, true) T(float, 2048, true, false)
+  T(float, 2048, true, true) T(float, 4096, false, true) T(float, 4096, true, false)
+  T(float, 8192, false, false) T(float, 8192, true, true)
+  T(double, 256, true, true) T(double, 512, false, false) T(double, 2048, false, true)
+  T(double, 2048, true, false) T(double, 4096, false, false) T(double, 4096, true, true)
   return 0;
 }
