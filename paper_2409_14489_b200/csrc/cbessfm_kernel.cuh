@@ -224,6 +224,50 @@ __device__ __forceinline__ void load_row(const Cx<double>* row, Cx<double>* w) {
   }
 }
 
+// ---- distributed shared memory push with transaction barriers (sm_90+)
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t cluster_addr(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}"
+      ::"r"(smem_addr(bar)), "r"(parity)
+      : "memory");
+}
+// 8- or 16-byte store into another CTA's shared memory that completes
+// `bytes` transactions on that CTA's mbarrier.
+__device__ __forceinline__ void push(uint32_t raddr, Cx<float> v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];"
+               ::"r"(raddr), "f"(v.x), "f"(v.y), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void push(uint32_t raddr, Cx<double> v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+               ::"r"(raddr), "d"(v.x), "d"(v.y), "r"(rbar)
+               : "memory");
+}
+
 __device__ __forceinline__ void bar_named(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -499,18 +543,35 @@ __host__ __device__ constexpr int threads_for() {
   return Q / 8;
 }
 
+#ifndef CB_FLOAT_THREADS
+#define CB_FLOAT_THREADS 1024
+#endif
 // Resident CTAs per SM the register budget is sized for.
 template <typename R, int Q>
 __host__ __device__ constexpr int min_blocks() {
-  return (sizeof(R) == 4 ? (Q <= 2048 ? 768 : 1024) : 512) / threads_for<R, Q>() > 1
-             ? (sizeof(R) == 4 ? (Q <= 2048 ? 768 : 1024) : 512) / threads_for<R, Q>()
+  return (sizeof(R) == 4 ? CB_FLOAT_THREADS : 512) / threads_for<R, Q>() > 1
+             ? (sizeof(R) == 4 ? CB_FLOAT_THREADS : 512) / threads_for<R, Q>()
              : 1;
+}
+
+// MIMO slice of CTA c: bins [mimo_lo(c), mimo_lo(c+1)) of the H+1 rfft bins.
+__host__ __device__ constexpr int mimo_lo(int c, int P, int H) { return (c * (H + 1)) / P; }
+__host__ __device__ constexpr int mimo_slice_max(int P, int H) { return (H + 1 + P - 1) / P; }
+
+// RB (P > 1) receives the P intensity-spectrum slices this CTA's MIMO
+// needs; IS + RB also stage one polarisation row in the outer exchanges.
+template <int Q>
+__host__ __device__ constexpr int rb_len(int P) {
+  return P * mimo_slice_max(P, Q / 2) > padded_len(Q) - padded_len(Q / 2 + 1)
+             ? P * mimo_slice_max(P, Q / 2)
+             : padded_len(Q) - padded_len(Q / 2 + 1);
 }
 
 template <typename R, int Q>
 __host__ __device__ constexpr size_t smem_bytes(int P) {
-  // F: 2 padded polarisation rows; IS, TS: padded spectra (Q/2+1 bins)
-  return sizeof(Cx<R>) * (size_t)(2 * padded_len(Q) + (P > 1 ? 2 : 1) * padded_len(Q / 2 + 1));
+  // F: 2 padded polarisation rows; IS: padded spectrum (Q/2+1 bins)
+  return sizeof(Cx<R>) *
+         (size_t)(2 * padded_len(Q) + padded_len(Q / 2 + 1) + (P > 1 ? rb_len<Q>(P) : 0));
 }
 
 // Position of global FFT bin g (of N = P*Q) in the subband layout:
@@ -535,10 +596,23 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Cx<R>* F = reinterpret_cast<Cx<R>*>(smem_raw);
   Cx<R>* IS = F + 2 * SF;
-  Cx<R>* TS = (P > 1) ? IS + padded_len(H + 1) : IS;
+  // TS (theta_hat, then theta) reuses IS: a remote CTA writes bin k of it
+  // only after it received this CTA's I_hat[k], whose computation was the
+  // last read of IS[k] (the untangle reads each slot once)
+  Cx<R>* TS = IS;
+  Cx<R>* RB = IS + padded_len(H + 1);  // P > 1 only
+  constexpr int SLM = mimo_slice_max(P, H);
 
   __shared__ int s_zero;
-  if (threadIdx.x == 0) s_zero = 0;
+  __shared__ uint64_t s_bar[2];  // [0]: intensity slices in RB, [1]: theta_hat in TS
+  if (threadIdx.x == 0) {
+    s_zero = 0;
+    if constexpr (P > 1) {
+      mbar_init(&s_bar[0], 1);
+      mbar_init(&s_bar[1], 1);
+      mbar_init_fence();
+    }
+  }
   const int tid = threadIdx.x;
   const int rank = (P > 1) ? (int)(blockIdx.x % P) : 0;
   const int64_t cid = prm.cid0 + blockIdx.x / P;
@@ -588,7 +662,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
     const int lo = (rank * Q) / P, hi = ((rank + 1) * Q) / P;
     const R invP = (R)1 / (R)P;
     const Cx<R>* ph0 = prm.phasor + (size_t)prm.ph_index[0] * ph_tab;
-    Cx<R>* S = IS;  // staging: padded_len(Q) entries fit in IS + TS
+    Cx<R>* S = IS;  // staging: padded_len(Q) entries fit in IS + RB
     cluster.sync();
     for (int pol = 0; pol < 2; ++pol) {
       for (int k2 = lo + tid; k2 < hi; k2 += NT) {
@@ -631,12 +705,32 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
     fft2<R, Q, NT, true, NoHook, IntensityHook<R>>(F, twpQ, &s_zero, NoHook(), ih);
     fft1<R, Q, H, NT, false>(IS, twpH, &s_zero);
 
-    // r2c untangle in place: I_hat[k], k = 0..H  (numpy rfft, dbp.py:194)
+    // r2c untangle: I_hat[k], k = 0..H (numpy rfft, dbp.py:194). For P > 1
+    // each bin goes straight from registers to the CTA whose MIMO slice
+    // holds it (st.async into its RB, completing on its mbarrier); for
+    // P == 1 it is written back in place.
+    if constexpr (P > 1) {
+      if (tid == 0) {
+        const int len = mimo_lo(rank + 1, P, H) - mimo_lo(rank, P, H);
+        mbar_expect(&s_bar[0], (uint32_t)(P * len * sizeof(Cx<R>)));
+        mbar_expect(&s_bar[1], (uint32_t)((H + 1) * sizeof(Cx<R>)));
+      }
+    }
+    auto emit = [&](int k, Cx<R> v) {
+      if constexpr (P > 1) {
+        int c = (k * P) / (H + 1);
+        if (mimo_lo(c + 1, P, H) <= k) ++c;
+        const uint32_t dst = cluster_addr(smem_addr(RB + rank * SLM + (k - mimo_lo(c, P, H))), c);
+        push(dst, v, cluster_addr(smem_addr(&s_bar[0]), c));
+      } else {
+        IS[pad(k)] = v;
+      }
+    };
     for (int k = tid; k <= H / 2; k += NT) {
       if (k == 0) {
         const Cx<R> z = IS[pad(0)];
-        IS[pad(0)] = mk(z.x + z.y, (R)0);
-        IS[pad(H)] = mk(z.x - z.y, (R)0);
+        emit(0, mk(z.x + z.y, (R)0));
+        emit(H, mk(z.x - z.y, (R)0));
       } else {
         const Cx<R> a = IS[pad(k)];
         const Cx<R> bq = conj(IS[pad(H - k)]);
@@ -644,36 +738,36 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
         const Cx<R> dd = a - bq;                           // 2i * O[k]
         const Cx<R> o = mk(dd.y * (R)0.5, -dd.x * (R)0.5); // O[k]
         const Cx<R> wo = cmul(o, ldg(twQ + k));
-        IS[pad(k)] = e + wo;
-        if (k != H - k) IS[pad(H - k)] = conj(e - wo);
+        emit(k, e + wo);
+        if (k != H - k) emit(H - k, conj(e - wo));
       }
     }
 
     // MIMO coupling (dbp.py:195): theta_hat_i[k] = sum_l T[i,l,k] I_hat_l[k]
     if constexpr (P > 1) {
-      cg::cluster_group cluster = cg::this_cluster();
-      cluster.sync();
-      const int lo = (rank * (H + 1)) / P, hi = ((rank + 1) * (H + 1)) / P;
+      const int lo = mimo_lo(rank, P, H), hi = mimo_lo(rank + 1, P, H);
+      const uint32_t ts_local = smem_addr(TS);
+      const uint32_t bar_t = smem_addr(&s_bar[1]);
       for (int k = lo + tid; k < hi; k += NT) {
-        Cx<R> iv[P], sv[P];
+        Cx<R> sv[P];
 #pragma unroll
-        for (int l = 0; l < P; ++l) {
-          const Cx<R>* ri = cluster.map_shared_rank(IS, l);
-          iv[l] = ri[pad(k)];
-          sv[l] = ldg(prm.mimo + (size_t)l * (H + 1) + k);
-        }
+        for (int l = 0; l < P; ++l) sv[l] = ldg(prm.mimo + (size_t)l * (H + 1) + k);
+        mbar_wait(&s_bar[0], st & 1);
+        Cx<R> iv[P];
+#pragma unroll
+        for (int l = 0; l < P; ++l) iv[l] = RB[l * SLM + (k - lo)];
 #pragma unroll
         for (int i = 0; i < P; ++i) {
-          Cx<R> s = mk((R)0, (R)0);
+          Cx<R> acc = mk((R)0, (R)0);
 #pragma unroll
           for (int l = 0; l < P; ++l) {
-            s = s + (l >= i ? cmul(sv[l - i], iv[l]) : cmul(conj(sv[i - l]), iv[l]));
+            acc = acc + (l >= i ? cmul(sv[l - i], iv[l]) : cmul(conj(sv[i - l]), iv[l]));
           }
-          Cx<R>* dst = cluster.map_shared_rank(TS, i);
-          dst[pad(k)] = s;
+          push(cluster_addr(ts_local + (uint32_t)(pad(k) * sizeof(Cx<R>)), i), acc,
+               cluster_addr(bar_t, i));
         }
       }
-      cluster.sync();
+      mbar_wait(&s_bar[1], st & 1);
     } else {
       __syncthreads();
       for (int k = tid; k <= H; k += NT) TS[pad(k)] = cmul(ldg(prm.mimo + k), IS[pad(k)]);
