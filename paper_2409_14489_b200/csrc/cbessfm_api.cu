@@ -56,12 +56,14 @@ std::vector<double> pass_tables(int Q, const std::vector<double>& tq) {
   using cbessfm::pass_radix;
   using cbessfm::twp_offset;
   using cbessfm::twp_size;
-  std::vector<double> out(2 * (size_t)(twp_size(Q) + twp_size(Q / 2)), 0.0);
-  auto fill = [&](int L, size_t base) {
-    for (int ns = 1; ns < L; ns *= pass_radix(L, ns)) {
-      const int R = pass_radix(L, ns);
+  using cbessfm::kMaxRad;
+  using cbessfm::kMaxRadHalf;
+  std::vector<double> out(2 * (size_t)(twp_size(Q) + twp_size(Q / 2, kMaxRadHalf)), 0.0);
+  auto fill = [&](int L, size_t base, int maxrad) {
+    for (int ns = 1; ns < L; ns *= pass_radix(L, ns, maxrad)) {
+      const int R = pass_radix(L, ns, maxrad);
       if (ns == 1) continue;
-      const size_t off = base + twp_offset(L, ns);
+      const size_t off = base + twp_offset(L, ns, maxrad);
       for (int k = 0; k < ns; ++k)
         for (int r = 0; r < R; ++r) {
           const int64_t e = ((int64_t)r * k * (Q / (ns * R))) % Q;
@@ -70,8 +72,8 @@ std::vector<double> pass_tables(int Q, const std::vector<double>& tq) {
         }
     }
   };
-  fill(Q, 0);
-  fill(Q / 2, twp_size(Q));
+  fill(Q, 0, kMaxRad);
+  fill(Q / 2, twp_size(Q), kMaxRadHalf);
   return out;
 }
 

@@ -188,18 +188,24 @@ __device__ __forceinline__ void dft_reg(Cx<R>* v) {
 // consecutive k read consecutive rows with 16-byte vector loads (fully
 // coalesced), instead of R-1 scattered 8-byte loads.
 
+// The two-polarisation field FFTs run radix-8 passes (one butterfly of x
+// and of y per thread); the half-length real-transform FFTs run radix-4
+// passes, which keeps all Q/8 threads busy on Q/2 points.
 constexpr int kMaxRad = 8;
+constexpr int kMaxRadHalf = 4;
 
-__host__ __device__ constexpr int pass_radix(int L, int ns) {
-  return L / ns >= kMaxRad ? kMaxRad : L / ns;
+__host__ __device__ constexpr int pass_radix(int L, int ns, int maxrad = kMaxRad) {
+  return L / ns >= maxrad ? maxrad : L / ns;
 }
-__host__ __device__ constexpr int twp_offset(int L, int NS) {
+__host__ __device__ constexpr int twp_offset(int L, int NS, int maxrad = kMaxRad) {
   int s = 0;
-  for (int ns = 1; ns < NS; ns *= pass_radix(L, ns))
-    if (ns > 1) s += ns * pass_radix(L, ns);
+  for (int ns = 1; ns < NS; ns *= pass_radix(L, ns, maxrad))
+    if (ns > 1) s += ns * pass_radix(L, ns, maxrad);
   return s;
 }
-__host__ __device__ constexpr int twp_size(int L) { return twp_offset(L, L); }
+__host__ __device__ constexpr int twp_size(int L, int maxrad = kMaxRad) {
+  return twp_offset(L, L, maxrad);
+}
 
 // Load the twiddle row of butterfly k (RAD entries, entry 0 unused).
 template <int RAD>
@@ -363,16 +369,57 @@ struct RotationHook : NoHook {
 
 // Two-polarisation pass: thread j runs butterfly j of x AND of y, sharing
 // the index arithmetic and the twiddle row.
-template <typename R, int Q, int NT, int NS, bool INV, bool FIRST, bool LAST, class Hook>
+// Butterfly run by thread slot t in a pass. The radix-4 pass with NS = 4
+// scatters to 16*(j/4) + j%4 + 4r, a 4-way bank conflict for consecutive
+// j; permuting j inside each 64-butterfly group as below makes both its
+// loads and its stores conflict-free (tests/test_host_logic.py checks the
+// bank mapping). All other passes keep j = t.
+template <int L, int NS, int RAD>
+__host__ __device__ constexpr int bfly(int t) {
+  if constexpr (RAD == 4 && NS == 4 && (L / RAD) % 64 == 0) {
+    return (t & ~63) | ((t & 15) << 2) | ((t >> 4) & 3);
+  } else {
+    return t;
+  }
+}
+
+// Twiddle rows of the butterflies a thread runs in the pass with
+// sub-transform size NS of a length-L FFT (PER butterflies of radix RAD).
+template <typename R, int L, int NT, int NS, int MAXRAD>
+struct PassRows {
+  static constexpr bool kLast = NS >= L;
+  static constexpr int RAD = kLast ? 1 : pass_radix(L, NS, MAXRAD);
+  static constexpr int PER = kLast ? 1 : ((L / RAD) >= NT ? (L / RAD) / NT : 1);
+  static constexpr bool kHas = !kLast && NS > 1;
+  Cx<R> w[PER][RAD];
+  // Issue the loads (no use yet): called one pass early so the L2 latency
+  // overlaps the current pass's stores, its barrier and the next pass's
+  // shared-memory loads.
+  __device__ __forceinline__ void fetch(const Cx<R>* twp) {
+    if constexpr (kHas) {
+      const Cx<R>* tw = twp + twp_offset(L, NS, MAXRAD);
+      const int tid = threadIdx.x;
+#pragma unroll
+      for (int p = 0; p < PER; ++p) {
+        const int t = tid + p * NT;
+        const int j = bfly<L, NS, RAD>(t);
+        if ((L / RAD) >= NT || t < L / RAD) load_row<RAD>(tw + (j % NS) * RAD, w[p]);
+      }
+    }
+  }
+};
+
+template <typename R, int Q, int NT, int NS, bool INV, bool FIRST, bool LAST, class Hook,
+          class Rows, class NextRows>
 __device__ __forceinline__ void fft2_pass(Cx<R>* __restrict__ F, const Cx<R>* __restrict__ twp,
-                                          const volatile int* zero, Hook& hook) {
+                                          const volatile int* zero, Hook& hook, Rows& rows,
+                                          NextRows& next) {
   constexpr int RAD = pass_radix(Q, NS);
   constexpr int LR = Q / RAD;
   constexpr int NB = Q / RAD;
   static_assert(NB % NT == 0, "butterflies must tile the block");
   constexpr int PER = NB / NT;
   constexpr int SF = padded_len(Q);
-  const Cx<R>* tw = twp + twp_offset(Q, NS);
   Cx<R> vx[PER][RAD], vy[PER][RAD];
   const int tid = threadIdx.x + *zero;
 #pragma unroll
@@ -386,12 +433,10 @@ __device__ __forceinline__ void fft2_pass(Cx<R>* __restrict__ F, const Cx<R>* __
     }
     if constexpr (FIRST) hook.template pre<R, RAD, LR>(j, vx[p], vy[p]);
     if constexpr (NS > 1) {
-      Cx<R> w[RAD];
-      load_row<RAD>(tw + (j % NS) * RAD, w);
 #pragma unroll
       for (int r = 1; r < RAD; ++r) {
-        vx[p][r] = INV ? cmulc(vx[p][r], w[r]) : cmul(vx[p][r], w[r]);
-        vy[p][r] = INV ? cmulc(vy[p][r], w[r]) : cmul(vy[p][r], w[r]);
+        vx[p][r] = INV ? cmulc(vx[p][r], rows.w[p][r]) : cmul(vx[p][r], rows.w[p][r]);
+        vy[p][r] = INV ? cmulc(vy[p][r], rows.w[p][r]) : cmul(vy[p][r], rows.w[p][r]);
       }
     }
     dft_reg<R, RAD, INV>(vx[p]);
@@ -410,26 +455,29 @@ __device__ __forceinline__ void fft2_pass(Cx<R>* __restrict__ F, const Cx<R>* __
       bx[SF + pad(r * NS)] = vy[p][bitrev<RAD>(r)];
     }
   }
+  next.fetch(twp);
   __syncthreads();
 }
 
 template <typename R, int Q, int NT, int NS, bool INV, class Pre, class Post>
 struct Fft2Run {
+  using Rows = PassRows<R, Q, NT, NS, kMaxRad>;
   static __device__ __forceinline__ void run(Cx<R>* F, const Cx<R>* twp, const volatile int* z,
-                                             Pre& pre, Post& post) {
+                                             Pre& pre, Post& post, Rows& rows) {
     constexpr int RAD = pass_radix(Q, NS);
     constexpr bool FIRST = NS == 1, LAST = NS * RAD == Q;
+    PassRows<R, Q, NT, NS * RAD, kMaxRad> next;
     if constexpr (FIRST && LAST) {
       static_assert(!(FIRST && LAST), "single-pass transforms are not used");
     } else if constexpr (FIRST) {
-      fft2_pass<R, Q, NT, NS, INV, true, false>(F, twp, z, pre);
+      fft2_pass<R, Q, NT, NS, INV, true, false>(F, twp, z, pre, rows, next);
     } else if constexpr (LAST) {
-      fft2_pass<R, Q, NT, NS, INV, false, true>(F, twp, z, post);
+      fft2_pass<R, Q, NT, NS, INV, false, true>(F, twp, z, post, rows, next);
     } else {
       NoHook none;
-      fft2_pass<R, Q, NT, NS, INV, false, false>(F, twp, z, none);
+      fft2_pass<R, Q, NT, NS, INV, false, false>(F, twp, z, none, rows, next);
     }
-    if constexpr (!LAST) Fft2Run<R, Q, NT, NS * RAD, INV, Pre, Post>::run(F, twp, z, pre, post);
+    if constexpr (!LAST) Fft2Run<R, Q, NT, NS * RAD, INV, Pre, Post>::run(F, twp, z, pre, post, next);
   }
 };
 
@@ -439,7 +487,8 @@ struct Fft2Run {
 template <typename R, int Q, int NT, bool INV, class Pre = NoHook, class Post = NoHook>
 __device__ __forceinline__ void fft2(Cx<R>* F, const Cx<R>* twp, const volatile int* z,
                                      Pre pre = Pre(), Post post = Post()) {
-  Fft2Run<R, Q, NT, 1, INV, Pre, Post>::run(F, twp, z, pre, post);
+  PassRows<R, Q, NT, 1, kMaxRad> none;
+  Fft2Run<R, Q, NT, 1, INV, Pre, Post>::run(F, twp, z, pre, post, none);
 }
 
 // Single-array pass for the half-length real-transform FFTs. Passes with
@@ -447,21 +496,18 @@ __device__ __forceinline__ void fft2(Cx<R>* F, const Cx<R>* twp, const volatile 
 // synchronise between load and store with a named barrier, and a full
 // barrier ends the pass so no warp runs ahead into a later pass whose named
 // barrier expects a different thread count.
-template <typename R, int Q, int L, int NT, int NS, bool INV>
+template <typename R, int Q, int L, int NT, int NS, bool INV, class Rows, class NextRows>
 __device__ __forceinline__ void fft1_pass(Cx<R>* __restrict__ buf, const Cx<R>* __restrict__ twp,
-                                          const volatile int* zero) {
-  constexpr int RAD = pass_radix(L, NS);
+                                          const volatile int* zero, Rows& rows, NextRows& next) {
+  constexpr int RAD = pass_radix(L, NS, kMaxRadHalf);
   constexpr int LR = L / RAD;
   constexpr int NB = L / RAD;
-  const Cx<R>* tw = twp + twp_offset(L, NS);
   const int tid = threadIdx.x + *zero;
-  auto body_load = [&](int j, Cx<R>* v) {
+  auto body_load = [&](int j, Cx<R>* v, const Cx<R>* w) {
     const Cx<R>* b = buf + pad(j);
 #pragma unroll
     for (int r = 0; r < RAD; ++r) v[r] = b[pad(r * LR)];
     if constexpr (NS > 1) {
-      Cx<R> w[RAD];
-      load_row<RAD>(tw + (j % NS) * RAD, w);
 #pragma unroll
       for (int r = 1; r < RAD; ++r) v[r] = INV ? cmulc(v[r], w[r]) : cmul(v[r], w[r]);
     }
@@ -477,39 +523,51 @@ __device__ __forceinline__ void fft1_pass(Cx<R>* __restrict__ buf, const Cx<R>* 
     constexpr int PER = NB / NT;
     Cx<R> v[PER][RAD];
 #pragma unroll
-    for (int p = 0; p < PER; ++p) body_load(tid + p * NT, v[p]);
+    for (int p = 0; p < PER; ++p) body_load(bfly<L, NS, RAD>(tid + p * NT), v[p], rows.w[p]);
     __syncthreads();
 #pragma unroll
-    for (int p = 0; p < PER; ++p) body_store(tid + p * NT, v[p]);
+    for (int p = 0; p < PER; ++p) body_store(bfly<L, NS, RAD>(tid + p * NT), v[p]);
+    next.fetch(twp);
     __syncthreads();
   } else {
-    constexpr int ACT = (NB + 31) / 32 * 32;  // active threads, whole warps
+    // fewer butterflies than threads: the leading whole warps run the pass
+    // and synchronise between load and store with a named barrier; the full
+    // barrier at the end keeps any warp from running ahead into a later
+    // pass whose named barrier expects a different thread count
+    constexpr int ACT = (NB + 31) / 32 * 32;
     if (tid < ACT) {
       Cx<R> v[RAD];
       const bool on = (NB % 32 == 0) || tid < NB;
-      if (on) body_load(tid, v);
+      if (on) body_load(tid, v, rows.w[0]);
       bar_named(1, ACT);
       if (on) body_store(tid, v);
     }
+    next.fetch(twp);
     __syncthreads();
   }
 }
 
 template <typename R, int Q, int L, int NT, int NS, bool INV>
 struct Fft1Run {
-  static __device__ __forceinline__ void run(Cx<R>* buf, const Cx<R>* twp, const volatile int* z) {
-    fft1_pass<R, Q, L, NT, NS, INV>(buf, twp, z);
-    Fft1Run<R, Q, L, NT, NS * pass_radix(L, NS), INV>::run(buf, twp, z);
+  using Rows = PassRows<R, L, NT, NS, kMaxRadHalf>;
+  static __device__ __forceinline__ void run(Cx<R>* buf, const Cx<R>* twp, const volatile int* z,
+                                             Rows& rows) {
+    constexpr int NS2 = NS * pass_radix(L, NS, kMaxRadHalf);
+    PassRows<R, L, NT, NS2, kMaxRadHalf> next;
+    fft1_pass<R, Q, L, NT, NS, INV>(buf, twp, z, rows, next);
+    Fft1Run<R, Q, L, NT, NS2, INV>::run(buf, twp, z, next);
   }
 };
 template <typename R, int Q, int L, int NT, bool INV>
 struct Fft1Run<R, Q, L, NT, L, INV> {
-  static __device__ __forceinline__ void run(Cx<R>*, const Cx<R>*, const volatile int*) {}
+  static __device__ __forceinline__ void run(Cx<R>*, const Cx<R>*, const volatile int*,
+                                             PassRows<R, L, NT, L, kMaxRadHalf>&) {}
 };
 
 template <typename R, int Q, int L, int NT, bool INV>
 __device__ __forceinline__ void fft1(Cx<R>* buf, const Cx<R>* twp, const volatile int* z) {
-  Fft1Run<R, Q, L, NT, 1, INV>::run(buf, twp, z);
+  PassRows<R, L, NT, 1, kMaxRadHalf> none;
+  Fft1Run<R, Q, L, NT, 1, INV>::run(buf, twp, z, none);
 }
 
 // ------------------------------------------------------------------------
@@ -531,7 +589,7 @@ struct Params {
   const R* theta_scale;    // [n_steps], carries 1/Q
   const Cx<R>* twQ;        // [Q]   exp(-2 pi i m / Q)
   const Cx<R>* twN;        // [P*Q] exp(-2 pi i m / (P Q))
-  const Cx<R>* twp;        // per-pass rows: [twp_size(Q)] then [twp_size(Q/2)]
+  const Cx<R>* twp;        // per-pass rows: [twp_size(Q)] then [twp_size(Q/2, 4)]
   int n_steps;
   int64_t cid0;            // first cluster index of this launch chunk
 };

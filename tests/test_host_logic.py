@@ -197,3 +197,37 @@ def test_oracle_is_not_imported_by_the_product():
     for f in pkg.rglob("*.py"):
         assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)",
                                           f.read_text(), re.M), f
+
+
+def _bank_ways(addrs):
+    """Max distinct 4-byte words per bank over the two 16-lane phases of a
+    warp's 8-byte shared access."""
+    worst = 1
+    for ph in (addrs[:16], addrs[16:]):
+        banks = {}
+        for a in ph:
+            for w in (2 * a, 2 * a + 1):
+                banks.setdefault(w % 32, set()).add(w)
+        worst = max(worst, max(len(v) for v in banks.values()))
+    return worst
+
+
+def test_fft1_ns4_butterfly_permutation_is_conflict_free():
+    # csrc/cbessfm_kernel.cuh bfly(): radix-4 pass with NS = 4 of the
+    # half-length FFT; identity mapping is 4-way conflicted on stores
+    pad = lambda i: i + (i >> 4)
+    for L, NT in ((1024, 256), (2048, 512), (512, 128)):
+        R, ns, LR = 4, 4, L // 4
+        def ways(sigma):
+            worst = 1
+            for w0 in range(0, NT, 32):
+                js = np.array([sigma(t) for t in range(w0, w0 + 32)])
+                for r in range(R):
+                    worst = max(worst, _bank_ways([pad(int(j) + r * LR) for j in js]))
+                    d0 = (js // ns) * ns * R + js % ns
+                    worst = max(worst, _bank_ways([pad(int(d) + r * ns) for d in d0]))
+            return worst
+        perm = lambda t: (t & ~63) | ((t & 15) << 2) | ((t >> 4) & 3)
+        assert sorted(perm(t) for t in range(NT)) == list(range(NT))
+        assert ways(lambda t: t) == 4
+        assert ways(perm) == 1

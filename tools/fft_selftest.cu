@@ -31,21 +31,21 @@ __global__ void __launch_bounds__(threads_for<R, Q>()) kfft(const Cx<R>* twp, Cx
 template <typename R>
 std::vector<Cx<R>> tables(int Q) {
   const long double pi = 3.141592653589793238462643383279502884L;
-  std::vector<Cx<R>> out(twp_size(Q) + twp_size(Q / 2));
-  auto fill = [&](int L, int base) {
-    for (int ns = 1; ns < L; ns *= pass_radix(L, ns)) {
-      const int Rr = pass_radix(L, ns);
+  std::vector<Cx<R>> out(twp_size(Q) + twp_size(Q / 2, kMaxRadHalf));
+  auto fill = [&](int L, int base, int mr) {
+    for (int ns = 1; ns < L; ns *= pass_radix(L, ns, mr)) {
+      const int Rr = pass_radix(L, ns, mr);
       if (ns == 1) continue;
       for (int k = 0; k < ns; ++k)
         for (int r = 0; r < Rr; ++r) {
           const long long e = (long long)r * k * (Q / (ns * Rr)) % Q;
-          out[base + twp_offset(L, ns) + k * Rr + r].x = (R)cosl(-2 * pi * e / Q);
-          out[base + twp_offset(L, ns) + k * Rr + r].y = (R)sinl(-2 * pi * e / Q);
+          out[base + twp_offset(L, ns, mr) + k * Rr + r].x = (R)cosl(-2 * pi * e / Q);
+          out[base + twp_offset(L, ns, mr) + k * Rr + r].y = (R)sinl(-2 * pi * e / Q);
         }
     }
   };
-  fill(Q, 0);
-  fill(Q / 2, twp_size(Q));
+  fill(Q, 0, kMaxRad);
+  fill(Q / 2, twp_size(Q), kMaxRadHalf);
   return out;
 }
 
