@@ -336,6 +336,28 @@ def main():
                "d2h_bytes_per_step": int(hout.numel() * hout.element_size()),
                "path": "DbpEngine.run_host: pinned host -> H2D -> fused kernel -> D2H"}
 
+    # the only collective of the path: final gather of the kept samples to
+    # every rank (all_gather over NCCL), timed separately from `value`
+    gather = None
+    if dist is not None:
+        flat = torch.view_as_real(out).reshape(-1)
+        allg = torch.empty(world * flat.numel(), dtype=flat.dtype, device=dev)
+        for _ in range(3):
+            dist.all_gather_into_tensor(allg, flat)
+        barrier()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(10):
+            dist.all_gather_into_tensor(allg, flat)
+        g1.record(stream)
+        barrier()
+        tg = torch.tensor([g0.elapsed_time(g1) / 10], device=dev, dtype=torch.float64)
+        dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+        gather = {"ms": float(tg.item()), "bytes_per_rank": int(flat.numel() * flat.element_size()),
+                  "collective": "all_gather_into_tensor (NCCL)",
+                  "value_with_gather": sym_per_step / ((per_step_ms + float(tg.item())) * 1e-3)}
+
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -376,7 +398,7 @@ def main():
             "data": "synthetic (seeded band-limited Gaussian WDM, configs[1] grid)",
             "config": config_block(args, world), "impl": "ours",
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": args.steps, "clocks": clocks,
+            "gpu_launches": args.steps, "clocks": clocks, "gather": gather,
             "kernel": {"name": "cbessfm_block_kernel<float,5,2048>" if args.dtype == "c64"
                        else "cbessfm_block_kernel<double,5,2048>",
                        "plan": {k: getattr(eng.plan.info(), k) for k in

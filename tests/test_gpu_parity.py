@@ -162,3 +162,21 @@ def test_counter_hook_matches_reference_cost(cuda):
     closed = pb.cb_essfm_cost(g.cfg.block_size, g.cfg.overlap,
                               g.cfg.oversampling, g.cfg.n_steps, 5)
     assert rep.rm_per_2d >= closed.rm_per_2d
+
+
+def test_gpu_compute_time_shards_reassemble(cuda):
+    # the product's per-rank compute of distributed.run_distributed, run for
+    # both ranks of a world of 2 in one process (no collective needed here)
+    from paper_2409_14489_b200.distributed import gpu_compute, shard_work
+    from paper_2409_14489_b200.planner import gather_slice
+    g = golden("cfg2_nsb5")
+    x = np.vstack([g.wave.x, g.wave.y])[None]
+    n = x.shape[-1]
+    eng = pb.DbpEngine(g.cfg, g.coeffs, g.wave.sample_rate, dtype="c128")
+    run = gpu_compute(eng)
+    out = np.zeros_like(x)
+    for rank in range(2):
+        w = shard_work(n, g.cfg.block_size, g.cfg.overlap, 1, 2, rank)
+        xs = gather_slice(x, w.in_origin, w.in_length)
+        out[:, :, w.out_begin:w.out_end] = run(xs, w, n)
+    assert rel_rms(out[0], g.out) < 1e-12
