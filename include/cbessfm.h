@@ -123,6 +123,11 @@ cbessfm_status cbessfm_run(const cbessfm_plan* plan, const cbessfm_io* io, void*
 /* Free the plan's device tables. */
 cbessfm_status cbessfm_plan_destroy(cbessfm_plan* plan);
 
+/* Debug: copy up to n phase timestamps (clock64) of CTA 0 of the last
+ * launch into out. Only builds compiled with -DCB_PHASE_PROFILE record
+ * them; other builds return 0. */
+int32_t cbessfm_debug_phase_times(const cbessfm_plan* plan, int64_t* out, int32_t n);
+
 /* Message of the last failing call on this thread ("" if none). */
 const char* cbessfm_last_error(void);
 

@@ -59,6 +59,7 @@ SIGNATURES = {
     "cbessfm_run": (C.c_int, [C.c_void_p, C.POINTER(Io), C.c_void_p]),
     "cbessfm_plan_destroy": (C.c_int, [C.c_void_p]),
     "cbessfm_last_error": (C.c_char_p, []),
+    "cbessfm_debug_phase_times": (C.c_int32, [C.c_void_p, C.POINTER(C.c_int64), C.c_int32]),
     # include/cbessfm_peaks.h
     "cbessfm_fma_peak": (C.c_double, [C.c_int32, C.c_double]),
 }

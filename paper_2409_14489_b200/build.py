@@ -55,8 +55,14 @@ def _compile(args):
     return obj, None
 
 
-def build(jobs: int | None = None, verbose: bool = False) -> Path:
-    """Compile (incrementally) and link libcbessfm.so; returns its path."""
+def build(jobs: int | None = None, verbose: bool = False, profile: bool = False) -> Path:
+    """Compile (incrementally) and link libcbessfm.so; returns its path.
+    profile=True builds the phase-clock debug variant libcbessfm_prof.so."""
+    global BUILD, LIB
+    if profile:
+        BUILD = BUILD.parent / "cbessfm_prof"
+        LIB = PKG / "libcbessfm_prof.so"
+        FLAGS.append("-DCB_PHASE_PROFILE")
     BUILD.mkdir(parents=True, exist_ok=True)
     jobs = jobs or max(1, min(len(REALS) * len(SUBBANDS) + 1, os.cpu_count() or 1))
     tasks = []
@@ -88,5 +94,5 @@ def build(jobs: int | None = None, verbose: bool = False) -> Path:
 
 
 if __name__ == "__main__":
-    build(verbose=True)
+    build(verbose=True, profile="--profile" in sys.argv)
     sys.exit(0)

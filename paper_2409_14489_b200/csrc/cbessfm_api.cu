@@ -53,17 +53,14 @@ std::vector<double> twiddles(int64_t n) {
 // the layout cbessfm_kernel.cuh reads (twp_offset / pass_radix): row k of
 // the pass with sub-transform size ns holds W_Q^(r*k*Q/(ns*R)), r < R.
 std::vector<double> pass_tables(int Q, const std::vector<double>& tq) {
-  using cbessfm::pass_radix;
-  using cbessfm::twp_offset;
-  using cbessfm::twp_size;
-  using cbessfm::kMaxRad;
-  using cbessfm::kMaxRadHalf;
-  std::vector<double> out(2 * (size_t)(twp_size(Q) + twp_size(Q / 2, kMaxRadHalf)), 0.0);
-  auto fill = [&](int L, size_t base, int maxrad) {
-    for (int ns = 1; ns < L; ns *= pass_radix(L, ns, maxrad)) {
-      const int R = pass_radix(L, ns, maxrad);
+  using namespace cbessfm;
+  std::vector<double> out(2 * (size_t)twp_total(Q), 0.0);
+  auto fill = [&](int L, int sched) {
+    const size_t base = twp_base(Q, sched);
+    for (int ns = 1; ns < L; ns *= sched_radix(L, ns, sched)) {
+      const int R = sched_radix(L, ns, sched);
       if (ns == 1) continue;
-      const size_t off = base + twp_offset(L, ns, maxrad);
+      const size_t off = base + twp_offset(L, ns, sched);
       for (int k = 0; k < ns; ++k)
         for (int r = 0; r < R; ++r) {
           const int64_t e = ((int64_t)r * k * (Q / (ns * R))) % Q;
@@ -72,8 +69,9 @@ std::vector<double> pass_tables(int Q, const std::vector<double>& tq) {
         }
     }
   };
-  fill(Q, 0, kMaxRad);
-  fill(Q / 2, twp_size(Q), kMaxRadHalf);
+  fill(Q, kTail);
+  fill(Q, kHead);
+  fill(Q / 2, kHalf);
   return out;
 }
 
@@ -88,6 +86,7 @@ struct cbessfm_plan {
   void* twQ = nullptr;     // [Q]
   void* twN = nullptr;     // [P*Q]
   void* twp = nullptr;     // per-pass twiddle rows
+  long long* dbg = nullptr;  // phase clocks (CB_PHASE_PROFILE builds)
 };
 
 namespace {
@@ -195,6 +194,11 @@ cbessfm_status upload_all(cbessfm_plan* p, const cbessfm_desc* d) {
   const std::vector<double> tp = pass_tables(p->Q, tq);
   if ((e = upload_complex<R>(tp.data(), tp.size() / 2, &p->twp, true)) != cudaSuccess)
     return cuda_fail(e, "upload pass twiddles");
+#ifdef CB_PHASE_PROFILE
+  if ((e = cudaMalloc((void**)&p->dbg, 256 * sizeof(long long))) != cudaSuccess)
+    return cuda_fail(e, "alloc phase clocks");
+  cudaMemset(p->dbg, 0, 256 * sizeof(long long));
+#endif
   return CBESSFM_OK;
 }
 
@@ -207,6 +211,7 @@ void free_plan(cbessfm_plan* p) {
   cudaFree(p->twQ);
   cudaFree(p->twN);
   cudaFree(p->twp);
+  cudaFree(p->dbg);
   delete p;
 }
 
@@ -263,6 +268,7 @@ cbessfm::Params<R> make_params(const cbessfm_plan* p, const cbessfm_io* io) {
   prm.twp = reinterpret_cast<const C*>(p->twp);
   prm.n_steps = p->n_steps;
   prm.cid0 = 0;
+  prm.dbg = p->dbg;
   return prm;
 }
 
@@ -390,5 +396,13 @@ cbessfm_status cbessfm_plan_destroy(cbessfm_plan* p) {
 }
 
 const char* cbessfm_last_error(void) { return g_err.c_str(); }
+
+int32_t cbessfm_debug_phase_times(const cbessfm_plan* p, int64_t* out, int32_t n) {
+  if (!p || !out || !p->dbg) return 0;
+  if (n > 256) n = 256;
+  return cudaMemcpy(out, p->dbg, sizeof(long long) * n, cudaMemcpyDeviceToHost) == cudaSuccess
+             ? n
+             : -1;
+}
 
 }  // extern "C"

@@ -40,6 +40,19 @@ namespace cbessfm {
 
 namespace cg = cooperative_groups;
 
+// Phase timestamps of CTA 0 (debug builds with -DCB_PHASE_PROFILE only;
+// read back with cbessfm_debug_phase_times).
+#ifdef CB_PHASE_PROFILE
+#define CB_MARK(i)                                                                    \
+  do {                                                                                \
+    if (prm.dbg && blockIdx.x == 0 && threadIdx.x == 0 && (i) < 256) prm.dbg[(i)] = clock64(); \
+  } while (0)
+#else
+#define CB_MARK(i) \
+  do {             \
+  } while (0)
+#endif
+
 template <typename R>
 struct alignas(2 * sizeof(R)) Cx {
   R x, y;
@@ -188,23 +201,41 @@ __device__ __forceinline__ void dft_reg(Cx<R>* v) {
 // consecutive k read consecutive rows with 16-byte vector loads (fully
 // coalesced), instead of R-1 scattered 8-byte loads.
 
-// The two-polarisation field FFTs run radix-8 passes (one butterfly of x
-// and of y per thread); the half-length real-transform FFTs run radix-4
-// passes, which keeps all Q/8 threads busy on Q/2 points.
+// Radix schedules (sub-transform sizes NS = 1, R1, R1*R2, ...):
+//   kTail -- radix-8 passes, leftover radix last   (2048: 8 8 8 4); used by
+//            the field IFFTs and the outer transforms
+//   kHead -- radix-8 passes, leftover radix first  (2048: 4 8 8 8); used by
+//            the in-step field FFT, so its last pass (radix 8, NS = Q/8)
+//            produces exactly the 8 samples the next step's IFFT first pass
+//            (radix 8, NS = 1) consumes and the two fuse (fft2_boundary)
+//   kHalf -- radix-4 passes for the half-length real-transform FFTs, which
+//            keeps all Q/8 threads busy on Q/2 points
 constexpr int kMaxRad = 8;
-constexpr int kMaxRadHalf = 4;
+constexpr int kTail = 0, kHead = 1, kHalf = 2;
 
-__host__ __device__ constexpr int pass_radix(int L, int ns, int maxrad = kMaxRad) {
-  return L / ns >= maxrad ? maxrad : L / ns;
+__host__ __device__ constexpr int sched_radix(int L, int ns, int sched) {
+  if (sched == kHalf) return L / ns >= 4 ? 4 : L / ns;
+  if (sched == kHead && ns == 1) {
+    int head = L;
+    while (head > kMaxRad) head /= kMaxRad;
+    return head;
+  }
+  return L / ns >= kMaxRad ? kMaxRad : L / ns;
 }
-__host__ __device__ constexpr int twp_offset(int L, int NS, int maxrad = kMaxRad) {
+__host__ __device__ constexpr int twp_offset(int L, int NS, int sched) {
   int s = 0;
-  for (int ns = 1; ns < NS; ns *= pass_radix(L, ns, maxrad))
-    if (ns > 1) s += ns * pass_radix(L, ns, maxrad);
+  for (int ns = 1; ns < NS; ns *= sched_radix(L, ns, sched))
+    if (ns > 1) s += ns * sched_radix(L, ns, sched);
   return s;
 }
-__host__ __device__ constexpr int twp_size(int L, int maxrad = kMaxRad) {
-  return twp_offset(L, L, maxrad);
+__host__ __device__ constexpr int twp_size(int L, int sched) { return twp_offset(L, L, sched); }
+// per-pass twiddle rows in Params::twp: [kTail rows of Q][kHead rows of Q][kHalf rows of Q/2]
+__host__ __device__ constexpr int twp_base(int Q, int sched) {
+  return sched == kTail ? 0 : sched == kHead ? twp_size(Q, kTail)
+                                             : twp_size(Q, kTail) + twp_size(Q, kHead);
+}
+__host__ __device__ constexpr int twp_total(int Q) {
+  return twp_size(Q, kTail) + twp_size(Q, kHead) + twp_size(Q / 2, kHalf);
 }
 
 // Load the twiddle row of butterfly k (RAD entries, entry 0 unused).
@@ -385,10 +416,10 @@ __host__ __device__ constexpr int bfly(int t) {
 
 // Twiddle rows of the butterflies a thread runs in the pass with
 // sub-transform size NS of a length-L FFT (PER butterflies of radix RAD).
-template <typename R, int L, int NT, int NS, int MAXRAD>
+template <typename R, int L, int NT, int NS, int SCHED>
 struct PassRows {
   static constexpr bool kLast = NS >= L;
-  static constexpr int RAD = kLast ? 1 : pass_radix(L, NS, MAXRAD);
+  static constexpr int RAD = kLast ? 1 : sched_radix(L, NS, SCHED);
   static constexpr int PER = kLast ? 1 : ((L / RAD) >= NT ? (L / RAD) / NT : 1);
   static constexpr bool kHas = !kLast && NS > 1;
   Cx<R> w[PER][RAD];
@@ -397,7 +428,7 @@ struct PassRows {
   // shared-memory loads.
   __device__ __forceinline__ void fetch(const Cx<R>* twp) {
     if constexpr (kHas) {
-      const Cx<R>* tw = twp + twp_offset(L, NS, MAXRAD);
+      const Cx<R>* tw = twp + twp_offset(L, NS, SCHED);
       const int tid = threadIdx.x;
 #pragma unroll
       for (int p = 0; p < PER; ++p) {
@@ -409,12 +440,12 @@ struct PassRows {
   }
 };
 
-template <typename R, int Q, int NT, int NS, bool INV, bool FIRST, bool LAST, class Hook,
-          class Rows, class NextRows>
+template <typename R, int Q, int NT, int SCHED, int NS, bool INV, bool FIRST, bool LAST,
+          class Hook, class Rows, class NextRows>
 __device__ __forceinline__ void fft2_pass(Cx<R>* __restrict__ F, const Cx<R>* __restrict__ twp,
                                           const volatile int* zero, Hook& hook, Rows& rows,
-                                          NextRows& next) {
-  constexpr int RAD = pass_radix(Q, NS);
+                                          NextRows& next, const Cx<R>* __restrict__ twp_next) {
+  constexpr int RAD = sched_radix(Q, NS, SCHED);
   constexpr int LR = Q / RAD;
   constexpr int NB = Q / RAD;
   static_assert(NB % NT == 0, "butterflies must tile the block");
@@ -455,40 +486,119 @@ __device__ __forceinline__ void fft2_pass(Cx<R>* __restrict__ F, const Cx<R>* __
       bx[SF + pad(r * NS)] = vy[p][bitrev<RAD>(r)];
     }
   }
-  next.fetch(twp);
+  next.fetch(twp_next);
   __syncthreads();
 }
 
-template <typename R, int Q, int NT, int NS, bool INV, class Pre, class Post>
+// Runs the passes NS, NS*R, ... of a length-Q two-polarisation FFT with
+// schedule SCHED, stopping before the pass with sub-transform size STOP
+// (STOP = Q: to the end). rows: this pass's prefetched twiddle rows.
+template <typename R, int Q, int NT, int SCHED, int NS, int STOP, bool INV, class Pre,
+          class Post>
 struct Fft2Run {
-  using Rows = PassRows<R, Q, NT, NS, kMaxRad>;
+  using Rows = PassRows<R, Q, NT, NS, SCHED>;
   static __device__ __forceinline__ void run(Cx<R>* F, const Cx<R>* twp, const volatile int* z,
                                              Pre& pre, Post& post, Rows& rows) {
-    constexpr int RAD = pass_radix(Q, NS);
-    constexpr bool FIRST = NS == 1, LAST = NS * RAD == Q;
-    PassRows<R, Q, NT, NS * RAD, kMaxRad> next;
-    if constexpr (FIRST && LAST) {
-      static_assert(!(FIRST && LAST), "single-pass transforms are not used");
-    } else if constexpr (FIRST) {
-      fft2_pass<R, Q, NT, NS, INV, true, false>(F, twp, z, pre, rows, next);
+    constexpr int RAD = sched_radix(Q, NS, SCHED);
+    constexpr int NS2 = NS * RAD;
+    constexpr bool FIRST = NS == 1, LAST = NS2 == Q;
+    static_assert(!(FIRST && LAST), "single-pass transforms are not used");
+    PassRows<R, Q, NT, (NS2 < STOP ? NS2 : Q), SCHED> next;
+    if constexpr (FIRST) {
+      fft2_pass<R, Q, NT, SCHED, NS, INV, true, false>(F, twp, z, pre, rows, next, twp);
     } else if constexpr (LAST) {
-      fft2_pass<R, Q, NT, NS, INV, false, true>(F, twp, z, post, rows, next);
+      fft2_pass<R, Q, NT, SCHED, NS, INV, false, true>(F, twp, z, post, rows, next, twp);
     } else {
       NoHook none;
-      fft2_pass<R, Q, NT, NS, INV, false, false>(F, twp, z, none, rows, next);
+      fft2_pass<R, Q, NT, SCHED, NS, INV, false, false>(F, twp, z, none, rows, next, twp);
     }
-    if constexpr (!LAST) Fft2Run<R, Q, NT, NS * RAD, INV, Pre, Post>::run(F, twp, z, pre, post, next);
+    if constexpr (NS2 < STOP)
+      Fft2Run<R, Q, NT, SCHED, NS2, STOP, INV, Pre, Post>::run(F, twp, z, pre, post, next);
   }
 };
 
 // Unnormalised length-Q FFT of both polarisation rows of F (forward:
-// exp(-), inverse: exp(+)), natural order in and out, with fused hooks.
-// Ends with a barrier.
-template <typename R, int Q, int NT, bool INV, class Pre = NoHook, class Post = NoHook>
+// exp(-), inverse: exp(+)), natural order in and out, with fused hooks
+// (Pre on the first pass, Post on the last). NS0 > 1 starts mid-transform
+// (after fft2_boundary); STOP < Q stops before that pass. twp points at
+// this schedule's rows. Ends with a barrier.
+template <typename R, int Q, int NT, int SCHED, bool INV, class Pre = NoHook, class Post = NoHook,
+          int NS0 = 1, int STOP = Q>
 __device__ __forceinline__ void fft2(Cx<R>* F, const Cx<R>* twp, const volatile int* z,
                                      Pre pre = Pre(), Post post = Post()) {
-  PassRows<R, Q, NT, 1, kMaxRad> none;
-  Fft2Run<R, Q, NT, 1, INV, Pre, Post>::run(F, twp, z, pre, post, none);
+  PassRows<R, Q, NT, NS0, SCHED> rows;
+  rows.fetch(twp);
+  Fft2Run<R, Q, NT, SCHED, NS0, STOP, INV, Pre, Post>::run(F, twp, z, pre, post, rows);
+}
+
+// Step boundary: the last pass of the in-step forward FFT (kHead, radix 8,
+// NS = Q/8), the next dispersion phasor, and the first pass of the next
+// step's IFFT (kTail, radix 8, NS = 1) in one load/compute/store round: the
+// forward butterfly j produces samples j + r*Q/8, exactly the inputs of
+// inverse butterfly j (dbp.py:398, :395, :396).
+template <typename R, int Q, int NT>
+__device__ __forceinline__ void fft2_boundary(Cx<R>* __restrict__ F,
+                                              const Cx<R>* __restrict__ twHead,
+                                              const Cx<R>* __restrict__ twTail,
+                                              const Cx<R>* __restrict__ ph,
+                                              const volatile int* zero) {
+  constexpr int RAD = 8;
+  constexpr int NSF = Q / RAD;  // forward last pass
+  static_assert(sched_radix(Q, NSF, kHead) == RAD && NSF * RAD == Q, "kHead must end radix-8");
+  static_assert(sched_radix(Q, 1, kTail) == RAD, "kTail must start radix-8");
+  constexpr int LR = Q / RAD;
+  constexpr int PER = (Q / RAD) / NT;
+  static_assert((Q / RAD) % NT == 0, "butterflies must tile the block");
+  constexpr int SF = padded_len(Q);
+  PassRows<R, Q, NT, NSF, kHead> rows;
+  rows.fetch(twHead);
+  Cx<R> vx[PER][RAD], vy[PER][RAD];
+  const int tid = threadIdx.x + *zero;
+#pragma unroll
+  for (int p = 0; p < PER; ++p) {
+    const int j = tid + p * NT;
+    const Cx<R>* bx = F + pad(j);
+#pragma unroll
+    for (int r = 0; r < RAD; ++r) {
+      vx[p][r] = bx[pad(r * LR)];
+      vy[p][r] = bx[SF + pad(r * LR)];
+    }
+#pragma unroll
+    for (int r = 1; r < RAD; ++r) {
+      vx[p][r] = cmul(vx[p][r], rows.w[p][r]);
+      vy[p][r] = cmul(vy[p][r], rows.w[p][r]);
+    }
+    dft_reg<R, RAD, false>(vx[p]);
+    dft_reg<R, RAD, false>(vy[p]);
+    // natural output r sits at j + r*LR in v[bitrev(r)]: apply the phasor
+    // and hand it to the inverse butterfly as its input r
+    Cx<R> ux[RAD], uy[RAD];
+#pragma unroll
+    for (int r = 0; r < RAD; ++r) {
+      const Cx<R> w = ldg(ph + j + r * LR);
+      ux[r] = cmul(vx[p][bitrev<RAD>(r)], w);
+      uy[r] = cmul(vy[p][bitrev<RAD>(r)], w);
+    }
+    dft_reg<R, RAD, true>(ux);
+    dft_reg<R, RAD, true>(uy);
+#pragma unroll
+    for (int r = 0; r < RAD; ++r) {
+      vx[p][r] = ux[r];
+      vy[p][r] = uy[r];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int p = 0; p < PER; ++p) {
+    const int j = tid + p * NT;
+    Cx<R>* bx = F + pad(j * RAD);  // inverse first pass: NS = 1, d0 = 8j
+#pragma unroll
+    for (int r = 0; r < RAD; ++r) {
+      bx[pad(r)] = vx[p][bitrev<RAD>(r)];
+      bx[SF + pad(r)] = vy[p][bitrev<RAD>(r)];
+    }
+  }
+  __syncthreads();
 }
 
 // Single-array pass for the half-length real-transform FFTs. Passes with
@@ -499,7 +609,7 @@ __device__ __forceinline__ void fft2(Cx<R>* F, const Cx<R>* twp, const volatile 
 template <typename R, int Q, int L, int NT, int NS, bool INV, class Rows, class NextRows>
 __device__ __forceinline__ void fft1_pass(Cx<R>* __restrict__ buf, const Cx<R>* __restrict__ twp,
                                           const volatile int* zero, Rows& rows, NextRows& next) {
-  constexpr int RAD = pass_radix(L, NS, kMaxRadHalf);
+  constexpr int RAD = sched_radix(L, NS, kHalf);
   constexpr int LR = L / RAD;
   constexpr int NB = L / RAD;
   const int tid = threadIdx.x + *zero;
@@ -549,11 +659,11 @@ __device__ __forceinline__ void fft1_pass(Cx<R>* __restrict__ buf, const Cx<R>* 
 
 template <typename R, int Q, int L, int NT, int NS, bool INV>
 struct Fft1Run {
-  using Rows = PassRows<R, L, NT, NS, kMaxRadHalf>;
+  using Rows = PassRows<R, L, NT, NS, kHalf>;
   static __device__ __forceinline__ void run(Cx<R>* buf, const Cx<R>* twp, const volatile int* z,
                                              Rows& rows) {
-    constexpr int NS2 = NS * pass_radix(L, NS, kMaxRadHalf);
-    PassRows<R, L, NT, NS2, kMaxRadHalf> next;
+    constexpr int NS2 = NS * sched_radix(L, NS, kHalf);
+    PassRows<R, L, NT, NS2, kHalf> next;
     fft1_pass<R, Q, L, NT, NS, INV>(buf, twp, z, rows, next);
     Fft1Run<R, Q, L, NT, NS2, INV>::run(buf, twp, z, next);
   }
@@ -561,12 +671,12 @@ struct Fft1Run {
 template <typename R, int Q, int L, int NT, bool INV>
 struct Fft1Run<R, Q, L, NT, L, INV> {
   static __device__ __forceinline__ void run(Cx<R>*, const Cx<R>*, const volatile int*,
-                                             PassRows<R, L, NT, L, kMaxRadHalf>&) {}
+                                             PassRows<R, L, NT, L, kHalf>&) {}
 };
 
 template <typename R, int Q, int L, int NT, bool INV>
 __device__ __forceinline__ void fft1(Cx<R>* buf, const Cx<R>* twp, const volatile int* z) {
-  PassRows<R, L, NT, 1, kMaxRadHalf> none;
+  PassRows<R, L, NT, 1, kHalf> none;
   Fft1Run<R, Q, L, NT, 1, INV>::run(buf, twp, z, none);
 }
 
@@ -589,9 +699,10 @@ struct Params {
   const R* theta_scale;    // [n_steps], carries 1/Q
   const Cx<R>* twQ;        // [Q]   exp(-2 pi i m / Q)
   const Cx<R>* twN;        // [P*Q] exp(-2 pi i m / (P Q))
-  const Cx<R>* twp;        // per-pass rows: [twp_size(Q)] then [twp_size(Q/2, 4)]
+  const Cx<R>* twp;        // per-pass rows, layout twp_base()
   int n_steps;
   int64_t cid0;            // first cluster index of this launch chunk
+  long long* dbg;          // phase clocks of CTA 0 (CB_PHASE_PROFILE builds only)
 };
 
 // One radix-8 butterfly of each polarisation per thread on the length-Q
@@ -680,9 +791,11 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
 
   const Cx<R>* __restrict__ twQ = prm.twQ;
   const Cx<R>* __restrict__ twN = prm.twN;
-  const Cx<R>* __restrict__ twpQ = prm.twp;                  // length-Q passes
-  const Cx<R>* __restrict__ twpH = prm.twp + twp_size(Q);    // length-Q/2 passes
+  const Cx<R>* __restrict__ twpT = prm.twp + twp_base(Q, kTail);  // field IFFT / outer
+  const Cx<R>* __restrict__ twpF = prm.twp + twp_base(Q, kHead);  // in-step field FFT
+  const Cx<R>* __restrict__ twpH = prm.twp + twp_base(Q, kHalf);  // half-length FFTs
 
+  CB_MARK(0);
   // ---- 1. load the polyphase component u[rank + P*t2] of the circular
   //         window starting at (b*keep - half) mod n (dbp.py:473-475)
   {
@@ -701,6 +814,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
   __syncthreads();
 
   const size_t ph_tab = (size_t)P * Q;
+  CB_MARK(1);
 
   // ---- 2. outer transform, polyphase part: FFT_Q of both polarisations.
   //         For P == 1 the subband layout is the natural FFT order
@@ -708,9 +822,9 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
   if constexpr (P == 1) {
     PhasorHook<R> ph0;
     ph0.ph = prm.phasor + (size_t)prm.ph_index[0] * ph_tab;
-    fft2<R, Q, NT, false, NoHook, PhasorHook<R>>(F, twpQ, &s_zero, NoHook(), ph0);
+    fft2<R, Q, NT, kTail, false, NoHook, PhasorHook<R>>(F, twpT, &s_zero, NoHook(), ph0);
   } else {
-    fft2<R, Q, NT, false>(F, twpQ, &s_zero);
+    fft2<R, Q, NT, kTail, false>(F, twpT, &s_zero);
     // ---- 3. cross-subband radix-P stage over DSMEM: CTA c produces bins
     //         Q*k1 + k2 for k2 in its slice and every k1, and writes each to
     //         the CTA that owns it in the fftshift'd subband layout. Results
@@ -750,18 +864,24 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
     }
   }
 
+  CB_MARK(2);
   const Cx<R>* ph_rank = prm.phasor + (size_t)rank * Q;  // this CTA's subband rows
   R* Ireal = reinterpret_cast<R*>(IS);
   const R* Treal = reinterpret_cast<const R*>(TS);
 
-  // ---- 4. nonlinear steps (dbp.py:394-398)
+  // ---- 4. nonlinear steps (dbp.py:394-398). The subband IFFT
+  //         (normalisation folded into the phasor) also writes, in its last
+  //         pass, I = |x|^2 + |y|^2 packed as z[t] = I[2t] + i I[2t+1]. The
+  //         first step's IFFT runs here; later steps' IFFTs start inside
+  //         the previous step's fft2_boundary.
+  IntensityHook<R> ih;
+  ih.I = Ireal;
+  if (prm.n_steps > 0)
+    fft2<R, Q, NT, kTail, true, NoHook, IntensityHook<R>>(F, twpT, &s_zero, NoHook(), ih);
+  CB_MARK(3);
   for (int st = 0; st < prm.n_steps; ++st) {
-    // subband IFFT (normalisation folded into the phasor); its last pass
-    // also writes I = |x|^2 + |y|^2 packed as z[t] = I[2t] + i I[2t+1]
-    IntensityHook<R> ih;
-    ih.I = Ireal;
-    fft2<R, Q, NT, true, NoHook, IntensityHook<R>>(F, twpQ, &s_zero, NoHook(), ih);
     fft1<R, Q, H, NT, false>(IS, twpH, &s_zero);
+    CB_MARK(8 + 8 * st + 0);
 
     // r2c untangle: I_hat[k], k = 0..H (numpy rfft, dbp.py:194). For P > 1
     // each bin goes straight from registers to the CTA whose MIMO slice
@@ -801,6 +921,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
       }
     }
 
+    CB_MARK(8 + 8 * st + 1);
     // MIMO coupling (dbp.py:195): theta_hat_i[k] = sum_l T[i,l,k] I_hat_l[k]
     if constexpr (P > 1) {
       const int lo = mimo_lo(rank, P, H), hi = mimo_lo(rank + 1, P, H);
@@ -825,6 +946,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
                cluster_addr(bar_t, i));
         }
       }
+      CB_MARK(8 + 8 * st + 2);
       mbar_wait(&s_bar[1], st & 1);
     } else {
       __syncthreads();
@@ -832,6 +954,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
       __syncthreads();
     }
 
+    CB_MARK(8 + 8 * st + 3);
     // c2r pre-twist in place (numpy irfft ignores Im of bins 0 and H)
     for (int k = tid; k <= H / 2; k += NT) {
       if (k == 0) {
@@ -856,19 +979,32 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
       }
     }
     __syncthreads();
+    CB_MARK(8 + 8 * st + 4);
     fft1<R, Q, H, NT, true>(TS, twpH, &s_zero);
+    CB_MARK(8 + 8 * st + 5);
 
-    // rotation exp(-i theta) fused into the first pass and the next
-    // dispersion stage into the last pass of the subband FFT
-    // (dbp.py:208, :398, then :395 or :399)
+    // rotation exp(-i theta) fused into the first pass of the subband FFT
+    // (dbp.py:208, :398); its last pass either fuses with the next phasor
+    // and the next step's IFFT (dbp.py:395-396) or, after the last step,
+    // applies the final phasor (dbp.py:399)
     RotationHook<R> rot;
     rot.th = Treal;
     rot.scale = prm.theta_scale[st];
-    PhasorHook<R> ph1;
-    ph1.ph = ph_rank + (size_t)prm.ph_index[st + 1] * ph_tab;
-    fft2<R, Q, NT, false, RotationHook<R>, PhasorHook<R>>(F, twpQ, &s_zero, rot, ph1);
+    const Cx<R>* ph_next = ph_rank + (size_t)prm.ph_index[st + 1] * ph_tab;
+    if (st + 1 < prm.n_steps) {
+      fft2<R, Q, NT, kHead, false, RotationHook<R>, NoHook, 1, Q / 8>(F, twpF, &s_zero, rot);
+      CB_MARK(8 + 8 * st + 6);
+      fft2_boundary<R, Q, NT>(F, twpF, twpT, ph_next, &s_zero);
+      CB_MARK(8 + 8 * st + 7);
+      fft2<R, Q, NT, kTail, true, NoHook, IntensityHook<R>, 8>(F, twpT, &s_zero, NoHook(), ih);
+    } else {
+      PhasorHook<R> ph1;
+      ph1.ph = ph_next;
+      fft2<R, Q, NT, kHead, false, RotationHook<R>, PhasorHook<R>>(F, twpF, &s_zero, rot, ph1);
+    }
   }
 
+  CB_MARK(4);
   // ---- 5. merge + outer IFFT (dbp.py:400-401): CTA c gathers, for k2 in
   //         its slice, the P bins Q*k1 + k2 from their owners, applies the
   //         inverse radix-P stage and the twiddle, and hands polyphase
@@ -903,8 +1039,9 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
       cluster.sync();
     }
   }
-  fft2<R, Q, NT, true>(F, twpQ, &s_zero);
+  fft2<R, Q, NT, kTail, true>(F, twpT, &s_zero);
 
+  CB_MARK(5);
   // ---- 6. keep proc[half : half + span] (dbp.py:476-477)
   {
     const int64_t span = min(prm.keep, n - b * prm.keep);

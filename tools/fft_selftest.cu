@@ -21,9 +21,11 @@ __global__ void __launch_bounds__(threads_for<R, Q>()) kfft(const Cx<R>* twp, Cx
     for (int i = threadIdx.x; i < L; i += NT) buf[a * padded_len(L) + pad(i)] = data[a * L + i];
   __syncthreads();
   if constexpr (HALF)
-    fft1<R, Q, L, NT, INV>(buf, twp + twp_size(Q), &z);
+    fft1<R, Q, L, NT, INV>(buf, twp + twp_base(Q, kHalf), &z);
+  else if constexpr (INV)
+    fft2<R, Q, NT, kTail, INV>(buf, twp + twp_base(Q, kTail), &z);
   else
-    fft2<R, Q, NT, INV>(buf, twp, &z);
+    fft2<R, Q, NT, kHead, INV>(buf, twp + twp_base(Q, kHead), &z);
   for (int a = 0; a < NA; ++a)
     for (int i = threadIdx.x; i < L; i += NT) data[a * L + i] = buf[a * padded_len(L) + pad(i)];
 }
@@ -31,21 +33,23 @@ __global__ void __launch_bounds__(threads_for<R, Q>()) kfft(const Cx<R>* twp, Cx
 template <typename R>
 std::vector<Cx<R>> tables(int Q) {
   const long double pi = 3.141592653589793238462643383279502884L;
-  std::vector<Cx<R>> out(twp_size(Q) + twp_size(Q / 2, kMaxRadHalf));
-  auto fill = [&](int L, int base, int mr) {
-    for (int ns = 1; ns < L; ns *= pass_radix(L, ns, mr)) {
-      const int Rr = pass_radix(L, ns, mr);
+  std::vector<Cx<R>> out(twp_total(Q));
+  auto fill = [&](int L, int sched) {
+    for (int ns = 1; ns < L; ns *= sched_radix(L, ns, sched)) {
+      const int Rr = sched_radix(L, ns, sched);
       if (ns == 1) continue;
       for (int k = 0; k < ns; ++k)
         for (int r = 0; r < Rr; ++r) {
           const long long e = (long long)r * k * (Q / (ns * Rr)) % Q;
-          out[base + twp_offset(L, ns, mr) + k * Rr + r].x = (R)cosl(-2 * pi * e / Q);
-          out[base + twp_offset(L, ns, mr) + k * Rr + r].y = (R)sinl(-2 * pi * e / Q);
+          Cx<R>& o = out[twp_base(Q, sched) + twp_offset(L, ns, sched) + k * Rr + r];
+          o.x = (R)cosl(-2 * pi * e / Q);
+          o.y = (R)sinl(-2 * pi * e / Q);
         }
     }
   };
-  fill(Q, 0, kMaxRad);
-  fill(Q / 2, twp_size(Q), kMaxRadHalf);
+  fill(Q, kTail);
+  fill(Q, kHead);
+  fill(Q / 2, kHalf);
   return out;
 }
 
