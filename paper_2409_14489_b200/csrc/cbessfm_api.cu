@@ -49,10 +49,10 @@ std::vector<double> twiddles(int64_t n) {
   return t;
 }
 
-// Per-pass twiddle rows of the length-Q and length-Q/2 Stockham FFTs, in
-// the layout cbessfm_kernel.cuh reads (twp_offset / pass_radix): row k of
-// the pass with sub-transform size ns holds W_Q^(r*k*Q/(ns*R)), r < R.
-std::vector<double> pass_tables(int Q, const std::vector<double>& tq) {
+// Per-pass twiddles of the length-Q and length-Q/2 Stockham FFTs in the
+// layout cbessfm_kernel.cuh reads (twp_base / twp_offset / tw_plane_index):
+// entry (k, r) of the pass with sub-transform size ns is W_Q^(r*k*Q/(ns*R)).
+std::vector<double> pass_tables(int Q, const std::vector<double>& tq, int real_bytes) {
   using namespace cbessfm;
   std::vector<double> out(2 * (size_t)twp_total(Q), 0.0);
   auto fill = [&](int L, int sched) {
@@ -62,10 +62,11 @@ std::vector<double> pass_tables(int Q, const std::vector<double>& tq) {
       if (ns == 1) continue;
       const size_t off = base + twp_offset(L, ns, sched);
       for (int k = 0; k < ns; ++k)
-        for (int r = 0; r < R; ++r) {
+        for (int r = 1; r < R; ++r) {
           const int64_t e = ((int64_t)r * k * (Q / (ns * R))) % Q;
-          out[2 * (off + (size_t)k * R + r)] = tq[2 * e];
-          out[2 * (off + (size_t)k * R + r) + 1] = tq[2 * e + 1];
+          const size_t at = off + (size_t)tw_plane_index(real_bytes, ns, k, r);
+          out[2 * at] = tq[2 * e];
+          out[2 * at + 1] = tq[2 * e + 1];
         }
     }
   };
@@ -191,7 +192,7 @@ cbessfm_status upload_all(cbessfm_plan* p, const cbessfm_desc* d) {
     return cuda_fail(e, "upload twiddles");
   if ((e = upload_complex<R>(tn.data(), PQ, &p->twN, true)) != cudaSuccess)
     return cuda_fail(e, "upload outer twiddles");
-  const std::vector<double> tp = pass_tables(p->Q, tq);
+  const std::vector<double> tp = pass_tables(p->Q, tq, (int)sizeof(R));
   if ((e = upload_complex<R>(tp.data(), tp.size() / 2, &p->twp, true)) != cudaSuccess)
     return cuda_fail(e, "upload pass twiddles");
 #ifdef CB_PHASE_PROFILE

@@ -238,26 +238,36 @@ __host__ __device__ constexpr int twp_total(int Q) {
   return twp_size(Q, kTail) + twp_size(Q, kHead) + twp_size(Q / 2, kHalf);
 }
 
-// Load the twiddle row of butterfly k (RAD entries, entry 0 unused).
-template <int RAD>
-__device__ __forceinline__ void load_row(const Cx<float>* row, Cx<float>* w) {
+// Twiddle storage of one pass (NS rows k, radix RAD, entries r = 1..RAD-1)
+// is plane-major so that every load instruction of a warp reads one
+// contiguous span (lanes = consecutive k): float rows are split into RAD/2
+// planes of 16-byte pairs (r = 2q+1, 2q+2; the last pair's second half is
+// padding), double rows into RAD-1 planes of one complex each. Plane q of
+// a pass starts at complex offset q * 2 * NS (float) or q * NS (double).
+__host__ __device__ constexpr int tw_plane_index(int real_bytes, int NS, int k, int r) {
+  return real_bytes == 4 ? ((r - 1) / 2) * 2 * NS + 2 * k + ((r - 1) & 1) : (r - 1) * NS + k;
+}
+
+template <int RAD, int NS>
+__device__ __forceinline__ void load_row(const Cx<float>* tw, int k, Cx<float>* w) {
 #pragma unroll
   for (int q = 0; q < RAD / 2; ++q) {
     float a, b, c, d;
     asm volatile("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];"
                  : "=f"(a), "=f"(b), "=f"(c), "=f"(d)
-                 : "l"(row + 2 * q));
-    w[2 * q] = mk(a, b);
-    w[2 * q + 1] = mk(c, d);
+                 : "l"(tw + q * 2 * NS + 2 * k));
+    w[2 * q + 1] = mk(a, b);
+    if (2 * q + 2 < RAD) w[2 * q + 2] = mk(c, d);
   }
 }
-template <int RAD>
-__device__ __forceinline__ void load_row(const Cx<double>* row, Cx<double>* w) {
+template <int RAD, int NS>
+__device__ __forceinline__ void load_row(const Cx<double>* tw, int k, Cx<double>* w) {
 #pragma unroll
-  for (int q = 0; q < RAD; ++q) {
+  for (int r = 1; r < RAD; ++r) {
     double a, b;
-    asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "l"(row + q));
-    w[q] = mk(a, b);
+    asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b)
+                 : "l"(tw + (r - 1) * NS + k));
+    w[r] = mk(a, b);
   }
 }
 
@@ -434,7 +444,7 @@ struct PassRows {
       for (int p = 0; p < PER; ++p) {
         const int t = tid + p * NT;
         const int j = bfly<L, NS, RAD>(t);
-        if ((L / RAD) >= NT || t < L / RAD) load_row<RAD>(tw + (j % NS) * RAD, w[p]);
+        if ((L / RAD) >= NT || t < L / RAD) load_row<RAD, NS>(tw, j % NS, w[p]);
       }
     }
   }

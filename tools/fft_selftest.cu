@@ -41,7 +41,9 @@ std::vector<Cx<R>> tables(int Q) {
       for (int k = 0; k < ns; ++k)
         for (int r = 0; r < Rr; ++r) {
           const long long e = (long long)r * k * (Q / (ns * Rr)) % Q;
-          Cx<R>& o = out[twp_base(Q, sched) + twp_offset(L, ns, sched) + k * Rr + r];
+          if (r == 0) continue;
+          Cx<R>& o = out[twp_base(Q, sched) + twp_offset(L, ns, sched) +
+                         tw_plane_index((int)sizeof(R), ns, k, r)];
           o.x = (R)cosl(-2 * pi * e / Q);
           o.y = (R)sinl(-2 * pi * e / Q);
         }
