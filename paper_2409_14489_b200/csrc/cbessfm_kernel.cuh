@@ -889,7 +889,16 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
   if (prm.n_steps > 0)
     fft2<R, Q, NT, kTail, true, NoHook, IntensityHook<R>>(F, twpT, &s_zero, NoHook(), ih);
   CB_MARK(3);
+  constexpr int KU = (H / 2 + 1 + NT - 1) / NT;  // untangle/twist bins per thread
   for (int st = 0; st < prm.n_steps; ++st) {
+    // W_Q^k of this thread's untangle/twist bins, issued before the FFT so
+    // the L2 latency hides behind it (the same k serve both)
+    Cx<R> twk[KU];
+#pragma unroll
+    for (int u = 0; u < KU; ++u) {
+      const int k = tid + u * NT;
+      twk[u] = (k <= H / 2) ? ldg(twQ + k) : mk((R)1, (R)0);
+    }
     fft1<R, Q, H, NT, false>(IS, twpH, &s_zero);
     CB_MARK(8 + 8 * st + 0);
 
@@ -914,7 +923,10 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
         IS[pad(k)] = v;
       }
     };
-    for (int k = tid; k <= H / 2; k += NT) {
+#pragma unroll
+    for (int u = 0; u < KU; ++u) {
+      const int k = tid + u * NT;
+      if (k > H / 2) break;
       if (k == 0) {
         const Cx<R> z = IS[pad(0)];
         emit(0, mk(z.x + z.y, (R)0));
@@ -925,7 +937,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
         const Cx<R> e = scale(a + bq, (R)0.5);
         const Cx<R> dd = a - bq;                           // 2i * O[k]
         const Cx<R> o = mk(dd.y * (R)0.5, -dd.x * (R)0.5); // O[k]
-        const Cx<R> wo = cmul(o, ldg(twQ + k));
+        const Cx<R> wo = cmul(o, twk[u]);
         emit(k, e + wo);
         if (k != H - k) emit(H - k, conj(e - wo));
       }
@@ -966,14 +978,17 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
 
     CB_MARK(8 + 8 * st + 3);
     // c2r pre-twist in place (numpy irfft ignores Im of bins 0 and H)
-    for (int k = tid; k <= H / 2; k += NT) {
+#pragma unroll
+    for (int u = 0; u < KU; ++u) {
+      const int k = tid + u * NT;
+      if (k > H / 2) break;
       if (k == 0) {
         const R x0 = TS[pad(0)].x, xh = TS[pad(H)].x;
         TS[pad(0)] = mk(x0 + xh, x0 - xh);
       } else {
         const Cx<R> a = TS[pad(k)];                 // X[k]
         const Cx<R> c = conj(TS[pad(H - k)]);       // X[k + H]
-        const Cx<R> wk = ldg(twQ + k);              // W^k
+        const Cx<R> wk = twk[u];                    // W^k
         const Cx<R> s = a + c;
         const Cx<R> dd = cmulc(a - c, wk);          // W^-k (a - c)
         TS[pad(k)] = mk(s.x - dd.y, s.y + dd.x);    // s + i dd
