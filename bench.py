@@ -35,29 +35,56 @@ sys.path.insert(0, str(ROOT))
 METRIC = "CB-ESSFM DBP throughput (2D symbols/s) at 1/2/4/8 B200; % of roofline"
 UNIT = "2D symbols/s"
 RATE = 512e9
-N_SAMPLES = 1 << 20
-SYMBOLS_PER_WAVE = 5 * 2 * (1 << 17)      # channels x polarisations x symbols
 SPS_EFF = RATE / (5 * 64e9)               # samples per 2D symbol per pol = 1.6
 
 
-def workload_cfg():
+WORKLOADS = {
+    # name: (configs index, spans, n, N_st, rho, N, N_ov, coefficient file, prefix, batch/GPU)
+    "cfg2": dict(index=1, spans=15, n=1 << 20, n_steps=15, rho=0.12, block=10240,
+                 overlap=2860, coeffs=("cfg2_nsb5.npz", ""), batch=1,
+                 text="BASELINE configs[1]: 5x64 GBd WDM @ 512 GS/s, 2^17 sym/ch, CB-ESSFM "
+                      "N_sb=5, N_st=15, rho=0.12, N'=2048 (N=10240, N_ov=2860), 31-tap MIMO"),
+    "cfg4": dict(index=3, spans=50, n=1 << 21, n_steps=50, rho=0.12, block=20480,
+                 overlap=2860, coeffs=("cfg4_nsb5_st50.npz", ""), batch=1,
+                 text="BASELINE configs[3]: 5x64 GBd over 50x80 km, 2^18 sym/ch, CB-ESSFM "
+                      "N_sb=5, N_st=50, rho=0.12, N'=4096 (N=20480, N_ov=2860)"),
+    "cfg4s10": dict(index=3, spans=50, n=1 << 21, n_steps=10, rho=0.5, block=20480,
+                    overlap=14290, coeffs=("cfg4_coeffs.npz", "s10_"), batch=1,
+                    text="BASELINE configs[3], N_st=10 (N_ov=14290)"),
+    "cfg4s1": dict(index=3, spans=50, n=1 << 21, n_steps=1, rho=0.5, block=20480,
+                   overlap=10240, coeffs=("cfg4_coeffs.npz", "s1_"), batch=1,
+                   text="BASELINE configs[3], N_st=1 (N_ov=10240)"),
+    "cfg5": dict(index=4, spans=15, n=1 << 23, n_steps=15, rho=0.12, block=10240,
+                 overlap=2860, coeffs=("cfg2_nsb5.npz", ""), batch=64,
+                 text="BASELINE configs[4]: 64 independent 5-subband Gaussian waveforms, "
+                      "2^20 sym/ch (n=2^23), configs[1] geometry, sharded over GPUs"),
+}
+WL = WORKLOADS["cfg2"]
+
+
+def workload_cfg(wl=None):
     from paper_2409_14489_b200 import DbpConfig, LinkConfig
     from paper_2409_14489_b200.config import load_coefficients_npz
-    link = LinkConfig(num_spans=15, span_length_km=80.0, alpha_db_per_km=0.2,
+    wl = WL if wl is None else wl
+    link = LinkConfig(num_spans=wl["spans"], span_length_km=80.0, alpha_db_per_km=0.2,
                       dispersion_d_ps_nm_km=17.0, gamma_w_km=1.3)
-    cfg = DbpConfig(link=link, variant="CB_ESSFM", n_steps=15, n_subbands=5,
-                    splitting_ratio=0.12, block_size=10240, overlap=2860,
+    cfg = DbpConfig(link=link, variant="CB_ESSFM", n_steps=wl["n_steps"], n_subbands=5,
+                    splitting_ratio=wl["rho"], block_size=wl["block"], overlap=wl["overlap"],
                     oversampling=SPS_EFF)
-    coeffs = load_coefficients_npz(ROOT / "tests" / "golden" / "cfg2_nsb5.npz")
+    fname, prefix = wl["coeffs"]
+    coeffs = load_coefficients_npz(ROOT / "tests" / "golden" / fname, prefix)
     return cfg, coeffs
 
 
+def symbols_per_wave(wl=None):
+    wl = WL if wl is None else wl
+    return int(wl["n"] / SPS_EFF) * 2          # 2D symbols: n / 1.6 per pol x 2 pols
+
+
 def config_block(args, world):
-    return {"workload": "BASELINE configs[1]: 5x64 GBd WDM @ 512 GS/s, 2^17 sym/ch, "
-                        "CB-ESSFM N_sb=5, N_st=15, rho=0.12, N'=2048 (N=10240, N_ov=2860), "
-                        "31-tap MIMO",
-            "n_samples_per_pol": N_SAMPLES, "waveforms_per_gpu": args.batch,
-            "two_d_symbols_per_waveform": SYMBOLS_PER_WAVE,
+    return {"workload": WL["text"], "baseline_config_index": WL["index"],
+            "n_samples_per_pol": WL["n"], "waveforms_per_gpu": args.batch,
+            "two_d_symbols_per_waveform": symbols_per_wave(),
             "parallelism": f"waveform-parallel x{world} (no collective in the step loop)",
             "l2": "flushed (256 MiB write) between timed steps"}
 
@@ -67,12 +94,14 @@ def config_block(args, world):
 def _oracle_worker(args):
     """One process: the numpy oracle over blocks [b0, b1) of a waveform."""
     os.environ["OMP_NUM_THREADS"] = "1"
-    b0, b1, seed = args
+    b0, b1, seed, wname = args
+    global WL
+    WL = WORKLOADS[wname]
     import numpy as np
     from oracle import cbessfm_oracle as orc        # checker / CPU baseline only
     from paper_2409_14489_b200.synth import gaussian_wdm
     cfg, coeffs = workload_cfg()
-    field = gaussian_wdm(N_SAMPLES, RATE, seed=seed)
+    field = gaussian_wdm(WL["n"], RATE, seed=seed)
     t0 = time.perf_counter()
     orc.run_cb_blocks(field, cfg, RATE, coeffs, b0, b1)
     return time.perf_counter() - t0
@@ -91,14 +120,15 @@ def cpu_baseline(max_procs: int | None = None) -> dict:
     import multiprocessing as mp
     from paper_2409_14489_b200.planner import BlockSchedule
     cores = _cores() if max_procs is None else min(max_procs, _cores())
-    nb = BlockSchedule(N_SAMPLES, 10240, 2860).n_blocks
+    nb = BlockSchedule(WL["n"], WL["block"], WL["overlap"]).n_blocks
     ctx = mp.get_context("spawn")
     with ctx.Pool(cores) as pool:
-        pool.map(_oracle_worker, [(0, 1, 0)] * cores)           # warm imports
+        name = next(k for k, v in WORKLOADS.items() if v is WL)
+        pool.map(_oracle_worker, [(0, 1, 0, name)] * cores)     # warm imports
         t0 = time.perf_counter()
-        pool.map(_oracle_worker, [(0, nb, i) for i in range(cores)])
+        pool.map(_oracle_worker, [(0, nb, i, name) for i in range(cores)])
         wall = time.perf_counter() - t0
-    return {"value": cores * SYMBOLS_PER_WAVE / wall, "unit": UNIT,
+    return {"value": cores * symbols_per_wave() / wall, "unit": UNIT,
             "cores": cores, "kind": "port",
             "sample": f"{cores} concurrent processes x one configs[1] waveform "
                       f"({nb} blocks, complex128 numpy oracle), wall {wall:.2f} s"}
@@ -112,9 +142,10 @@ def run_reference(args, rank, world):
     import multiprocessing as mp
     from paper_2409_14489_b200.planner import BlockSchedule
     cores = _cores()
-    nb = BlockSchedule(N_SAMPLES, 10240, 2860).n_blocks
+    nb = BlockSchedule(WL["n"], WL["block"], WL["overlap"]).n_blocks
     parts = min(cores, nb)
-    ranges = [(nb * i // parts, nb * (i + 1) // parts, 0) for i in range(parts)]
+    name = next(k for k, v in WORKLOADS.items() if v is WL)
+    ranges = [(nb * i // parts, nb * (i + 1) // parts, 0, name) for i in range(parts)]
     ctx = mp.get_context("spawn")
     times = []
     with ctx.Pool(parts) as pool:
@@ -125,7 +156,7 @@ def run_reference(args, rank, world):
             if i >= args.warmup:
                 times.append(dt)
     per = sum(times) / len(times)
-    value = SYMBOLS_PER_WAVE / per
+    value = symbols_per_wave() / per
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -198,9 +229,10 @@ class ClockSampler:
 
 def roofline_numbers(dtype: str):
     from paper_2409_14489_b200 import cb_essfm_cost
-    rm = cb_essfm_cost(10240, 2860, SPS_EFF, 15, 5).rm_per_2d
+    n, ov = WL["block"], WL["overlap"]
+    rm = cb_essfm_cost(n, ov, SPS_EFF, WL["n_steps"], 5).rm_per_2d
     sample_bytes = 8 if dtype == "c64" else 16
-    byt = SPS_EFF * sample_bytes * (10240 / (10240 - 2860) + 1)
+    byt = SPS_EFF * sample_bytes * (n / (n - ov) + 1)
     return rm, byt
 
 
@@ -235,19 +267,27 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--dtype", default="c64", choices=("c64", "c128"))
-    ap.add_argument("--batch", type=int, default=1,
-                    help="configs[1] waveforms per GPU per step")
+    ap.add_argument("--batch", type=int, default=None,
+                    help="waveforms per GPU per step (default: the workload's)")
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS),
+                    help="BASELINE config the step runs (default configs[1])")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true",
                     help="minimal run for ncu (no sampler, no CPU legs)")
     args = ap.parse_args()
+    global WL
+    WL = WORKLOADS[args.workload]
     if args.warmup < 3 and not args.profile:
         args.warmup = 3
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.batch is None:
+        # configs[4] is a fixed batch sharded over the GPUs (strong scaling);
+        # the others run one waveform per GPU (weak scaling)
+        args.batch = max(1, WL["batch"] // world) if WL["batch"] > 1 else 1
 
     if args.impl == "reference":
         return run_reference(args, rank, world)
@@ -272,9 +312,11 @@ def main():
     cfg, coeffs = workload_cfg()
     eng = pb.DbpEngine(cfg, coeffs, RATE, dtype=args.dtype, device=local)
     ct = torch.complex64 if args.dtype == "c64" else torch.complex128
-    host = np.stack([gaussian_wdm(N_SAMPLES, RATE, seed=1000 * rank + b)
-                     for b in range(args.batch)])
-    x = torch.from_numpy(host).to(dev).to(ct)
+    # waveforms are synthesised one at a time straight into HBM (configs[4]
+    # is 64 x 2^23 samples; the host never holds the whole batch)
+    x = torch.empty((args.batch, 2, WL["n"]), dtype=ct, device=dev)
+    for b in range(args.batch):
+        x[b] = torch.from_numpy(gaussian_wdm(WL["n"], RATE, seed=1000 * rank + b)).to(dev)
     out = torch.empty_like(x)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -308,13 +350,14 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
     per_step_ms = t_ms / args.steps
-    sym_per_step = world * args.batch * SYMBOLS_PER_WAVE
+    sym_per_step = world * args.batch * symbols_per_wave()
     value = sym_per_step / (per_step_ms * 1e-3)
 
     # end to end through the public API with pinned host buffers
     e2e = None
-    if not (args.no_e2e or args.profile):
-        hx = torch.from_numpy(host).to(ct).pin_memory()
+    big = x.numel() * x.element_size() > (4 << 30)   # configs[4]: 2 x 8.6 GB pinned
+    if not (args.no_e2e or args.profile or big):
+        hx = x.cpu().pin_memory()
         hout = torch.empty_like(hx).pin_memory()
         for _ in range(3):
             eng.run_host(hx, hout)
@@ -366,7 +409,7 @@ def main():
     peaks, peak_src = measured_peaks()
     rm_2d, b_2d = roofline_numbers(args.dtype)
     launch_s = per_step_ms * 1e-3                 # one kernel launch per step
-    sym_launch = args.batch * SYMBOLS_PER_WAVE
+    sym_launch = args.batch * symbols_per_wave()
     fma_kinds = (0, 1) if args.dtype == "c64" else (2,)
     fma_peak = max(_native.fma_peak(k) for k in fma_kinds)
     achieved_rm = rm_2d * sym_launch / launch_s
@@ -393,14 +436,15 @@ def main():
     clocks = sampler.summary() if sampler else None
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step_ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True,
+            "scaling": "strong" if WL["batch"] > 1 else "weak", "vs_baseline": None,
             "dtype": "c64 (f32)" if args.dtype == "c64" else "c128 (f64)",
             "data": "synthetic (seeded band-limited Gaussian WDM, configs[1] grid)",
             "config": config_block(args, world), "impl": "ours",
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": args.steps, "clocks": clocks, "gather": gather,
-            "kernel": {"name": "cbessfm_block_kernel<float,5,2048>" if args.dtype == "c64"
-                       else "cbessfm_block_kernel<double,5,2048>",
+            "kernel": {"name": "cbessfm_block_kernel<%s,5,%d>" % (
+                           "float" if args.dtype == "c64" else "double", WL["block"] // 5),
                        "plan": {k: getattr(eng.plan.info(), k) for k in
                                 ("threads_per_cta", "cluster_size", "smem_per_cta",
                                  "max_active_clusters", "q")}}}

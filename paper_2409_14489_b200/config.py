@@ -232,15 +232,16 @@ class DualPolWaveform:
                                self.sample_rate, self.center_freq)
 
 
-def load_coefficients_npz(path) -> CoefficientSet:
+def load_coefficients_npz(path, prefix: str = "") -> CoefficientSet:
     """Read a CoefficientSet saved by tests/golden/make_golden.py (keys
-    c_n_sb, c_subband_rate, ..., c_tap_<h>)."""
+    <prefix>c_n_sb, <prefix>c_subband_rate, ..., <prefix>c_tap_<h>)."""
     d = np.load(path, allow_pickle=False)
-    hs = [int(h) for h in d["c_hs"]]
+    p = prefix
+    hs = [int(h) for h in d[p + "c_hs"]]
     return CoefficientSet(
-        n_sb=int(d["c_n_sb"]), subband_rate=float(d["c_subband_rate"]),
-        subband_spacing=float(d["c_subband_spacing"]),
-        reference_power_w=float(d["c_reference_power_w"]),
-        phase_norm_rad=float(d["c_phase_norm_rad"]),
-        step_scales=d["c_step_scales"], geometry_hash=str(d["c_geometry_hash"]),
-        coeffs={h: d[f"c_tap_{h}"] for h in hs})
+        n_sb=int(d[p + "c_n_sb"]), subband_rate=float(d[p + "c_subband_rate"]),
+        subband_spacing=float(d[p + "c_subband_spacing"]),
+        reference_power_w=float(d[p + "c_reference_power_w"]),
+        phase_norm_rad=float(d[p + "c_phase_norm_rad"]),
+        step_scales=d[p + "c_step_scales"], geometry_hash=str(d[p + "c_geometry_hash"]),
+        coeffs={h: d[f"{p}c_tap_{h}"] for h in hs})

@@ -66,18 +66,19 @@ class Golden:
         return self.data[key]
 
 
-def load_coeffs(d):
-    if "c_n_sb" not in d.files:
+def load_coeffs(d, prefix: str = ""):
+    if prefix + "c_n_sb" not in d.files:
         return None
-    hs = [int(h) for h in d["c_hs"]]
+    p = prefix
+    hs = [int(h) for h in d[p + "c_hs"]]
     return CoefficientSet(
-        n_sb=int(d["c_n_sb"]), subband_rate=float(d["c_subband_rate"]),
-        subband_spacing=float(d["c_subband_spacing"]),
-        reference_power_w=float(d["c_reference_power_w"]),
-        phase_norm_rad=float(d["c_phase_norm_rad"]),
-        step_scales=d["c_step_scales"],
-        geometry_hash=str(d["c_geometry_hash"]),
-        coeffs={h: d[f"c_tap_{h}"] for h in hs})
+        n_sb=int(d[p + "c_n_sb"]), subband_rate=float(d[p + "c_subband_rate"]),
+        subband_spacing=float(d[p + "c_subband_spacing"]),
+        reference_power_w=float(d[p + "c_reference_power_w"]),
+        phase_norm_rad=float(d[p + "c_phase_norm_rad"]),
+        step_scales=d[p + "c_step_scales"],
+        geometry_hash=str(d[p + "c_geometry_hash"]),
+        coeffs={h: d[f"{p}c_tap_{h}"] for h in hs})
 
 
 _cache = {}

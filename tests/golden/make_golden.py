@@ -232,6 +232,42 @@ def main():
         np.savez_compressed(HERE / "nlpr_kat.npz", **arr)
         print("  wrote nlpr_kat.npz")
 
+    # --- coefficient sets for the BASELINE.json configs[2] sweep grid
+    #     (N_st x N_sb x rho on the configs[0] link and rate). The sweep's
+    #     parity tests run the GPU and the oracle on the same set; taps are
+    #     capped at memory=7 so the reference builder stays fast.
+    if want("sweep_coeffs"):
+        arrays = {}
+        for n_st in (1, 2, 3, 5, 8, 15):
+            for n_sb in (1, 3, 5, 9):
+                for rho in (0.5, 0.7, 1.0):
+                    cfg = fd.DbpConfig(link=link(15), variant="CB_ESSFM",
+                                       n_steps=n_st, n_subbands=n_sb,
+                                       splitting_ratio=rho,
+                                       block_size=512 * n_sb, overlap=0,
+                                       oversampling=2.0)
+                    c = coeffs_for(cfg, rate1, p1, 7)
+                    tag = f"s{n_st}_b{n_sb}_r{int(rho * 10)}_"
+                    for k, v in coeff_arrays(c).items():
+                        arrays[tag + k] = v
+        np.savez_compressed(HERE / "sweep_coeffs.npz", **arrays)
+        print("  wrote sweep_coeffs.npz")
+
+    # --- configs[3] coefficient sets for N_st = 1 and 10 (rho = 0.5)
+    if want("cfg4_coeffs"):
+        arrays = {}
+        rate4 = 512e9
+        p4 = fd.WdmConfig(64e9, 5, 100e9, 0.05, "16-qam", 1.0).launch_power_w
+        for n_st, ov in ((1, 10240), (10, 14290)):
+            cfg = fd.DbpConfig(link=link(50), variant="CB_ESSFM", n_steps=n_st,
+                               n_subbands=5, splitting_ratio=0.5,
+                               block_size=20480, overlap=ov, oversampling=1.6)
+            c = coeffs_for(cfg, rate4, p4, 15)
+            for k, v in coeff_arrays(c).items():
+                arrays[f"s{n_st}_" + k] = v
+        np.savez_compressed(HERE / "cfg4_coeffs.npz", **arrays)
+        print("  wrote cfg4_coeffs.npz")
+
     print(f"done in {time.time() - t0:.1f} s")
 
 

@@ -1,0 +1,128 @@
+"""BASELINE.json configs[0], [2], [3] and [4] on the GPU against the oracle.
+
+Inputs are seeded synthetic waveforms at each config's size and spectral
+layout (the forward-propagated versions live in tests/golden for the
+smaller sizes); coefficient sets were built by the reference
+(tests/golden/make_golden.py). Bars: rel L2 <= 1e-12 (c128), <= 1e-5 (c64).
+"""
+
+import math
+import warnings
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden, load_coeffs, rel_rms
+from oracle import cbessfm_oracle as orc
+
+import paper_2409_14489_b200 as pb
+from paper_2409_14489_b200.synth import gaussian_wdm
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"c128": 1e-12, "c64": 1e-5}
+
+
+def _gpu(field, cfg, coeffs, rate, dtype, block_range=None):
+    import torch
+    ct = torch.complex64 if dtype == "c64" else torch.complex128
+    x = torch.from_numpy(np.ascontiguousarray(field)).cuda().to(ct)
+    if x.dim() == 2:
+        x = x[None]
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        out = pb.run_dbp_tensor(x, cfg, coeffs, rate, block_range=block_range)
+    return out.to(torch.complex128).cpu().numpy()
+
+
+def _link(spans):
+    return pb.LinkConfig(num_spans=spans, span_length_km=80.0, alpha_db_per_km=0.2,
+                         dispersion_d_ps_nm_km=17.0, gamma_w_km=1.3)
+
+
+@pytest.mark.parametrize("block,overlap", [(4096, 2680), (1024, 512)])
+def test_config0_full_size(cuda, block, overlap):
+    # configs[0]: single channel, N_sb = 1, N_st = 1, 2^16 symbols at 2 sps
+    g = golden("cfg1_nsb1")                      # its 511-tap coefficient set
+    rate = 128e9
+    field = gaussian_wdm(1 << 17, rate, n_channels=1, spacing=0.0, dbm_per_channel=2.0,
+                         seed=17)
+    cfg = replace(g.cfg, block_size=block, overlap=overlap)
+    ref = orc.run_cb_blocks(field, cfg, rate, g.coeffs)
+    for dtype in ("c128", "c64"):
+        assert rel_rms(_gpu(field, cfg, g.coeffs, rate, dtype)[0], ref) < TOL[dtype]
+
+
+def _sweep_points():
+    """Every feasible point of the configs[2] grid: N' = FFT size, N = N_sb N',
+    N_ov = per-step memory ceil(2679 / N_st) rounded up to a multiple of
+    2 N_sb; points with N_ov >= N are infeasible."""
+    mem = 2679                                   # configs[0] whole-link memory
+    pts = []
+    for n_st in (1, 2, 3, 5, 8, 15):
+        for n_sb in (1, 3, 5, 9):
+            for rho in (0.5, 0.7, 1.0):
+                for q in (512, 1024, 2048, 4096):
+                    per_step = math.ceil(mem / n_st)
+                    ov = -(-per_step // (2 * n_sb)) * (2 * n_sb)
+                    if ov >= n_sb * q:
+                        continue
+                    pts.append((n_st, n_sb, rho, q, ov))
+    return pts
+
+
+def test_config2_sweep_grid(cuda):
+    # configs[2]: the full N_st x N_sb x rho x N' grid on the configs[0]
+    # waveform (every feasible point)
+    d = np.load(GOLDEN / "sweep_coeffs.npz")
+    rate = 128e9
+    field = gaussian_wdm(1 << 17, rate, n_channels=1, spacing=0.0, dbm_per_channel=2.0,
+                         seed=3)
+    worst = {"c128": 0.0, "c64": 0.0}
+    pts = _sweep_points()
+    assert len(pts) == 261                       # 261 of 288
+    for n_st, n_sb, rho, q, ov in pts:
+        c = load_coeffs(d, f"s{n_st}_b{n_sb}_r{int(rho * 10)}_")
+        cfg = pb.DbpConfig(link=_link(15), variant="CB_ESSFM", n_steps=n_st,
+                           n_subbands=n_sb, splitting_ratio=rho, block_size=n_sb * q,
+                           overlap=ov, oversampling=2.0)
+        ref = orc.run_cb_blocks(field, cfg, rate, c)
+        for dtype in ("c128", "c64"):
+            e = rel_rms(_gpu(field, cfg, c, rate, dtype)[0], ref)
+            worst[dtype] = max(worst[dtype], e)
+            assert e < TOL[dtype], (n_st, n_sb, rho, q, ov, dtype, e)
+
+
+@pytest.mark.parametrize("n_st,overlap", [(1, 10240), (10, 14290)])
+def test_config3_steps(cuda, n_st, overlap):
+    # configs[3]: 50 x 80 km, 5 subbands, N' = 4096; N_st = 50 is a golden case
+    d = np.load(GOLDEN / "cfg4_coeffs.npz")
+    c = load_coeffs(d, f"s{n_st}_")
+    g = golden("cfg4_nsb5_st50")                 # its forward-propagated input
+    cfg = pb.DbpConfig(link=_link(50), variant="CB_ESSFM", n_steps=n_st, n_subbands=5,
+                       splitting_ratio=0.5, block_size=20480, overlap=overlap,
+                       oversampling=1.6)
+    field = np.vstack([g.wave.x, g.wave.y])
+    ref = orc.run_cb_blocks(field, cfg, g.wave.sample_rate, c)
+    for dtype in ("c128", "c64"):
+        e = rel_rms(_gpu(field, cfg, c, g.wave.sample_rate, dtype)[0], ref)
+        assert e < TOL[dtype], (dtype, e)
+
+
+def test_config4_batch_subset(cuda):
+    # configs[4]: a batch of independent 2^20-symbol/ch 5-subband Gaussian
+    # waveforms, c64; checked on a seeded subset of waveforms x blocks
+    g = golden("cfg2_nsb5")                      # configs[1]/[4] geometry
+    rate = 512e9
+    n = 1 << 23
+    batch = 4
+    x = np.stack([gaussian_wdm(n, rate, seed=1000 + k) for k in range(batch)])
+    out = _gpu(x, g.cfg, g.coeffs, rate, "c64")
+    sched = pb.BlockSchedule(n, g.cfg.block_size, g.cfg.overlap)
+    rng = np.random.default_rng(5)
+    for w in rng.choice(batch, 2, replace=False):
+        for b in (0, sched.n_blocks // 2, sched.n_blocks - 1):
+            ref = orc.run_cb_blocks(x[w], g.cfg, rate, g.coeffs, b, b + 1)
+            o0, o1 = sched.output_range(b, b + 1)
+            assert rel_rms(out[w][:, o0:o1], ref[:, o0:o1]) < 1e-5
