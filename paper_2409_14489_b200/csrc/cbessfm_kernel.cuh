@@ -168,9 +168,19 @@ __device__ __forceinline__ Cx<R> tw16(Cx<R> d, int e16) {
   if (e16 == 6)  // (-1 -+ i)/sqrt2
     return INV ? mk(-mul_rsqrt2(d.x + d.y), mul_rsqrt2(d.x - d.y))
                : mk(mul_rsqrt2(d.y - d.x), -mul_rsqrt2(d.x + d.y));
-  const R c = (R)c16(e16);
-  const R s = INV ? (R)s16(e16) : (R)-s16(e16);
-  return mk(d.x * c - d.y * s, d.x * s + d.y * c);
+  // odd sixteenths: cos/sin of pi/8 and 3pi/8 (two-term in float, same
+  // reason as mul_rsqrt2)
+  const double cd = c16(e16), sd = INV ? s16(e16) : -s16(e16);
+  if constexpr (sizeof(R) == 4) {
+    const float ch = (float)cd, sh = (float)sd;
+    const float cl = (float)(cd - (double)ch), sl = (float)(sd - (double)sh);
+    const float lre = __fmaf_rn(d.x, cl, -d.y * sl);
+    const float lim = __fmaf_rn(d.x, sl, d.y * cl);
+    return mk(__fmaf_rn(d.x, ch, __fmaf_rn(-d.y, sh, lre)),
+              __fmaf_rn(d.x, sh, __fmaf_rn(d.y, ch, lim)));
+  } else {
+    return mk(d.x * (R)cd - d.y * (R)sd, d.x * (R)sd + d.y * (R)cd);
+  }
 }
 
 template <typename R, int RAD, bool INV>
@@ -202,15 +212,15 @@ __device__ __forceinline__ void dft_reg(Cx<R>* v) {
 // coalesced), instead of R-1 scattered 8-byte loads.
 
 // Radix schedules (sub-transform sizes NS = 1, R1, R1*R2, ...):
-//   kTail -- radix-8 passes, leftover radix last   (2048: 8 8 8 4); used by
+//   kTail -- radix-16 passes, leftover radix last  (2048: 16 16 8); used by
 //            the field IFFTs and the outer transforms
-//   kHead -- radix-8 passes, leftover radix first  (2048: 4 8 8 8); used by
-//            the in-step field FFT, so its last pass (radix 8, NS = Q/8)
-//            produces exactly the 8 samples the next step's IFFT first pass
-//            (radix 8, NS = 1) consumes and the two fuse (fft2_boundary)
+//   kHead -- radix-16 passes, leftover radix first (2048: 8 16 16); used by
+//            the in-step field FFT, so its last pass (radix 16, NS = Q/16)
+//            produces exactly the 16 samples the next step's IFFT first pass
+//            (radix 16, NS = 1) consumes and the two fuse (fft2_boundary)
 //   kHalf -- radix-4 passes for the half-length real-transform FFTs, which
 //            keeps all Q/8 threads busy on Q/2 points
-constexpr int kMaxRad = 8;
+constexpr int kMaxRad = 16;
 constexpr int kTail = 0, kHead = 1, kHalf = 2;
 
 __host__ __device__ constexpr int sched_radix(int L, int ns, int sched) {
@@ -324,16 +334,26 @@ __device__ __forceinline__ void bar_named(int id, int nthreads) {
 __device__ __forceinline__ int fpos(int p) { return 2 * pad(p >> 1) + (p & 1); }
 
 // ------------------------------------------------------------------------
+// Field FFT thread mapping: the two polarisations of a butterfly run on the
+// two half-warps (lane bit 4 selects x or y), so a thread holds one
+// radix-16 butterfly (16 complex values) and both half-warps read the same
+// twiddle rows in the same instruction.
+
+template <int NT>
+__device__ __forceinline__ int fpol(int t) { return (t >> 4) & 1; }
+template <int NT>
+__device__ __forceinline__ int fbase(int t) { return ((t >> 5) << 4) | (t & 15); }
+
 // Hooks fused into the first (pre: after the loads) or last (post: before
-// the stores) pass of a two-polarisation FFT. Element r of butterfly j sits
-// at position j + r*LR on load; natural output r sits at d0 + r*NS on store
-// and lives in v[bitrev(r)].
+// the stores) pass of a field FFT. Element r of butterfly j sits at position
+// j + r*LR on load; natural output r sits at d0 + r*NS on store and lives
+// in v[bitrev(r)]. v is this thread's polarisation.
 
 struct NoHook {
   template <typename R, int RAD, int LR>
-  __device__ __forceinline__ void pre(int, Cx<R>*, Cx<R>*) {}
+  __device__ __forceinline__ void pre(int, Cx<R>*) {}
   template <typename R, int RAD, int NS>
-  __device__ __forceinline__ void post(int, Cx<R>*, Cx<R>*) {}
+  __device__ __forceinline__ void post(int, Cx<R>*) {}
 };
 
 // Multiply by a dispersion phasor row (dbp.py:395 / :399); ph is indexed by
@@ -342,28 +362,29 @@ template <typename R>
 struct PhasorHook : NoHook {
   const Cx<R>* ph;
   template <typename, int RAD, int NS>
-  __device__ __forceinline__ void post(int d0, Cx<R>* vx, Cx<R>* vy) {
+  __device__ __forceinline__ void post(int d0, Cx<R>* v) {
 #pragma unroll
-    for (int r = 0; r < RAD; ++r) {
-      const Cx<R> w = ldg(ph + d0 + r * NS);
-      vx[bitrev<RAD>(r)] = cmul(vx[bitrev<RAD>(r)], w);
-      vy[bitrev<RAD>(r)] = cmul(vy[bitrev<RAD>(r)], w);
-    }
+    for (int r = 0; r < RAD; ++r) v[bitrev<RAD>(r)] = cmul(v[bitrev<RAD>(r)], ldg(ph + d0 + r * NS));
   }
 };
 
 // Write the intensity |x|^2 + |y|^2 (dbp.py:193) of the just-computed time
-// samples into the packed real array I (float view of IS).
+// samples into the packed real array I (float view of IS); the partner
+// half-warp holds the other polarisation at the same positions, and each
+// half-warp writes half of the positions.
 template <typename R>
 struct IntensityHook : NoHook {
   R* I;
   template <typename, int RAD, int NS>
-  __device__ __forceinline__ void post(int d0, Cx<R>* vx, Cx<R>* vy) {
+  __device__ __forceinline__ void post(int d0, Cx<R>* v) {
+    const int pol = (threadIdx.x >> 4) & 1;
     R* base = I + fpos(d0);
 #pragma unroll
     for (int r = 0; r < RAD; ++r) {
-      const Cx<R> a = vx[bitrev<RAD>(r)], b = vy[bitrev<RAD>(r)];
-      base[2 * pad(r * NS / 2)] = a.x * a.x + a.y * a.y + (b.x * b.x + b.y * b.y);
+      const Cx<R> a = v[bitrev<RAD>(r)];
+      const R own = a.x * a.x + a.y * a.y;
+      const R other = __shfl_xor_sync(0xffffffffu, own, 16);
+      if ((r & 1) == pol) base[2 * pad(r * NS / 2)] = pol ? other + own : own + other;
     }
   }
 };
@@ -379,22 +400,21 @@ __device__ __forceinline__ void sincos_acc<double>(double a, double* s, double* 
   sincos(a, s, c);
 }
 
-// Rotate both polarisations by exp(-i theta), theta = scale * th[p]
-// (dbp.py:196, :208); th is the float view of the packed irfft output.
+// Rotate by exp(-i theta), theta = scale * th[p] (dbp.py:196, :208); th is
+// the float view of the packed irfft output. Both half-warps read the same
+// theta (broadcast) and rotate their own polarisation.
 template <typename R>
 struct RotationHook : NoHook {
   const R* th;
   R scale;
   template <typename, int RAD, int LR>
-  __device__ __forceinline__ void pre(int j, Cx<R>* vx, Cx<R>* vy) {
+  __device__ __forceinline__ void pre(int j, Cx<R>* v) {
     const R* base = th + fpos(j);
 #pragma unroll
     for (int r = 0; r < RAD; ++r) {
       R s, c;
       sincos_acc<R>(base[2 * pad(r * LR / 2)] * scale, &s, &c);
-      const Cx<R> rot = mk(c, -s);
-      vx[r] = cmul(vx[r], rot);
-      vy[r] = cmul(vy[r], rot);
+      v[r] = cmul(v[r], mk(c, -s));
     }
   }
 };
@@ -408,8 +428,6 @@ struct RotationHook : NoHook {
 // pass's addressing inside the step loop (ptxas otherwise hoists every
 // pass's address registers out of the loop and spills).
 
-// Two-polarisation pass: thread j runs butterfly j of x AND of y, sharing
-// the index arithmetic and the twiddle row.
 // Butterfly run by thread slot t in a pass. The radix-4 pass with NS = 4
 // scatters to 16*(j/4) + j%4 + 4r, a 4-way bank conflict for consecutive
 // j; permuting j inside each 64-butterfly group as below makes both its
@@ -424,13 +442,16 @@ __host__ __device__ constexpr int bfly(int t) {
   }
 }
 
-// Twiddle rows of the butterflies a thread runs in the pass with
-// sub-transform size NS of a length-L FFT (PER butterflies of radix RAD).
+// Twiddle rows of the butterflies a thread runs in one pass. FIELD: the
+// field FFT mapping (butterfly fbase(t) + p * NT/2 of polarisation fpol(t));
+// otherwise the half-length mapping (butterfly bfly(t + p * NT)).
 template <typename R, int L, int NT, int NS, int SCHED>
 struct PassRows {
+  static constexpr bool kField = SCHED != kHalf;
   static constexpr bool kLast = NS >= L;
   static constexpr int RAD = kLast ? 1 : sched_radix(L, NS, SCHED);
-  static constexpr int PER = kLast ? 1 : ((L / RAD) >= NT ? (L / RAD) / NT : 1);
+  static constexpr int SLOTS = kField ? NT / 2 : NT;  // threads per butterfly set
+  static constexpr int PER = kLast ? 1 : ((L / RAD) >= SLOTS ? (L / RAD) / SLOTS : 1);
   static constexpr bool kHas = !kLast && NS > 1;
   Cx<R> w[PER][RAD];
   // Issue the loads (no use yet): called one pass early so the L2 latency
@@ -442,9 +463,14 @@ struct PassRows {
       const int tid = threadIdx.x;
 #pragma unroll
       for (int p = 0; p < PER; ++p) {
-        const int t = tid + p * NT;
-        const int j = bfly<L, NS, RAD>(t);
-        if ((L / RAD) >= NT || t < L / RAD) load_row<RAD, NS>(tw, j % NS, w[p]);
+        if constexpr (kField) {
+          const int j = fbase<NT>(tid) + p * SLOTS;
+          load_row<RAD, NS>(tw, j % NS, w[p]);
+        } else {
+          const int t = tid + p * NT;
+          const int j = bfly<L, NS, RAD>(t);
+          if ((L / RAD) >= NT || t < L / RAD) load_row<RAD, NS>(tw, j % NS, w[p]);
+        }
       }
     }
   }
@@ -457,52 +483,45 @@ __device__ __forceinline__ void fft2_pass(Cx<R>* __restrict__ F, const Cx<R>* __
                                           NextRows& next, const Cx<R>* __restrict__ twp_next) {
   constexpr int RAD = sched_radix(Q, NS, SCHED);
   constexpr int LR = Q / RAD;
-  constexpr int NB = Q / RAD;
-  static_assert(NB % NT == 0, "butterflies must tile the block");
-  constexpr int PER = NB / NT;
+  constexpr int SLOTS = NT / 2;
+  static_assert((Q / RAD) % SLOTS == 0, "butterflies must tile the half-block");
+  constexpr int PER = (Q / RAD) / SLOTS;
   constexpr int SF = padded_len(Q);
-  Cx<R> vx[PER][RAD], vy[PER][RAD];
+  Cx<R> v[PER][RAD];
   const int tid = threadIdx.x + *zero;
+  Cx<R>* Fp = F + fpol<NT>(tid) * SF;
+  const int jb = fbase<NT>(tid);
 #pragma unroll
   for (int p = 0; p < PER; ++p) {
-    const int j = tid + p * NT;
-    const Cx<R>* bx = F + pad(j);
+    const int j = jb + p * SLOTS;
+    const Cx<R>* b = Fp + pad(j);
 #pragma unroll
-    for (int r = 0; r < RAD; ++r) {
-      vx[p][r] = bx[pad(r * LR)];
-      vy[p][r] = bx[SF + pad(r * LR)];
-    }
-    if constexpr (FIRST) hook.template pre<R, RAD, LR>(j, vx[p], vy[p]);
+    for (int r = 0; r < RAD; ++r) v[p][r] = b[pad(r * LR)];
+    if constexpr (FIRST) hook.template pre<R, RAD, LR>(j, v[p]);
     if constexpr (NS > 1) {
 #pragma unroll
-      for (int r = 1; r < RAD; ++r) {
-        vx[p][r] = INV ? cmulc(vx[p][r], rows.w[p][r]) : cmul(vx[p][r], rows.w[p][r]);
-        vy[p][r] = INV ? cmulc(vy[p][r], rows.w[p][r]) : cmul(vy[p][r], rows.w[p][r]);
-      }
+      for (int r = 1; r < RAD; ++r)
+        v[p][r] = INV ? cmulc(v[p][r], rows.w[p][r]) : cmul(v[p][r], rows.w[p][r]);
     }
-    dft_reg<R, RAD, INV>(vx[p]);
-    dft_reg<R, RAD, INV>(vy[p]);
+    dft_reg<R, RAD, INV>(v[p]);
   }
   __syncthreads();
 #pragma unroll
   for (int p = 0; p < PER; ++p) {
-    const int j = tid + p * NT;
+    const int j = jb + p * SLOTS;
     const int d0 = (j / NS) * NS * RAD + j % NS;
-    if constexpr (LAST) hook.template post<R, RAD, NS>(d0, vx[p], vy[p]);
-    Cx<R>* bx = F + pad(d0);
+    if constexpr (LAST) hook.template post<R, RAD, NS>(d0, v[p]);
+    Cx<R>* b = Fp + pad(d0);
 #pragma unroll
-    for (int r = 0; r < RAD; ++r) {
-      bx[pad(r * NS)] = vx[p][bitrev<RAD>(r)];
-      bx[SF + pad(r * NS)] = vy[p][bitrev<RAD>(r)];
-    }
+    for (int r = 0; r < RAD; ++r) b[pad(r * NS)] = v[p][bitrev<RAD>(r)];
   }
   next.fetch(twp_next);
   __syncthreads();
 }
 
-// Runs the passes NS, NS*R, ... of a length-Q two-polarisation FFT with
-// schedule SCHED, stopping before the pass with sub-transform size STOP
-// (STOP = Q: to the end). rows: this pass's prefetched twiddle rows.
+// Runs the passes NS, NS*R, ... of a length-Q field FFT with schedule
+// SCHED, stopping before the pass with sub-transform size STOP (STOP = Q:
+// to the end). rows: this pass's prefetched twiddle rows.
 template <typename R, int Q, int NT, int SCHED, int NS, int STOP, bool INV, class Pre,
           class Post>
 struct Fft2Run {
@@ -541,72 +560,55 @@ __device__ __forceinline__ void fft2(Cx<R>* F, const Cx<R>* twp, const volatile 
   Fft2Run<R, Q, NT, SCHED, NS0, STOP, INV, Pre, Post>::run(F, twp, z, pre, post, rows);
 }
 
-// Step boundary: the last pass of the in-step forward FFT (kHead, radix 8,
-// NS = Q/8), the next dispersion phasor, and the first pass of the next
-// step's IFFT (kTail, radix 8, NS = 1) in one load/compute/store round: the
-// forward butterfly j produces samples j + r*Q/8, exactly the inputs of
+// Step boundary: the last pass of the in-step forward FFT (kHead, radix R,
+// NS = Q/R), the next dispersion phasor, and the first pass of the next
+// step's IFFT (kTail, radix R, NS = 1) in one load/compute/store round: the
+// forward butterfly j produces samples j + r*Q/R, exactly the inputs of
 // inverse butterfly j (dbp.py:398, :395, :396).
 template <typename R, int Q, int NT>
 __device__ __forceinline__ void fft2_boundary(Cx<R>* __restrict__ F,
                                               const Cx<R>* __restrict__ twHead,
-                                              const Cx<R>* __restrict__ twTail,
                                               const Cx<R>* __restrict__ ph,
                                               const volatile int* zero) {
-  constexpr int RAD = 8;
+  constexpr int RAD = sched_radix(Q, 1, kTail);
   constexpr int NSF = Q / RAD;  // forward last pass
-  static_assert(sched_radix(Q, NSF, kHead) == RAD && NSF * RAD == Q, "kHead must end radix-8");
-  static_assert(sched_radix(Q, 1, kTail) == RAD, "kTail must start radix-8");
+  static_assert(sched_radix(Q, NSF, kHead) == RAD, "kHead must end with kTail's first radix");
   constexpr int LR = Q / RAD;
-  constexpr int PER = (Q / RAD) / NT;
-  static_assert((Q / RAD) % NT == 0, "butterflies must tile the block");
+  constexpr int SLOTS = NT / 2;
+  static_assert((Q / RAD) % SLOTS == 0, "butterflies must tile the half-block");
+  constexpr int PER = (Q / RAD) / SLOTS;
   constexpr int SF = padded_len(Q);
   PassRows<R, Q, NT, NSF, kHead> rows;
   rows.fetch(twHead);
-  Cx<R> vx[PER][RAD], vy[PER][RAD];
+  Cx<R> v[PER][RAD];
   const int tid = threadIdx.x + *zero;
+  Cx<R>* Fp = F + fpol<NT>(tid) * SF;
+  const int jb = fbase<NT>(tid);
 #pragma unroll
   for (int p = 0; p < PER; ++p) {
-    const int j = tid + p * NT;
-    const Cx<R>* bx = F + pad(j);
+    const int j = jb + p * SLOTS;
+    const Cx<R>* b = Fp + pad(j);
 #pragma unroll
-    for (int r = 0; r < RAD; ++r) {
-      vx[p][r] = bx[pad(r * LR)];
-      vy[p][r] = bx[SF + pad(r * LR)];
-    }
+    for (int r = 0; r < RAD; ++r) v[p][r] = b[pad(r * LR)];
 #pragma unroll
-    for (int r = 1; r < RAD; ++r) {
-      vx[p][r] = cmul(vx[p][r], rows.w[p][r]);
-      vy[p][r] = cmul(vy[p][r], rows.w[p][r]);
-    }
-    dft_reg<R, RAD, false>(vx[p]);
-    dft_reg<R, RAD, false>(vy[p]);
+    for (int r = 1; r < RAD; ++r) v[p][r] = cmul(v[p][r], rows.w[p][r]);
+    dft_reg<R, RAD, false>(v[p]);
     // natural output r sits at j + r*LR in v[bitrev(r)]: apply the phasor
     // and hand it to the inverse butterfly as its input r
-    Cx<R> ux[RAD], uy[RAD];
+    Cx<R> u[RAD];
 #pragma unroll
-    for (int r = 0; r < RAD; ++r) {
-      const Cx<R> w = ldg(ph + j + r * LR);
-      ux[r] = cmul(vx[p][bitrev<RAD>(r)], w);
-      uy[r] = cmul(vy[p][bitrev<RAD>(r)], w);
-    }
-    dft_reg<R, RAD, true>(ux);
-    dft_reg<R, RAD, true>(uy);
+    for (int r = 0; r < RAD; ++r) u[r] = cmul(v[p][bitrev<RAD>(r)], ldg(ph + j + r * LR));
+    dft_reg<R, RAD, true>(u);
 #pragma unroll
-    for (int r = 0; r < RAD; ++r) {
-      vx[p][r] = ux[r];
-      vy[p][r] = uy[r];
-    }
+    for (int r = 0; r < RAD; ++r) v[p][r] = u[r];
   }
   __syncthreads();
 #pragma unroll
   for (int p = 0; p < PER; ++p) {
-    const int j = tid + p * NT;
-    Cx<R>* bx = F + pad(j * RAD);  // inverse first pass: NS = 1, d0 = 8j
+    const int j = jb + p * SLOTS;
+    Cx<R>* b = Fp + pad(j * RAD);  // inverse first pass: NS = 1, d0 = R*j
 #pragma unroll
-    for (int r = 0; r < RAD; ++r) {
-      bx[pad(r)] = vx[p][bitrev<RAD>(r)];
-      bx[SF + pad(r)] = vy[p][bitrev<RAD>(r)];
-    }
+    for (int r = 0; r < RAD; ++r) b[pad(r)] = v[p][bitrev<RAD>(r)];
   }
   __syncthreads();
 }
@@ -1017,11 +1019,13 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
     rot.scale = prm.theta_scale[st];
     const Cx<R>* ph_next = ph_rank + (size_t)prm.ph_index[st + 1] * ph_tab;
     if (st + 1 < prm.n_steps) {
-      fft2<R, Q, NT, kHead, false, RotationHook<R>, NoHook, 1, Q / 8>(F, twpF, &s_zero, rot);
+      fft2<R, Q, NT, kHead, false, RotationHook<R>, NoHook, 1, Q / sched_radix(Q, 1, kTail)>(
+          F, twpF, &s_zero, rot);
       CB_MARK(8 + 8 * st + 6);
-      fft2_boundary<R, Q, NT>(F, twpF, twpT, ph_next, &s_zero);
+      fft2_boundary<R, Q, NT>(F, twpF, ph_next, &s_zero);
       CB_MARK(8 + 8 * st + 7);
-      fft2<R, Q, NT, kTail, true, NoHook, IntensityHook<R>, 8>(F, twpT, &s_zero, NoHook(), ih);
+      fft2<R, Q, NT, kTail, true, NoHook, IntensityHook<R>, sched_radix(Q, 1, kTail)>(
+          F, twpT, &s_zero, NoHook(), ih);
     } else {
       PhasorHook<R> ph1;
       ph1.ph = ph_next;

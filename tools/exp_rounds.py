@@ -11,7 +11,7 @@ cfg, coeffs = bench.workload_cfg()
 dtype = sys.argv[1] if len(sys.argv) > 1 else "c64"
 eng = pb.DbpEngine(cfg, coeffs, bench.RATE, dtype=dtype)
 ct = torch.complex64 if dtype == "c64" else torch.complex128
-nb = pb.BlockSchedule(bench.N_SAMPLES, 10240, 2860).n_blocks
+nb = pb.BlockSchedule(bench.WL["n"], 10240, 2860).n_blocks
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
 def timeit(fn, reps=30):
@@ -26,11 +26,11 @@ def timeit(fn, reps=30):
     return float(np.median(ts))
 
 for batch in (1, 2, 4, 8):
-    x = torch.from_numpy(np.stack([gaussian_wdm(bench.N_SAMPLES, bench.RATE, seed=s) for s in range(batch)])).cuda().to(ct)
+    x = torch.from_numpy(np.stack([gaussian_wdm(bench.WL["n"], bench.RATE, seed=s) for s in range(batch)])).cuda().to(ct)
     out = torch.empty_like(x)
     t = timeit(lambda: eng.run_device(x, out))
-    print(f"batch {batch}: {t:.3f} ms/step  {batch*bench.SYMBOLS_PER_WAVE/t/1e-3:.3e} 2D/s", flush=True)
-x = torch.from_numpy(gaussian_wdm(bench.N_SAMPLES, bench.RATE, seed=0)[None]).cuda().to(ct)
+    print(f"batch {batch}: {t:.3f} ms/step  {batch*bench.symbols_per_wave()/t/1e-3:.3e} 2D/s", flush=True)
+x = torch.from_numpy(gaussian_wdm(bench.WL["n"], bench.RATE, seed=0)[None]).cuda().to(ct)
 out = torch.empty_like(x)
 for k in (2, 3, 4):
     cuts = [nb * i // k for i in range(k + 1)]

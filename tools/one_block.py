@@ -10,7 +10,7 @@ dtype, b0, b1 = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
 cfg, coeffs = bench.workload_cfg()
 eng = pb.DbpEngine(cfg, coeffs, bench.RATE, dtype=dtype)
 ct = torch.complex64 if dtype == "c64" else torch.complex128
-x = torch.from_numpy(gaussian_wdm(bench.N_SAMPLES, bench.RATE, seed=0)[None]).cuda().to(ct)
+x = torch.from_numpy(gaussian_wdm(bench.WL["n"], bench.RATE, seed=0)[None]).cuda().to(ct)
 out = torch.empty_like(x)
 for _ in range(3):
     eng.run_device(x, out, block_range=(b0, b1))

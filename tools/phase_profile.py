@@ -14,7 +14,7 @@ dtype = sys.argv[1] if len(sys.argv) > 1 else "c64"
 cfg, coeffs = bench.workload_cfg()
 eng = pb.DbpEngine(cfg, coeffs, bench.RATE, dtype=dtype)
 ct = torch.complex64 if dtype == "c64" else torch.complex128
-x = torch.from_numpy(gaussian_wdm(bench.N_SAMPLES, bench.RATE, seed=0)[None]).cuda().to(ct)
+x = torch.from_numpy(gaussian_wdm(bench.WL["n"], bench.RATE, seed=0)[None]).cuda().to(ct)
 out = torch.empty_like(x)
 lib = _native.load()
 names = {0: "start", 1: "loaded", 2: "outer fwd (FFT+exchange)", 3: "first IFFT",
