@@ -2,6 +2,8 @@
 // cudaLaunchKernelEx, dynamic shared memory opt-in, non-portable clusters).
 #pragma once
 
+#include <cstdlib>
+
 #include "cbessfm_kernel.cuh"
 
 namespace cbessfm {
@@ -38,6 +40,9 @@ cudaError_t launch_one(const Params<R>& prm, int64_t nclusters, cudaStream_t str
       if (e != cudaSuccess) return e;
     }
     __atomic_fetch_or(&configured, bit, __ATOMIC_RELEASE);
+  }
+  if (const char* env = getenv("CBESSFM_CARVEOUT")) {  // experiment hook
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(env));
   }
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(NT, 1, 1);

@@ -263,7 +263,7 @@ class DbpEngine:
 
     run_device(x)  -- x [B, 2, n] complex CUDA tensor already in HBM.
     run_host(x)    -- x [B, 2, n] complex CPU tensor (pinned for async
-                      copies); H2D, kernel and D2H are stream-ordered.
+                      copies); H2D, kernel and D2H overlap chunk by chunk.
     """
 
     def __init__(self, cfg, coeffs, sample_rate: float, dtype: str = "c64",
@@ -298,23 +298,98 @@ class DbpEngine:
             self._dev_out = torch.empty_like(self._dev_in)
         return self._dev_in, self._dev_out
 
-    def run_host(self, x, out=None, stream=None):
-        """Host [B, 2, n] in, host [B, 2, n] out (pinned if given pinned)."""
+    def run_host(self, x, out=None, stream=None, chunks: int = 8):
+        """Host [B, 2, n] in, host [B, 2, n] out (pinned for overlap).
+
+        Pipelined: the waveform is copied in ``chunks`` sample ranges on a
+        copy stream; as soon as the blocks whose windows lie inside the
+        copied prefix are runnable they launch on a compute stream (block
+        ranges of the same schedule), and their kept samples go back on a
+        third stream -- H2D, the kernel and D2H overlap. The wrap-around
+        blocks (window crossing sample 0 or n) run last. Returns ``out``
+        with all work enqueued behind ``stream``."""
         torch = _torch()
         if x.dtype != self.torch_dtype:
             raise ValueError(f"host input must be {self.torch_dtype}")
         if x.dim() == 2:
             x = x.unsqueeze(0)
-        if self.cfg.block_size > x.shape[-1]:
+        n = x.shape[-1]
+        if self.cfg.block_size > n:
             raise ValueError("block_size exceeds the sequence length")
         din, dout = self._buffers(x.shape)
         if out is None:
             out = torch.empty(x.shape, dtype=x.dtype, pin_memory=x.is_pinned())
         stream = stream or torch.cuda.current_stream(self.device)
-        with torch.cuda.stream(stream):
-            din.copy_(x, non_blocking=True)
-            launch(self.plan, din, dout, stream=stream)
-            out.copy_(dout, non_blocking=True)
+        if not hasattr(self, "_streams"):
+            self._streams = tuple(torch.cuda.Stream(self.device) for _ in range(3))
+        s_in, s_k, s_out = self._streams
+        sched = self.schedule(n)
+        keep, half, nb = sched.keep, sched.half, sched.n_blocks
+        N = self.cfg.block_size
+        # interior blocks: window [b*keep - half, b*keep - half + N) inside [0, n)
+        first = -(-half // keep)
+        last = (n + half - N) // keep          # inclusive
+        groups = []                            # (copy_end, b0, b1)
+        chunks = max(1, min(chunks, max(1, last - first + 1)))
+        prev_b = first
+        for c in range(1, chunks + 1):
+            end = n if c == chunks else (n * c) // chunks
+            b1 = min(last, (end + half - N) // keep) + 1
+            if b1 > prev_b:
+                groups.append((end, prev_b, b1))
+                prev_b = b1
+        start_ev = torch.cuda.Event()
+        start_ev.record(stream)
+        for s_ in (s_in, s_k, s_out):
+            s_.wait_event(start_ev)
+        rows = [(b, p) for b in range(x.shape[0]) for p in range(2)]
+
+        def h2d(a, b):                    # contiguous row pieces only
+            for r, p in rows:
+                din[r, p, a:b].copy_(x[r, p, a:b], non_blocking=True)
+
+        def d2h(a, b):
+            for r, p in rows:
+                out[r, p, a:b].copy_(dout[r, p, a:b], non_blocking=True)
+
+        copied = 0
+        for end, b0, b1 in groups:
+            with torch.cuda.stream(s_in):
+                if end > copied:
+                    h2d(copied, end)
+                    copied = end
+                ev_in = torch.cuda.Event()
+                ev_in.record(s_in)
+            s_k.wait_event(ev_in)
+            launch(self.plan, din, dout, block_range=(b0, b1), stream=s_k)
+            ev_k = torch.cuda.Event()
+            ev_k.record(s_k)
+            s_out.wait_event(ev_k)
+            o0, o1 = sched.output_range(b0, b1)
+            with torch.cuda.stream(s_out):
+                d2h(o0, o1)
+        with torch.cuda.stream(s_in):
+            if copied < n:
+                h2d(copied, n)
+            ev_in = torch.cuda.Event()
+            ev_in.record(s_in)
+        s_k.wait_event(ev_in)
+        # wrap-around blocks: [0, first) and (last, nb)
+        rest = [(0, min(first, nb))] + [(max(last + 1, first), nb)]
+        ev_k = torch.cuda.Event()
+        for b0, b1 in rest:
+            if b1 > b0:
+                launch(self.plan, din, dout, block_range=(b0, b1), stream=s_k)
+        ev_k.record(s_k)
+        s_out.wait_event(ev_k)
+        with torch.cuda.stream(s_out):
+            for b0, b1 in rest:
+                if b1 > b0:
+                    o0, o1 = sched.output_range(b0, b1)
+                    d2h(o0, o1)
+        done = torch.cuda.Event()
+        done.record(s_out)
+        stream.wait_event(done)
         return out
 
 

@@ -180,3 +180,15 @@ def test_gpu_compute_time_shards_reassemble(cuda):
         xs = gather_slice(x, w.in_origin, w.in_length)
         out[:, :, w.out_begin:w.out_end] = run(xs, w, n)
     assert rel_rms(out[0], g.out) < 1e-12
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 8])
+def test_run_host_pipeline_matches_device_path(cuda, chunks):
+    import torch
+    for name in ("cfg2_nsb5", "cfg1_nsb3_st2", "cfg1_nsb1"):
+        g = golden(name)
+        eng = pb.DbpEngine(g.cfg, g.coeffs, g.wave.sample_rate, dtype="c128")
+        x = torch.from_numpy(np.vstack([g.wave.x, g.wave.y])[None]).pin_memory()
+        out = eng.run_host(x, chunks=chunks)
+        torch.cuda.synchronize()
+        assert rel_rms(out[0].numpy(), g.out) < 1e-12, (name, chunks)
