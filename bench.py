@@ -377,7 +377,7 @@ def main():
         e2e = {"value": sym_per_step / (te / args.steps * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(hx.numel() * hx.element_size()),
                "d2h_bytes_per_step": int(hout.numel() * hout.element_size()),
-               "path": "DbpEngine.run_host: pinned host -> H2D -> fused kernel -> D2H"}
+               "path": "C ABI cbessfm_run_host (via DbpEngine.run_host): pinned host buffers, chunked H2D / fused kernel / D2H overlap"}
 
     # the only collective of the path: final gather of the kept samples to
     # every rank (all_gather over NCCL), timed separately from `value`

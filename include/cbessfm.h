@@ -91,6 +91,20 @@ typedef struct {
   int64_t block_end;       /*   overlap-save schedule (dbp.py:471-477)     */
 } cbessfm_io;
 
+/* Host-buffer variant (the call a reference-side binding makes with the
+ * waveform in host memory): in/out are HOST pointers, layout [batch][2][n]
+ * contiguous, of the plan's dtype; page-locked memory is required for the
+ * copies to overlap. The waveform is copied in `chunks` sample ranges and
+ * every block range launches as soon as its input window has landed, while
+ * finished kept samples are copied back (three-way overlap). */
+typedef struct {
+  const void* in;
+  void* out;
+  int64_t n;               /* samples per polarisation                    */
+  int64_t batch;           /* waveforms                                   */
+  int32_t chunks;          /* pipeline depth (<= 0: default 8)            */
+} cbessfm_host_io;
+
 typedef struct {
   int32_t threads_per_cta;
   int32_t cluster_size;
@@ -119,6 +133,10 @@ cbessfm_status cbessfm_plan_info_get(const cbessfm_plan* plan, cbessfm_plan_info
  * the legacy default stream). Asynchronous; errors of the launch itself
  * are reported, kernel faults surface at the caller's next sync. */
 cbessfm_status cbessfm_run(const cbessfm_plan* plan, const cbessfm_io* io, void* stream);
+
+/* Enqueue H2D, the fused kernel and D2H on `stream` for host buffers;
+ * returns once enqueued (synchronise `stream` before reading `out`). */
+cbessfm_status cbessfm_run_host(const cbessfm_plan* plan, const cbessfm_host_io* io, void* stream);
 
 /* Free the plan's device tables. */
 cbessfm_status cbessfm_plan_destroy(cbessfm_plan* plan);

@@ -43,6 +43,11 @@ class Io(C.Structure):
                 ("block_begin", C.c_int64), ("block_end", C.c_int64)]
 
 
+class HostIo(C.Structure):
+    _fields_ = [("in_", C.c_void_p), ("out", C.c_void_p), ("n", C.c_int64),
+                ("batch", C.c_int64), ("chunks", C.c_int32)]
+
+
 class PlanInfo(C.Structure):
     _fields_ = [("threads_per_cta", C.c_int32), ("cluster_size", C.c_int32),
                 ("smem_per_cta", C.c_int64),
@@ -57,6 +62,7 @@ SIGNATURES = {
     "cbessfm_plan_create": (C.c_int, [C.POINTER(Desc), C.POINTER(C.c_void_p)]),
     "cbessfm_plan_info_get": (C.c_int, [C.c_void_p, C.POINTER(PlanInfo)]),
     "cbessfm_run": (C.c_int, [C.c_void_p, C.POINTER(Io), C.c_void_p]),
+    "cbessfm_run_host": (C.c_int, [C.c_void_p, C.POINTER(HostIo), C.c_void_p]),
     "cbessfm_plan_destroy": (C.c_int, [C.c_void_p]),
     "cbessfm_last_error": (C.c_char_p, []),
     "cbessfm_debug_phase_times": (C.c_int32, [C.c_void_p, C.POINTER(C.c_int64), C.c_int32]),
@@ -145,6 +151,12 @@ class NativePlan:
                 block_begin, block_end)
         check(self._lib.cbessfm_run(self.handle, C.byref(io), C.c_void_p(stream)),
               "cbessfm_run")
+
+    def run_host(self, *, in_ptr: int, out_ptr: int, n: int, batch: int, chunks: int,
+                 stream: int) -> None:
+        io = HostIo(in_ptr, out_ptr, n, batch, chunks)
+        check(self._lib.cbessfm_run_host(self.handle, C.byref(io), C.c_void_p(stream)),
+              "cbessfm_run_host")
 
     def __del__(self):
         h = getattr(self, "handle", None)

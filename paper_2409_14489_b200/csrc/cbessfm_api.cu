@@ -4,6 +4,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -88,6 +90,9 @@ struct cbessfm_plan {
   void* twN = nullptr;     // [P*Q]
   void* twp = nullptr;     // per-pass twiddle rows
   long long* dbg = nullptr;  // phase clocks (CB_PHASE_PROFILE builds)
+  // host-buffer pipeline (cbessfm_run_host): streams created on first use
+  std::mutex host_mu;
+  std::vector<cudaStream_t> host_streams;  // [0] copy in, [1] copy out, [2..] compute
 };
 
 namespace {
@@ -205,6 +210,7 @@ cbessfm_status upload_all(cbessfm_plan* p, const cbessfm_desc* d) {
 
 void free_plan(cbessfm_plan* p) {
   if (!p) return;
+  for (cudaStream_t st : p->host_streams) cudaStreamDestroy(st);
   cudaFree(p->phasor);
   cudaFree(p->ph_index);
   cudaFree(p->mimo);
@@ -336,6 +342,13 @@ cbessfm_status cbessfm_plan_create(const cbessfm_desc* d, cbessfm_plan** out) {
     delete p;
     return cuda_fail(e, "cudaSetDevice");
   }
+  // cbessfm_run_host allocates its staging buffers stream-ordered: keep
+  // freed blocks in the device's default pool instead of returning them
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, d->device) == cudaSuccess) {
+    uint64_t keep_all = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep_all);
+  }
   const cbessfm_status st =
       p->dtype == CBESSFM_C64 ? upload_all<float>(p, d) : upload_all<double>(p, d);
   if (st != CBESSFM_OK) {
@@ -387,6 +400,87 @@ cbessfm_status cbessfm_run(const cbessfm_plan* p, const cbessfm_io* io, void* st
   else
     e = dispatch<double>(p->P, make_params<double>(p, io), p->Q, nclusters, st, nullptr);
   if (e != cudaSuccess) return cuda_fail(e, "cbessfm kernel launch");
+  return CBESSFM_OK;
+}
+
+cbessfm_status cbessfm_run_host(const cbessfm_plan* cp, const cbessfm_host_io* io, void* stream) {
+  g_err.clear();
+  if (!cp || !io) return fail(CBESSFM_ERR_INVALID, "null plan or io");
+  if (!io->in || !io->out) return fail(CBESSFM_ERR_INVALID, "null input or output buffer");
+  if (io->n < cp->N) return fail(CBESSFM_ERR_INVALID, "block_size exceeds the sequence length");
+  if (io->batch <= 0) return fail(CBESSFM_ERR_INVALID, "batch must be positive");
+  cbessfm_plan* p = const_cast<cbessfm_plan*>(cp);  // only the stream pool is touched
+  const int64_t n = io->n, batch = io->batch;
+  const int64_t keep = p->N - p->overlap, half = p->overlap / 2;
+  const int64_t nb = cbessfm_num_blocks(n, p->N, p->overlap);
+  const int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(io->chunks > 0 ? io->chunks : 8, nb));
+  const size_t esz = p->dtype == CBESSFM_C64 ? 8 : 16;
+  const size_t rowb = (size_t)n * esz, rows = (size_t)batch * 2;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  std::lock_guard<std::mutex> lock(p->host_mu);
+  cudaError_t e;
+  while ((int)p->host_streams.size() < 2 + chunks) {
+    cudaStream_t s2;
+    if ((e = cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(e, "stream create");
+    p->host_streams.push_back(s2);
+  }
+  cudaStream_t s_in = p->host_streams[0], s_out = p->host_streams[1];
+  void *din = nullptr, *dout = nullptr;
+  if ((e = cudaMallocAsync(&din, rows * rowb, st)) != cudaSuccess) return cuda_fail(e, "alloc in");
+  if ((e = cudaMallocAsync(&dout, rows * rowb, st)) != cudaSuccess) return cuda_fail(e, "alloc out");
+  std::vector<cudaEvent_t> evs;
+  auto event = [&](cudaStream_t s2) {
+    cudaEvent_t ev;
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    cudaEventRecord(ev, s2);
+    evs.push_back(ev);
+    return ev;
+  };
+  cudaEvent_t ev0 = event(st);
+  for (int i = 0; i < 2 + chunks; ++i) cudaStreamWaitEvent(p->host_streams[i], ev0, 0);
+  // column ranges [a, b) of every (waveform, polarisation) row in one call
+  auto h2d = [&](int64_t a, int64_t b) {
+    return cudaMemcpy2DAsync((char*)din + a * esz, rowb, (const char*)io->in + a * esz, rowb,
+                             (size_t)(b - a) * esz, rows, cudaMemcpyHostToDevice, s_in);
+  };
+  auto d2h = [&](int64_t a, int64_t b) {
+    return cudaMemcpy2DAsync((char*)io->out + a * esz, rowb, (const char*)dout + a * esz, rowb,
+                             (size_t)(b - a) * esz, rows, cudaMemcpyDeviceToHost, s_out);
+  };
+  // same schedule as DbpEngine.run_host: wrap piece first, then `chunks`
+  // sample ranges; blocks whose windows end inside the copied prefix run
+  // as soon as it lands, the last chunk takes the remaining blocks
+  const int64_t wrap = half > 0 ? n - half : n;
+  if (half > 0 && (e = h2d(wrap, n)) != cudaSuccess) return cuda_fail(e, "h2d");
+  int64_t b_prev = 0, lo = 0;
+  for (int c = 1; c <= chunks; ++c) {
+    const int64_t hi = c == chunks ? n : (n * c) / chunks;
+    int64_t b1 = c == chunks ? nb : (hi + half - p->N >= 0 ? (hi + half - p->N) / keep + 1 : 0);
+    b1 = std::max(b_prev, std::min(b1, nb));
+    if (std::min(hi, wrap) > lo && (e = h2d(lo, std::min(hi, wrap))) != cudaSuccess)
+      return cuda_fail(e, "h2d");
+    cudaEvent_t ev_in = event(s_in);
+    if (b1 > b_prev) {
+      cudaStream_t sk = p->host_streams[1 + c];
+      cudaStreamWaitEvent(sk, ev_in, 0);
+      cbessfm_io dio{din, 2 * n, n, 0, dout, 2 * n, n, 0, n, batch, b_prev, b1};
+      const cbessfm_status r = cbessfm_run(p, &dio, sk);
+      if (r != CBESSFM_OK) return r;
+      cudaEvent_t ev_k = event(sk);
+      cudaStreamWaitEvent(s_out, ev_k, 0);
+      const int64_t o0 = b_prev * keep, o1 = std::min(b1 * keep, n);
+      if ((e = d2h(o0, o1)) != cudaSuccess) return cuda_fail(e, "d2h");
+    }
+    b_prev = b1;
+    lo = hi;
+  }
+  cudaEvent_t done = event(s_out);
+  cudaStreamWaitEvent(st, done, 0);
+  cudaFreeAsync(din, st);
+  cudaFreeAsync(dout, st);
+  for (cudaEvent_t ev : evs) cudaEventDestroy(ev);  // released once complete
+  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "cbessfm_run_host");
   return CBESSFM_OK;
 }
 

@@ -299,97 +299,30 @@ class DbpEngine:
         return self._dev_in, self._dev_out
 
     def run_host(self, x, out=None, stream=None, chunks: int = 8):
-        """Host [B, 2, n] in, host [B, 2, n] out (pinned for overlap).
-
-        Pipelined: the waveform is copied in ``chunks`` sample ranges on a
-        copy stream; as soon as the blocks whose windows lie inside the
-        copied prefix are runnable they launch on a compute stream (block
-        ranges of the same schedule), and their kept samples go back on a
-        third stream -- H2D, the kernel and D2H overlap. The wrap-around
-        blocks (window crossing sample 0 or n) run last. Returns ``out``
-        with all work enqueued behind ``stream``."""
+        """Host [B, 2, n] in, host [B, 2, n] out, through the C ABI's
+        host-buffer entry (cbessfm_run_host): the waveform is copied in
+        ``chunks`` sample ranges, each block range launches as soon as its
+        input windows have landed and finished kept samples go back while
+        later chunks compute (H2D / kernel / D2H overlap). Pinned tensors
+        are needed for the overlap. Returns ``out`` with the work enqueued
+        behind ``stream``."""
         torch = _torch()
         if x.dtype != self.torch_dtype:
             raise ValueError(f"host input must be {self.torch_dtype}")
         if x.dim() == 2:
             x = x.unsqueeze(0)
+        if x.is_cuda or not x.is_contiguous():
+            raise ValueError("run_host takes a contiguous host tensor")
         n = x.shape[-1]
         if self.cfg.block_size > n:
             raise ValueError("block_size exceeds the sequence length")
-        din, dout = self._buffers(x.shape)
         if out is None:
             out = torch.empty(x.shape, dtype=x.dtype, pin_memory=x.is_pinned())
+        if out.shape != x.shape or not out.is_contiguous() or out.is_cuda:
+            raise ValueError("out must be a contiguous host tensor shaped like x")
         stream = stream or torch.cuda.current_stream(self.device)
-        if not hasattr(self, "_streams"):
-            self._streams = tuple(torch.cuda.Stream(self.device) for _ in range(3))
-        s_in, s_k, s_out = self._streams
-        sched = self.schedule(n)
-        keep, half, nb = sched.keep, sched.half, sched.n_blocks
-        N = self.cfg.block_size
-        # interior blocks: window [b*keep - half, b*keep - half + N) inside [0, n)
-        first = -(-half // keep)
-        last = (n + half - N) // keep          # inclusive
-        groups = []                            # (copy_end, b0, b1)
-        chunks = max(1, min(chunks, max(1, last - first + 1)))
-        prev_b = first
-        for c in range(1, chunks + 1):
-            end = n if c == chunks else (n * c) // chunks
-            b1 = min(last, (end + half - N) // keep) + 1
-            if b1 > prev_b:
-                groups.append((end, prev_b, b1))
-                prev_b = b1
-        start_ev = torch.cuda.Event()
-        start_ev.record(stream)
-        for s_ in (s_in, s_k, s_out):
-            s_.wait_event(start_ev)
-        rows = [(b, p) for b in range(x.shape[0]) for p in range(2)]
-
-        def h2d(a, b):                    # contiguous row pieces only
-            for r, p in rows:
-                din[r, p, a:b].copy_(x[r, p, a:b], non_blocking=True)
-
-        def d2h(a, b):
-            for r, p in rows:
-                out[r, p, a:b].copy_(dout[r, p, a:b], non_blocking=True)
-
-        copied = 0
-        for end, b0, b1 in groups:
-            with torch.cuda.stream(s_in):
-                if end > copied:
-                    h2d(copied, end)
-                    copied = end
-                ev_in = torch.cuda.Event()
-                ev_in.record(s_in)
-            s_k.wait_event(ev_in)
-            launch(self.plan, din, dout, block_range=(b0, b1), stream=s_k)
-            ev_k = torch.cuda.Event()
-            ev_k.record(s_k)
-            s_out.wait_event(ev_k)
-            o0, o1 = sched.output_range(b0, b1)
-            with torch.cuda.stream(s_out):
-                d2h(o0, o1)
-        with torch.cuda.stream(s_in):
-            if copied < n:
-                h2d(copied, n)
-            ev_in = torch.cuda.Event()
-            ev_in.record(s_in)
-        s_k.wait_event(ev_in)
-        # wrap-around blocks: [0, first) and (last, nb)
-        rest = [(0, min(first, nb))] + [(max(last + 1, first), nb)]
-        ev_k = torch.cuda.Event()
-        for b0, b1 in rest:
-            if b1 > b0:
-                launch(self.plan, din, dout, block_range=(b0, b1), stream=s_k)
-        ev_k.record(s_k)
-        s_out.wait_event(ev_k)
-        with torch.cuda.stream(s_out):
-            for b0, b1 in rest:
-                if b1 > b0:
-                    o0, o1 = sched.output_range(b0, b1)
-                    d2h(o0, o1)
-        done = torch.cuda.Event()
-        done.record(s_out)
-        stream.wait_event(done)
+        self.plan.run_host(in_ptr=x.data_ptr(), out_ptr=out.data_ptr(), n=n,
+                           batch=x.shape[0], chunks=chunks, stream=stream.cuda_stream)
         return out
 
 
