@@ -401,8 +401,9 @@ __device__ __forceinline__ void sincos_acc<double>(double a, double* s, double* 
 }
 
 // Rotate by exp(-i theta), theta = scale * th[p] (dbp.py:196, :208); th is
-// the float view of the packed irfft output. Both half-warps read the same
-// theta (broadcast) and rotate their own polarisation.
+// the float view of the packed irfft output. The two half-warps hold the
+// same positions (x and y): each evaluates sincos for half of them and the
+// halves are exchanged with shuffles, so every angle is evaluated once.
 template <typename R>
 struct RotationHook : NoHook {
   const R* th;
@@ -410,11 +411,19 @@ struct RotationHook : NoHook {
   template <typename, int RAD, int LR>
   __device__ __forceinline__ void pre(int j, Cx<R>* v) {
     const R* base = th + fpos(j);
+    const int pol = (threadIdx.x >> 4) & 1;
+    static_assert(RAD % 2 == 0, "rotation split needs an even radix");
 #pragma unroll
-    for (int r = 0; r < RAD; ++r) {
+    for (int h = 0; h < RAD / 2; ++h) {
+      // this half-warp evaluates r = 2h + pol, the partner r = 2h + 1 - pol
+      const int ro = 2 * h + pol;
       R s, c;
-      sincos_acc<R>(base[2 * pad(r * LR / 2)] * scale, &s, &c);
-      v[r] = cmul(v[r], mk(c, -s));
+      sincos_acc<R>(base[2 * pad(ro * LR / 2)] * scale, &s, &c);
+      const R so = __shfl_xor_sync(0xffffffffu, s, 16);
+      const R co = __shfl_xor_sync(0xffffffffu, c, 16);
+      const Cx<R> mine = mk(c, -s), theirs = mk(co, -so);
+      v[2 * h] = cmul(v[2 * h], pol ? theirs : mine);
+      v[2 * h + 1] = cmul(v[2 * h + 1], pol ? mine : theirs);
     }
   }
 };
