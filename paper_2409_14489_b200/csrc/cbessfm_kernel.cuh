@@ -230,11 +230,14 @@ __device__ __forceinline__ void dft_reg(Cx<R>* v) {
 //            (radix 16, NS = 1) consumes and the two fuse (fft2_boundary)
 //   kHalf -- radix-4 passes for the half-length real-transform FFTs, which
 //            keeps all Q/8 threads busy on Q/2 points
+#ifndef CB_HALF_RAD
+#define CB_HALF_RAD 4
+#endif
 constexpr int kMaxRad = 16;
 constexpr int kTail = 0, kHead = 1, kHalf = 2;
 
 __host__ __device__ constexpr int sched_radix(int L, int ns, int sched) {
-  if (sched == kHalf) return L / ns >= 4 ? 4 : L / ns;
+  if (sched == kHalf) return L / ns >= CB_HALF_RAD ? CB_HALF_RAD : L / ns;
   if (sched == kHead && ns == 1) {
     int head = L;
     while (head > kMaxRad) head /= kMaxRad;
