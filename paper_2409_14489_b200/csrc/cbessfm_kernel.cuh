@@ -861,9 +861,12 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
     fft2<R, Q, NT, kTail, false>(F, twpT, &s_zero);
     // ---- 3. cross-subband radix-P stage over DSMEM: CTA c produces bins
     //         Q*k1 + k2 for k2 in its slice and every k1, and writes each to
-    //         the CTA that owns it in the fftshift'd subband layout. Results
-    //         are staged in the owner's idle IS/TS region (one polarisation
-    //         at a time), so no CTA overwrites fields another CTA still reads.
+    //         the CTA that owns it in the fftshift'd subband layout. Row 0's
+    //         results are staged in the owner's idle IS/RB region and row 1's
+    //         land in the owner's row 0 once every CTA has read it, so no CTA
+    //         overwrites fields another CTA still reads (3 cluster barriers).
+    //         The polarisation rows come out swapped; everything in the step
+    //         loop is symmetric in x and y, and step 5 swaps them back.
     cg::cluster_group cluster = cg::this_cluster();
     const int lo = (rank * Q) / P, hi = ((rank + 1) * Q) / P;
     const R invP = (R)1 / (R)P;
@@ -888,14 +891,17 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
           int i, m;
           bin_home<P, Q>(Q * k1 + k2, i, m);
           const Cx<R> w = ldg(ph0 + (size_t)i * Q + m);
-          Cx<R>* dst = cluster.map_shared_rank(S, i);
+          // row 0 results go to the staging area, row 1 results into the
+          // owner's row 0 (consumed by then): the rows come out swapped
+          Cx<R>* dst = cluster.map_shared_rank(pol ? F : S, i);
           dst[pad(m)] = cmul(scale(s, invP), w);
         }
       }
       cluster.sync();
-      for (int t = tid; t < Q; t += NT) F[pol * SF + pad(t)] = S[pad(t)];
-      cluster.sync();
     }
+    // every remote read of row 1 is done: move the staged row-0 results in
+    for (int t = tid; t < Q; t += NT) F[SF + pad(t)] = S[pad(t)];
+    __syncthreads();
   }
 
   CB_MARK(2);
@@ -1059,7 +1065,8 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
   // ---- 5. merge + outer IFFT (dbp.py:400-401): CTA c gathers, for k2 in
   //         its slice, the P bins Q*k1 + k2 from their owners, applies the
   //         inverse radix-P stage and the twiddle, and hands polyphase
-  //         component n1 to CTA n1 (staged as in step 3).
+  //         component n1 to CTA n1 (staged as in step 3, which swaps the
+  //         rows back).
   if constexpr (P > 1) {
     cg::cluster_group cluster = cg::this_cluster();
     const int lo = (rank * Q) / P, hi = ((rank + 1) * Q) / P;
@@ -1081,14 +1088,14 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
 #pragma unroll
           for (int k1 = 1; k1 < P; ++k1) s = s + cmulc(xv[k1], ldg(twN + ((n1 * k1) % P) * Q));
           if (n1) s = cmulc(s, ldg(twN + n1 * k2));
-          Cx<R>* dst = cluster.map_shared_rank(S, n1);
+          Cx<R>* dst = cluster.map_shared_rank(pol ? F : S, n1);
           dst[pad(k2)] = s;
         }
       }
       cluster.sync();
-      for (int t = tid; t < Q; t += NT) F[pol * SF + pad(t)] = S[pad(t)];
-      cluster.sync();
     }
+    for (int t = tid; t < Q; t += NT) F[SF + pad(t)] = S[pad(t)];
+    __syncthreads();
   }
   fft2<R, Q, NT, kTail, true>(F, twpT, &s_zero);
 
