@@ -138,6 +138,14 @@ cbessfm_status cbessfm_run(const cbessfm_plan* plan, const cbessfm_io* io, void*
  * returns once enqueued (synchronise `stream` before reading `out`). */
 cbessfm_status cbessfm_run_host(const cbessfm_plan* plan, const cbessfm_host_io* io, void* stream);
 
+/* The public nlpr_step helper (dbp.py:211-230) on the GPU: coupled-band
+ * nonlinear phase rotation of P time-domain subband waveforms of n_prime
+ * samples. in/out: DEVICE [2][P][n_prime] of `dtype`; mimo: HOST
+ * [P][P][n_prime/2+1] complex128 (a MimoTransfer matrix, any structure);
+ * theta_scale = step_power_scale / reference_power_w. Synchronous. */
+cbessfm_status cbessfm_nlpr(int32_t dtype, int32_t n_subbands, int32_t n_prime, const void* in,
+                            void* out, const double* mimo, double theta_scale, void* stream);
+
 /* Free the plan's device tables. */
 cbessfm_status cbessfm_plan_destroy(cbessfm_plan* plan);
 

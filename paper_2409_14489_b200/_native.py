@@ -63,6 +63,8 @@ SIGNATURES = {
     "cbessfm_plan_info_get": (C.c_int, [C.c_void_p, C.POINTER(PlanInfo)]),
     "cbessfm_run": (C.c_int, [C.c_void_p, C.POINTER(Io), C.c_void_p]),
     "cbessfm_run_host": (C.c_int, [C.c_void_p, C.POINTER(HostIo), C.c_void_p]),
+    "cbessfm_nlpr": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                               C.POINTER(C.c_double), C.c_double, C.c_void_p]),
     "cbessfm_plan_destroy": (C.c_int, [C.c_void_p]),
     "cbessfm_last_error": (C.c_char_p, []),
     "cbessfm_debug_phase_times": (C.c_int32, [C.c_void_p, C.POINTER(C.c_int64), C.c_int32]),
@@ -166,6 +168,18 @@ class NativePlan:
             except Exception:
                 pass
             self.handle = None
+
+
+def nlpr(dtype: int, n_subbands: int, n_prime: int, in_ptr: int, out_ptr: int,
+         mimo: np.ndarray, theta_scale: float, stream: int) -> None:
+    m = np.ascontiguousarray(mimo, dtype=np.complex128)
+    st = load().cbessfm_nlpr(dtype, n_subbands, n_prime, C.c_void_p(in_ptr),
+                             C.c_void_p(out_ptr), _dptr(m.view(np.float64)), theta_scale,
+                             C.c_void_p(stream))
+    if st != CBESSFM_OK:
+        text = f"cbessfm_nlpr: status {st} (n_prime must be a power of two in [256, 4096])"
+        raise ValueError(text) if st in (CBESSFM_ERR_INVALID, CBESSFM_ERR_UNSUPPORTED) \
+            else RuntimeError(text)
 
 
 def fma_peak(kind: int, ms: float = 200.0) -> float:

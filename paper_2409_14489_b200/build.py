@@ -76,6 +76,8 @@ def build(jobs: int | None = None, verbose: bool = False, profile: bool = False)
                   BUILD / "api.log"))
     tasks.append((CSRC / "cbessfm_peaks.cu", BUILD / "peaks.o", [], HEADERS,
                   BUILD / "peaks.log"))
+    tasks.append((CSRC / "cbessfm_nlpr.cu", BUILD / "nlpr.o", [], HEADERS,
+                  BUILD / "nlpr.log"))
     with ThreadPoolExecutor(jobs) as ex:
         results = list(ex.map(_compile, tasks))
     errors = [e for _, e in results if e]

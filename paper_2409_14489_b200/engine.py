@@ -327,25 +327,20 @@ class DbpEngine:
 
 
 def nlpr_step(subbands, mimo: MimoTransfer, step_power_scale: float,
-              reference_power_w: float, counter=None):
-    """Nonlinear phase rotation across subband waveforms (dbp.py:211-230).
-
-    A host-side helper of the public API (the reference's tests call it on
-    256-sample lists); the hot path runs the same rotation inside the fused
-    kernel. Numpy FP64, identical formula (dbp.py:185-208)."""
+              reference_power_w: float, counter=None, *, dtype: str = "c128"):
+    """Nonlinear phase rotation across subband waveforms (dbp.py:211-230),
+    on the GPU (cbessfm_nlpr, csrc/cbessfm_nlpr.cu): a cluster of one CTA
+    per subband computes theta_i = irfft(sum_l T[i,l] rfft(I_l)) * scale and
+    rotates both polarisations (dbp.py:185-208). Accepts any MimoTransfer
+    matrix; n_prime must be a power of two in [256, 4096]."""
+    torch = _torch()
     n_prime = subbands[0].num_samples
     if any(s.num_samples != n_prime for s in subbands):
         raise ValueError("subbands must share their length")
     if len(subbands) != mimo.matrix.shape[0] or n_prime != mimo.block_len:
         raise ValueError("transfer matrix does not match the subband set")
-    fields = np.stack([[s.x for s in subbands], [s.y for s in subbands]])
-    scale = step_power_scale / reference_power_w
-    power = np.abs(fields[0]) ** 2 + np.abs(fields[1]) ** 2
-    theta = np.fft.irfft(np.einsum("ilk,lk->ik", mimo.matrix,
-                                   np.fft.rfft(power, axis=-1)),
-                         n=n_prime, axis=-1) * scale
+    n_sb = len(subbands)
     if counter is not None:
-        n_sb = len(subbands)
         total = n_sb * n_prime
         counter.rmul(4 * total, "intensity")
         counter.radd(3 * total, "intensity")
@@ -355,7 +350,16 @@ def nlpr_step(subbands, mimo: MimoTransfer, step_power_scale: float,
         counter.cadd(n_sb * (n_sb - 1) * n_prime / 2, "mimo")
         counter.lut_exp(total)
         counter.pair_shared_cmul(total, "rotation")
-    fields = fields * np.exp(-1j * theta)[None]
+    fields = np.stack([[s.x for s in subbands], [s.y for s in subbands]])
+    cdt = torch.complex64 if _DTYPES[dtype] == _native.C64 else torch.complex128
+    dev = torch.device("cuda", torch.cuda.current_device())
+    x = torch.from_numpy(np.ascontiguousarray(fields)).to(dev).to(cdt).contiguous()
+    out = torch.empty_like(x)
+    stream = torch.cuda.current_stream(dev)
+    _native.nlpr(_DTYPES[dtype], n_sb, n_prime, x.data_ptr(), out.data_ptr(),
+                 np.asarray(mimo.matrix), step_power_scale / reference_power_w,
+                 stream.cuda_stream)
+    res = out.to(torch.complex128).cpu().numpy()
     cls = type(subbands[0])
-    return [cls(fields[0, i], fields[1, i], s.sample_rate, s.center_freq)
+    return [cls(res[0, i], res[1, i], s.sample_rate, s.center_freq)
             for i, s in enumerate(subbands)]

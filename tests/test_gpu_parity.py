@@ -192,3 +192,52 @@ def test_run_host_pipeline_matches_device_path(cuda, chunks):
         out = eng.run_host(x, chunks=chunks)
         torch.cuda.synchronize()
         assert rel_rms(out[0].numpy(), g.out) < 1e-12, (name, chunks)
+
+
+@pytest.mark.parametrize("dtype,tol", [("c128", 1e-13), ("c64", 1e-5)])
+def test_nlpr_step_on_gpu_matches_reference_kat(cuda, dtype, tol):
+    # pkg/tests/test_dbp.py:143-169: nlpr_step vs the reference's own output
+    # (tests/golden/nlpr_kat.npz) and the direct circular lag-sum formula
+    from conftest import GOLDEN, load_coeffs
+    d = np.load(GOLDEN / "nlpr_kat.npz")
+    c = load_coeffs(d)
+    subs = [pb.DualPolWaveform(d["sx"][i], d["sy"][i], 32e9) for i in range(2)]
+    mimo = pb.build_mimo_transfer(c, 256)
+    got = pb.nlpr_step(subs, mimo, 1.0, 1e-3, dtype=dtype)
+    for i in range(2):
+        assert rel_rms(got[i].x, d["gx"][i]) < tol
+        assert rel_rms(got[i].y, d["gy"][i]) < tol
+    intens = [np.abs(d["sx"][i]) ** 2 + np.abs(d["sy"][i]) ** 2 for i in range(2)]
+    for i in range(2):
+        theta = np.zeros(256)
+        for ell in range(2):
+            taps = c.coeffs[abs(ell - i)]
+            w = (taps.size - 1) // 2
+            weight = 1.0 if ell == i else 1.5
+            sgn = 1 if ell >= i else -1
+            for m, cm in zip(range(-w, w + 1), taps):
+                theta += weight * cm * np.roll(intens[ell], sgn * m)
+        theta /= 1e-3
+        assert rel_rms(got[i].x, d["sx"][i] * np.exp(-1j * theta)) < max(tol, 1e-10)
+
+
+def test_nlpr_step_general_matrix(cuda):
+    # a MimoTransfer need not be Toeplitz: random Hermitian-consistent rows
+    rng = np.random.default_rng(3)
+    p, q = 3, 512
+    subs = [pb.DualPolWaveform(rng.normal(size=q) * 0.02 + 1j * rng.normal(size=q) * 0.02,
+                               rng.normal(size=q) * 0.02 + 0j, 1e9) for _ in range(p)]
+    taps = rng.normal(size=(p, p, 9)) * 1e-4
+    m = np.zeros((p, p, q // 2 + 1), complex)
+    for i in range(p):
+        for ell in range(p):
+            buf = np.zeros(q)
+            buf[(np.arange(9) - 4) % q] = taps[i, ell]
+            m[i, ell] = np.fft.rfft(buf)
+    mt = pb.MimoTransfer(m, q)
+    got = pb.nlpr_step(subs, mt, 0.7, 2e-3)
+    fields = np.stack([[s.x for s in subs], [s.y for s in subs]])
+    ref = orc.nonlinear_rotation(fields, m, 0.7 / 2e-3)
+    for i in range(p):
+        assert rel_rms(got[i].x, ref[0, i]) < 1e-13
+        assert rel_rms(got[i].y, ref[1, i]) < 1e-13
