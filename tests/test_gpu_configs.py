@@ -126,3 +126,52 @@ def test_config4_batch_subset(cuda):
             ref = orc.run_cb_blocks(x[w], g.cfg, rate, g.coeffs, b, b + 1)
             o0, o1 = sched.output_range(b, b + 1)
             assert rel_rms(out[w][:, o0:o1], ref[:, o0:o1]) < 1e-5
+
+
+def _random_coeffs(n_sb, n_steps, q_taps=7, seed=0):
+    """A valid CoefficientSet with random taps (c_0 even-symmetric), for
+    shape coverage where no reference-built set is needed."""
+    rng = np.random.default_rng(seed)
+    coeffs = {}
+    for h in range(n_sb):
+        c = rng.normal(size=2 * q_taps + 1) * 2e-2
+        if h == 0:
+            c = 0.5 * (c + c[::-1])
+        coeffs[h] = c
+    return pb.CoefficientSet(n_sb=n_sb, subband_rate=1.0, subband_spacing=1.0,
+                             reference_power_w=1e-3, phase_norm_rad=-1e-2,
+                             step_scales=rng.uniform(0.5, 1.0, n_steps),
+                             geometry_hash="synthetic", coeffs=coeffs)
+
+
+@pytest.mark.parametrize("n_sb,q,n_st,rho", [(2, 256, 2, 0.3), (4, 512, 3, 0.5),
+                                             (6, 1024, 2, 0.9), (7, 512, 4, 0.2),
+                                             (8, 256, 3, 0.5), (9, 256, 1, 1.0),
+                                             (1, 8192, 2, 0.5), (3, 4096, 2, 0.1)])
+def test_every_cluster_size_and_fft_size(cuda, n_sb, q, n_st, rho):
+    # every compiled (N_sb, N') family against the oracle, random taps
+    rate = 64e9
+    n = 3 * n_sb * q + 1000                      # partial last block, wrap-around
+    field = gaussian_wdm(n, rate, n_channels=1, spacing=0.0, baud=16e9,
+                         dbm_per_channel=3.0, seed=n_sb)
+    cfg = pb.DbpConfig(link=_link(4), variant="CB_ESSFM", n_steps=n_st, n_subbands=n_sb,
+                       splitting_ratio=rho, block_size=n_sb * q,
+                       overlap=2 * n_sb * (q // 8), oversampling=2.0)
+    c = _random_coeffs(n_sb, n_st, seed=q + n_sb)
+    ref = orc.run_cb_blocks(field, cfg, rate, c)
+    for dtype in ("c128", "c64"):
+        if dtype == "c128" and q > 4096:
+            continue
+        e = rel_rms(_gpu(field, cfg, c, rate, dtype)[0], ref)
+        assert e < TOL[dtype], (dtype, e)
+
+
+def test_single_block_covering_the_waveform(cuda):
+    # block_size == n, overlap 0: one circular block (dbp.py:456-477)
+    g = golden("cfg1_nsb3_st2")
+    n = g.wave.num_samples
+    cfg = replace(g.cfg, block_size=n - n % 3 if n % 3 else n, overlap=0)
+    cfg = replace(cfg, block_size=6144, n_subbands=3)
+    field = np.vstack([g.wave.x, g.wave.y])[:, :6144]
+    ref = orc.run_cb_blocks(field, cfg, g.wave.sample_rate, g.coeffs)
+    assert rel_rms(_gpu(field, cfg, g.coeffs, g.wave.sample_rate, "c128")[0], ref) < 1e-12
