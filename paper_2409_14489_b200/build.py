@@ -55,14 +55,19 @@ def _compile(args):
     return obj, None
 
 
-def build(jobs: int | None = None, verbose: bool = False, profile: bool = False) -> Path:
+def build(jobs: int | None = None, verbose: bool = False, profile: bool = False,
+          variant: str | None = None, defines=()) -> Path:
     """Compile (incrementally) and link libcbessfm.so; returns its path.
-    profile=True builds the phase-clock debug variant libcbessfm_prof.so."""
+    profile=True builds the phase-clock debug variant libcbessfm_prof.so;
+    variant="x" with defines=("FOO",) builds an experiment variant
+    libcbessfm_x.so (load it with CBESSFM_LIB)."""
     global BUILD, LIB
     if profile:
-        BUILD = BUILD.parent / "cbessfm_prof"
-        LIB = PKG / "libcbessfm_prof.so"
-        FLAGS.append("-DCB_PHASE_PROFILE")
+        variant, defines = "prof", (*defines, "CB_PHASE_PROFILE")
+    if variant:
+        BUILD = BUILD.parent / f"cbessfm_{variant}"
+        LIB = PKG / f"libcbessfm_{variant}.so"
+        FLAGS.extend(f"-D{d}" for d in defines)
     BUILD.mkdir(parents=True, exist_ok=True)
     jobs = jobs or max(1, min(len(REALS) * len(SUBBANDS) + 1, os.cpu_count() or 1))
     tasks = []
@@ -96,5 +101,8 @@ def build(jobs: int | None = None, verbose: bool = False, profile: bool = False)
 
 
 if __name__ == "__main__":
-    build(verbose=True, profile="--profile" in sys.argv)
+    argv = sys.argv[1:]
+    var = argv[argv.index("--variant") + 1] if "--variant" in argv else None
+    defs = [argv[i + 1] for i, a in enumerate(argv) if a == "--define"]
+    build(verbose=True, profile="--profile" in argv, variant=var, defines=defs)
     sys.exit(0)

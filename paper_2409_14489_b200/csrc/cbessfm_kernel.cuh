@@ -316,13 +316,20 @@ __device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+// The suspend-time hint parks the waiting warps until the phase completes
+// instead of spinning (a spin loop costs issue slots the other CTAs on the
+// SM need); the hint is an upper bound, completion wakes them.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
+#ifdef CB_MBAR_SPIN  // experiment knob: plain try_wait spin
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+#else
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+#endif
       "@!P1 bra WAIT_%=;\n\t}"
-      ::"r"(smem_addr(bar)), "r"(parity)
+      ::"r"(smem_addr(bar)), "r"(parity), "r"(0x989680u)
       : "memory");
 }
 // 8- or 16-byte store into another CTA's shared memory that completes
@@ -404,9 +411,33 @@ struct IntensityHook : NoHook {
 
 template <typename R>
 __device__ __forceinline__ void sincos_acc(R a, R* s, R* c);
+// FP32: three-term Cody-Waite reduction to [-pi/4, pi/4] and the Cephes
+// minimax polynomials (about 1 ulp), roughly half the instructions of
+// sincosf; arguments beyond 2^13 (never reached by a nonlinear phase per
+// step, but legal) take the libdevice path.
 template <>
 __device__ __forceinline__ void sincos_acc<float>(float a, float* s, float* c) {
-  sincosf(a, s, c);
+  if (fabsf(a) > 8192.0f) {
+    sincosf(a, s, c);
+    return;
+  }
+  const float j = rintf(a * 0.636619772367581343f);
+  float r = __fmaf_rn(j, -0x1.921fb6p+0f, a);
+  r = __fmaf_rn(j, 0x1.777a5cp-25f, r);
+  r = __fmaf_rn(j, 0x1.ee59dap-50f, r);
+  const float r2 = r * r;
+  float ps = __fmaf_rn(r2, -1.9515295891e-4f, 8.3321608736e-3f);
+  ps = __fmaf_rn(r2, ps, -1.6666654611e-1f);
+  const float sn = __fmaf_rn(r * r2, ps, r);
+  float pc = __fmaf_rn(r2, 2.443315711809948e-5f, -1.388731625493765e-3f);
+  pc = __fmaf_rn(r2, pc, 4.166664568298827e-2f);
+  pc = __fmaf_rn(r2, pc, -0.5f);
+  const float cs = __fmaf_rn(r2, pc, 1.0f);
+  const int q = __float2int_rn(j);
+  const float ss = (q & 1) ? cs : sn;
+  const float cc = (q & 1) ? sn : cs;
+  *s = (q & 2) ? -ss : ss;
+  *c = ((q + 1) & 2) ? -cc : cc;
 }
 template <>
 __device__ __forceinline__ void sincos_acc<double>(double a, double* s, double* c) {
