@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define CBESSFM_VERSION 1
+#define CBESSFM_VERSION 2
 
 typedef enum {
   CBESSFM_OK = 0,
@@ -61,13 +61,20 @@ typedef struct {
   /* [n_steps + 1]: table applied before step s (s < n_steps) and the
    * final one (s == n_steps), i.e. gvd_lengths + [final_gvd]            */
   const int32_t* phasor_index;
-  /* [P][Q/2 + 1] complex128 spectra S_h = rfft(centred taps c_h),
+  /* [n_sets][P][Q/2 + 1] complex128 spectra S_h = rfft(centred taps c_h),
    * S_h for h >= 1 pre-multiplied by the 3/2 XPM weight (dbp.py:152-182);
    * may be NULL when n_steps == 0                                       */
   const double* mimo;
-  /* [n_steps]: step_scales / reference_power_w / Q (dbp.py:386, :196)    */
+  /* [n_sets][n_steps]: step_scales / reference_power_w / Q (dbp.py:386,
+   * :196)                                                                */
   const double* theta_scale;
   int32_t device;       /* CUDA device ordinal the plan lives on          */
+  /* Coefficient sets (CoefficientSet, kernel.py:390-453) sharing this
+   * geometry; waveform w of a launch uses set w % n_sets. 0 or 1: one set.
+   * Several sets evaluate candidate coefficients on one waveform in one
+   * launch (in_batch_stride 0), as optimize_coefficients' finite
+   * differences do one run_dbp call at a time (optimize.py:129-167).     */
+  int32_t n_sets;
 } cbessfm_desc;
 
 /* One launch over a block range of a batch of waveforms. Buffers are

@@ -31,7 +31,7 @@ class Desc(C.Structure):
                 ("phasor_index", C.POINTER(C.c_int32)),
                 ("mimo", C.POINTER(C.c_double)),
                 ("theta_scale", C.POINTER(C.c_double)),
-                ("device", C.c_int32)]
+                ("device", C.c_int32), ("n_sets", C.c_int32)]
 
 
 class Io(C.Structure):
@@ -76,6 +76,9 @@ _lib = None
 _lock = threading.Lock()
 
 
+ABI_VERSION = 2   # CBESSFM_VERSION in include/cbessfm.h
+
+
 def load() -> C.CDLL:
     """Load (once) and return the library; raises if it is not built."""
     global _lib
@@ -92,6 +95,10 @@ def load() -> C.CDLL:
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args
+            if lib.cbessfm_version() != ABI_VERSION:
+                raise RuntimeError(
+                    f"{path} has ABI {lib.cbessfm_version()}, this package binds "
+                    f"{ABI_VERSION} (include/cbessfm.h); rebuild the extension")
             _lib = lib
     return _lib
 
@@ -116,7 +123,9 @@ class NativePlan:
     def __init__(self, *, dtype: int, n_subbands: int, block_size: int,
                  overlap: int, n_steps: int, phasors: np.ndarray,
                  phasor_index: np.ndarray, mimo: np.ndarray | None,
-                 theta_scale: np.ndarray, device: int):
+                 theta_scale: np.ndarray, device: int, n_sets: int = 1):
+        """mimo [n_sets][P][Q/2+1] (or [P][Q/2+1]) and theta_scale
+        [n_sets][n_steps] (or [n_steps]); waveform w uses set w % n_sets."""
         lib = load()
         self._lib = lib
         ph = np.ascontiguousarray(phasors, dtype=np.complex128)
@@ -127,7 +136,7 @@ class NativePlan:
                  ph.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)),
                  idx.ctypes.data_as(C.POINTER(C.c_int32)),
                  None if mi is None else _dptr(mi.view(np.float64)),
-                 _dptr(th) if th.size else None, device)
+                 _dptr(th) if th.size else None, device, n_sets)
         handle = C.c_void_p()
         check(lib.cbessfm_plan_create(C.byref(d), C.byref(handle)),
               "cbessfm_plan_create")

@@ -81,11 +81,11 @@ std::vector<double> pass_tables(int Q, const std::vector<double>& tq, int real_b
 }  // namespace
 
 struct cbessfm_plan {
-  int dtype, P, Q, N, overlap, n_steps, n_phasors, device;
+  int dtype, P, Q, N, overlap, n_steps, n_phasors, n_sets, device;
   void* phasor = nullptr;  // [n_phasors][P][Q]
   int* ph_index = nullptr; // [n_steps + 1]
   void* mimo = nullptr;    // [P][Q/2+1]
-  void* theta = nullptr;   // [n_steps]
+  void* theta = nullptr;   // [n_sets][n_steps]
   void* twQ = nullptr;     // [Q]
   void* twN = nullptr;     // [P*Q]
   void* twp = nullptr;     // per-pass twiddle rows
@@ -127,7 +127,8 @@ void round_unit(double re, double im, float* ore, float* oim) {
       if (b < 0) ci = std::nextafter(fi, -INFINITY);
       if (b > 0) ci = std::nextafter(fi, INFINITY);
       const double m2 = (double)cr * cr + (double)ci * ci;
-      const double ang = std::fabs(std::atan2((double)ci, (double)cr) - std::atan2(ui, ur));
+      // phase error as the cross product (sin of the angle, ~1e-7 here)
+      const double ang = std::fabs((double)ci * ur - (double)cr * ui) / target;
       const double score = std::fabs(m2 - t2) + 1e-3 * ang;
       if (score < best) {
         best = score;
@@ -185,12 +186,13 @@ cbessfm_status upload_all(cbessfm_plan* p, const cbessfm_desc* d) {
   std::vector<double> zeros;
   const double* mimo = d->mimo;
   if (!mimo) {
-    zeros.assign(2 * p->P * H1, 0.0);
+    zeros.assign(2 * (size_t)p->n_sets * p->P * H1, 0.0);
     mimo = zeros.data();
   }
-  if ((e = upload_complex<R>(mimo, (size_t)p->P * H1, &p->mimo)) != cudaSuccess)
+  if ((e = upload_complex<R>(mimo, (size_t)p->n_sets * p->P * H1, &p->mimo)) != cudaSuccess)
     return cuda_fail(e, "upload MIMO spectra");
-  if ((e = upload_real<R>(d->theta_scale, (size_t)p->n_steps, &p->theta)) != cudaSuccess)
+  if ((e = upload_real<R>(d->theta_scale, (size_t)p->n_sets * p->n_steps, &p->theta)) !=
+      cudaSuccess)
     return cuda_fail(e, "upload theta scales");
   const std::vector<double> tq = twiddles(p->Q), tn = twiddles((int64_t)p->P * p->Q);
   if ((e = upload_complex<R>(tq.data(), (size_t)p->Q, &p->twQ, true)) != cudaSuccess)
@@ -274,6 +276,7 @@ cbessfm::Params<R> make_params(const cbessfm_plan* p, const cbessfm_io* io) {
   prm.twN = reinterpret_cast<const C*>(p->twN);
   prm.twp = reinterpret_cast<const C*>(p->twp);
   prm.n_steps = p->n_steps;
+  prm.n_sets = p->n_sets;
   prm.cid0 = 0;
   prm.dbg = p->dbg;
   return prm;
@@ -312,6 +315,7 @@ cbessfm_status cbessfm_plan_create(const cbessfm_desc* d, cbessfm_plan** out) {
   if (d->overlap % (2 * d->n_subbands))
     return fail(CBESSFM_ERR_INVALID, "overlap must be a multiple of 2*n_subbands");
   if (d->n_steps < 0) return fail(CBESSFM_ERR_INVALID, "n_steps must be >= 0");
+  if (d->n_sets < 0) return fail(CBESSFM_ERR_INVALID, "n_sets must be >= 0");
   if (d->n_phasors < 1 || !d->phasors || !d->phasor_index)
     return fail(CBESSFM_ERR_INVALID, "phasor tables missing");
   if (d->n_steps > 0 && !d->theta_scale)
@@ -336,6 +340,7 @@ cbessfm_status cbessfm_plan_create(const cbessfm_desc* d, cbessfm_plan** out) {
   p->overlap = d->overlap;
   p->n_steps = d->n_steps;
   p->n_phasors = d->n_phasors;
+  p->n_sets = d->n_sets > 1 ? d->n_sets : 1;
   p->device = d->device;
   cudaError_t e = cudaSetDevice(d->device);
   if (e != cudaSuccess) {

@@ -760,8 +760,9 @@ struct Params {
   int64_t half;     // overlap / 2
   const Cx<R>* phasor;     // [n_tab][P][Q], carries 1/Q
   const int* ph_index;     // [n_steps + 1]
-  const Cx<R>* mimo;       // [P][Q/2+1], S_h with the 3/2 XPM weight folded
-  const R* theta_scale;    // [n_steps], carries 1/Q
+  const Cx<R>* mimo;       // [n_sets][P][Q/2+1], S_h with the 3/2 XPM weight folded
+  const R* theta_scale;    // [n_sets][n_steps], carries 1/Q
+  int n_sets;              // coefficient sets; waveform w uses set w % n_sets
   const Cx<R>* twQ;        // [Q]   exp(-2 pi i m / Q)
   const Cx<R>* twN;        // [P*Q] exp(-2 pi i m / (P Q))
   const Cx<R>* twp;        // per-pass rows, layout twp_base()
@@ -770,8 +771,8 @@ struct Params {
   long long* dbg;          // phase clocks of CTA 0 (CB_PHASE_PROFILE builds only)
 };
 
-// One radix-8 butterfly of each polarisation per thread on the length-Q
-// field FFTs.
+// Q/8 threads: on the length-Q field FFTs each half-warp takes one
+// polarisation and each thread one radix-16 butterfly per pass.
 template <typename R, int Q>
 __host__ __device__ constexpr int threads_for() {
   return Q / 8;
@@ -853,6 +854,9 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
   const int64_t wv = cid / prm.nb;
   const int64_t b = prm.b0 + cid % prm.nb;
   const int64_t n = prm.n;
+  const int64_t cset = prm.n_sets > 1 ? wv % prm.n_sets : 0;
+  const Cx<R>* __restrict__ mimo = prm.mimo + cset * (int64_t)P * (H + 1);
+  const R* __restrict__ theta_scale = prm.theta_scale + cset * prm.n_steps;
 
   const Cx<R>* __restrict__ twQ = prm.twQ;
   const Cx<R>* __restrict__ twN = prm.twN;
@@ -1013,7 +1017,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
       for (int k = lo + tid; k < hi; k += NT) {
         Cx<R> sv[P];
 #pragma unroll
-        for (int l = 0; l < P; ++l) sv[l] = ldg(prm.mimo + (size_t)l * (H + 1) + k);
+        for (int l = 0; l < P; ++l) sv[l] = ldg(mimo + (size_t)l * (H + 1) + k);
         mbar_wait(&s_bar[0], st & 1);
         Cx<R> iv[P];
 #pragma unroll
@@ -1033,7 +1037,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
       mbar_wait(&s_bar[1], st & 1);
     } else {
       __syncthreads();
-      for (int k = tid; k <= H; k += NT) TS[pad(k)] = cmul(ldg(prm.mimo + k), IS[pad(k)]);
+      for (int k = tid; k <= H; k += NT) TS[pad(k)] = cmul(ldg(mimo + k), IS[pad(k)]);
       __syncthreads();
     }
 
@@ -1075,7 +1079,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
     // applies the final phasor (dbp.py:399)
     RotationHook<R> rot;
     rot.th = Treal;
-    rot.scale = prm.theta_scale[st];
+    rot.scale = theta_scale[st];
     const Cx<R>* ph_next = ph_rank + (size_t)prm.ph_index[st + 1] * ph_tab;
     if (st + 1 < prm.n_steps) {
       fft2<R, Q, NT, kHead, false, RotationHook<R>, NoHook, 1, Q / sched_radix(Q, 1, kTail)>(

@@ -256,6 +256,77 @@ def run_dbp(w, cfg, coeffs=None, counter=None, *, dtype: str = "c128",
     return type(w)(res[0], res[1], w.sample_rate, w.center_freq)
 
 
+def _sets_plan(cfg, rate: float, coeff_sets, dtype: str, device: int):
+    """One plan holding every coefficient set (cbessfm_desc.n_sets): the
+    dispersion tables depend on the config only, the MIMO spectra and theta
+    scales on the set (dbp.py:318-369)."""
+    if cfg.variant != "CB_ESSFM" or not cfg.n_steps:
+        raise ValueError("coefficient sets need the CB_ESSFM variant with n_steps >= 1")
+    if not coeff_sets:
+        raise ValueError("at least one coefficient set is required")
+    n_sb = _variant_geometry(cfg, coeff_sets[0])
+    tabs = [build_tables(cfg, rate, c, n_sb) for c in coeff_sets]
+    t0 = tabs[0]
+    for t in tabs[1:]:
+        if t.phasors.shape != t0.phasors.shape or not np.array_equal(t.phasors, t0.phasors):
+            raise ValueError("coefficient sets imply different dispersion geometries")
+    if not _native.supported(_DTYPES[dtype], n_sb, cfg.block_size):
+        raise ValueError(f"no sm_100a kernel for n_subbands={n_sb}, N'={cfg.block_size // n_sb}")
+    torch = _torch()
+    with torch.cuda.device(device):
+        return _native.NativePlan(
+            dtype=_DTYPES[dtype], n_subbands=n_sb, block_size=cfg.block_size,
+            overlap=cfg.overlap, n_steps=cfg.n_steps, phasors=t0.phasors,
+            phasor_index=t0.phasor_index, mimo=np.stack([t.mimo for t in tabs]),
+            theta_scale=np.stack([t.theta_scale for t in tabs]), device=int(device),
+            n_sets=len(tabs))
+
+
+def run_dbp_sets_tensor(x, cfg, coeff_sets, sample_rate: float, out=None, stream=None):
+    """Evaluate S coefficient sets on one device-resident waveform in one
+    launch: x [2, n] (or [1, 2, n]) complex CUDA tensor, returns [S, 2, n].
+    The batch axis carries the sets (input batch stride 0); the per-set
+    outputs equal S run_dbp calls (the finite-difference
+    evaluations of optimize_coefficients, optimize.py:129-167)."""
+    torch = _torch()
+    validate_config(cfg)
+    if x.dim() == 3:
+        if x.shape[0] != 1:
+            raise ValueError("one waveform per coefficient-set evaluation")
+        x = x[0]
+    dtype = "c64" if x.dtype == torch.complex64 else "c128"
+    n = x.shape[-1]
+    if cfg.block_size > n:
+        raise ValueError("block_size exceeds the sequence length")
+    plan = _sets_plan(cfg, sample_rate, list(coeff_sets), dtype, x.device.index)
+    s = len(coeff_sets)
+    if out is None:
+        out = torch.empty((s, 2, n), dtype=x.dtype, device=x.device)
+    launch(plan, x.unsqueeze(0).expand(s, 2, n), out, stream=stream)
+    return out
+
+
+def run_dbp_sets(w, cfg, coeff_sets, counter=None, *, dtype: str = "c128",
+                 device: int | None = None) -> list:
+    """run_dbp(w, cfg, c) for every c in coeff_sets, as one launch; returns
+    the list of output waveforms (same values as the separate calls)."""
+    torch = _torch()
+    w.require_finite()
+    coeff_sets = list(coeff_sets)
+    if device is None:
+        device = torch.cuda.current_device()
+    cdt = torch.complex64 if _DTYPES.get(dtype) == _native.C64 else torch.complex128
+    x = torch.from_numpy(np.stack([np.asarray(w.x), np.asarray(w.y)])).to(
+        torch.device("cuda", device)).to(cdt)
+    with torch.cuda.device(device):
+        out = run_dbp_sets_tensor(x, cfg, coeff_sets, w.sample_rate)
+        res = out.to(torch.complex128).cpu().numpy()
+    n_blocks = BlockSchedule(w.num_samples, cfg.block_size, cfg.overlap).n_blocks
+    for _ in coeff_sets:
+        record_cb_blocks(counter, cfg.block_size, cfg.n_steps, cfg.n_subbands, n_blocks)
+    return [type(w)(r[0], r[1], w.sample_rate, w.center_freq) for r in res]
+
+
 class DbpEngine:
     """A reusable CB-ESSFM engine for one (config, coefficients, rate, dtype)
     on one device: the plan is uploaded once, device buffers are kept, and

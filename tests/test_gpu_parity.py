@@ -7,6 +7,7 @@ post-DBP SNR within 0.01 dB. Fixed cases come from the real reference
 """
 
 import warnings
+from dataclasses import replace
 
 import numpy as np
 import pytest
@@ -241,3 +242,27 @@ def test_nlpr_step_general_matrix(cuda):
     for i in range(p):
         assert rel_rms(got[i].x, ref[0, i]) < 1e-13
         assert rel_rms(got[i].y, ref[1, i]) < 1e-13
+
+
+def test_coefficient_sets_in_one_launch(cuda):
+    # S perturbed coefficient sets on one waveform (optimize.py:129-167's
+    # finite differences) == S separate oracle runs
+    g = golden("cfg1_nsb3_st2")
+    rng = np.random.default_rng(3)
+    sets = [g.coeffs]
+    for s in range(4):
+        taps = {h: c * (1 + 1e-2 * rng.normal(size=c.size)) for h, c in g.coeffs.coeffs.items()}
+        taps[0] = 0.5 * (taps[0] + taps[0][::-1])
+        sets.append(replace(g.coeffs, coeffs=taps,
+                            step_scales=g.coeffs.step_scales * (1 + 0.1 * s)))
+    field = np.vstack([g.wave.x, g.wave.y])
+    for dtype, tol in (("c128", 1e-12), ("c64", 1e-5)):
+        outs = pb.run_dbp_sets(g.wave, g.cfg, sets, dtype=dtype)
+        assert len(outs) == len(sets)
+        for c, o in zip(sets, outs):
+            ref = orc.run_cb_blocks(field, g.cfg, g.wave.sample_rate, c)
+            assert rel_rms(np.vstack([o.x, o.y]), ref) < tol
+    # the sets really differ
+    assert rel_rms(np.vstack([outs[1].x, outs[1].y]), np.vstack([outs[0].x, outs[0].y])) > 1e-4
+    with pytest.raises(ValueError):
+        pb.run_dbp_sets(g.wave, replace(g.cfg, n_steps=0), sets)

@@ -186,7 +186,7 @@ def test_native_library_exports_every_header_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert declared == set(_native.SIGNATURES)
-    assert lib.cbessfm_version() == 1
+    assert lib.cbessfm_version() == _native.ABI_VERSION
     assert lib.cbessfm_supported(0, 5, 10240) == 1
     assert lib.cbessfm_supported(1, 5, 10240 * 4) == 0
     assert lib.cbessfm_supported(0, 3, 3000) == 0
@@ -231,3 +231,12 @@ def test_fft1_ns4_butterfly_permutation_is_conflict_free():
         assert sorted(perm(t) for t in range(NT)) == list(range(NT))
         assert ways(lambda t: t) == 4
         assert ways(perm) == 1
+
+
+def test_header_abi_version_matches_binding():
+    import re
+    from paper_2409_14489_b200 import _native
+    hdr = (ROOT / "include" / "cbessfm.h").read_text()
+    assert int(re.search(r"#define CBESSFM_VERSION (\d+)", hdr).group(1)) == _native.ABI_VERSION
+    # the desc struct the binding mirrors ends with n_sets (ABI 2)
+    assert [f for f, _ in _native.Desc._fields_][-1] == "n_sets"
