@@ -54,7 +54,21 @@ class PlanInfo(C.Structure):
                 ("max_active_clusters", C.c_int32), ("q", C.c_int32)]
 
 
-# every symbol include/cbessfm.h declares: name -> (restype, argtypes)
+class SsfmDesc(C.Structure):
+    _fields_ = [("dtype", C.c_int32), ("n", C.c_int64), ("batch", C.c_int32),
+                ("n_spans", C.c_int32), ("steps_per_span", C.c_int32),
+                ("n_tables", C.c_int32), ("half", C.POINTER(C.c_double)),
+                ("step_table", C.POINTER(C.c_int32)), ("nl_coef", C.POINTER(C.c_double)),
+                ("backward", C.c_int32), ("gain", C.c_double), ("device", C.c_int32)]
+
+
+class SsfmInfo(C.Structure):
+    _fields_ = [("n1", C.c_int32), ("n2", C.c_int32), ("rows_per_tile", C.c_int32),
+                ("cols_per_tile", C.c_int32), ("grid", C.c_int32), ("threads", C.c_int32),
+                ("smem_bytes", C.c_int64)]
+
+
+# every symbol include/*.h declares: name -> (restype, argtypes)
 SIGNATURES = {
     "cbessfm_version": (C.c_int32, []),
     "cbessfm_num_blocks": (C.c_int64, [C.c_int64, C.c_int32, C.c_int32]),
@@ -70,6 +84,11 @@ SIGNATURES = {
     "cbessfm_debug_phase_times": (C.c_int32, [C.c_void_p, C.POINTER(C.c_int64), C.c_int32]),
     # include/cbessfm_peaks.h
     "cbessfm_fma_peak": (C.c_double, [C.c_int32, C.c_double]),
+    # include/cbessfm_ssfm.h
+    "cbessfm_ssfm_run": (C.c_int, [C.POINTER(SsfmDesc), C.c_void_p, C.c_void_p, C.c_void_p]),
+    "cbessfm_ssfm_info_get": (C.c_int, [C.c_int32, C.c_int64, C.c_int32, C.c_int32,
+                                        C.POINTER(SsfmInfo)]),
+    "cbessfm_ssfm_last_error": (C.c_char_p, []),
 }
 
 _lib = None
@@ -103,10 +122,10 @@ def load() -> C.CDLL:
     return _lib
 
 
-def check(status: int, what: str) -> None:
+def check(status: int, what: str, err=None) -> None:
     if status == CBESSFM_OK:
         return
-    msg = load().cbessfm_last_error().decode(errors="replace")
+    msg = (err or load().cbessfm_last_error)().decode(errors="replace")
     text = f"{what}: {msg}"
     if status in (CBESSFM_ERR_INVALID, CBESSFM_ERR_UNSUPPORTED):
         raise ValueError(text)
@@ -202,3 +221,29 @@ def num_blocks(n: int, block_size: int, overlap: int) -> int:
 
 def supported(dtype: int, n_subbands: int, block_size: int) -> bool:
     return bool(load().cbessfm_supported(dtype, n_subbands, block_size))
+
+
+def ssfm_info(dtype: int, n: int, batch: int = 1, device: int = -1) -> SsfmInfo:
+    lib = load()
+    out = SsfmInfo()
+    check(lib.cbessfm_ssfm_info_get(dtype, n, batch, device, C.byref(out)),
+          "cbessfm_ssfm_info_get", lib.cbessfm_ssfm_last_error)
+    return out
+
+
+def ssfm_run(*, dtype: int, data_ptr: int, n: int, batch: int, n_spans: int,
+             half: np.ndarray, step_table: np.ndarray, nl_coef: np.ndarray,
+             backward: bool, gain: float, noise_ptr: int | None, device: int,
+             stream: int) -> None:
+    """cbessfm_ssfm_run over a device [batch][2][n] buffer, in place."""
+    lib = load()
+    h = np.ascontiguousarray(half, np.complex128)
+    st = np.ascontiguousarray(step_table, np.int32)
+    nl = np.ascontiguousarray(nl_coef, np.float64)
+    d = SsfmDesc(dtype, n, batch, n_spans, st.size, h.shape[0],
+                 _dptr(h.view(np.float64)), st.ctypes.data_as(C.POINTER(C.c_int32)),
+                 _dptr(nl), int(backward), float(gain), device)
+    check(lib.cbessfm_ssfm_run(C.byref(d), C.c_void_p(data_ptr),
+                               C.c_void_p(noise_ptr) if noise_ptr else None,
+                               C.c_void_p(stream)),
+          "cbessfm_ssfm_run", lib.cbessfm_ssfm_last_error)

@@ -20,7 +20,8 @@ BUILD = PKG.parent / "build" / "cbessfm"
 LIB = PKG / "libcbessfm.so"
 HEADERS = [CSRC / "cbessfm_kernel.cuh", CSRC / "cbessfm_launch.cuh",
            PKG.parent / "include" / "cbessfm.h",
-           PKG.parent / "include" / "cbessfm_peaks.h"]
+           PKG.parent / "include" / "cbessfm_peaks.h",
+           PKG.parent / "include" / "cbessfm_ssfm.h"]
 REALS = ("float", "double")
 SUBBANDS = tuple(range(1, 10))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -83,6 +84,8 @@ def build(jobs: int | None = None, verbose: bool = False, profile: bool = False,
                   BUILD / "peaks.log"))
     tasks.append((CSRC / "cbessfm_nlpr.cu", BUILD / "nlpr.o", [], HEADERS,
                   BUILD / "nlpr.log"))
+    tasks.append((CSRC / "cbessfm_ssfm.cu", BUILD / "ssfm.o", [], HEADERS,
+                  BUILD / "ssfm.log"))
     with ThreadPoolExecutor(jobs) as ex:
         results = list(ex.map(_compile, tasks))
     errors = [e for _, e in results if e]

@@ -99,9 +99,8 @@ def _variant_geometry(cfg, coeffs):
         return cfg.n_subbands
     if cfg.variant in ("EDC", "ESSFM", "OSSFM"):
         return 1
-    raise NotImplementedError(
-        f"variant {cfg.variant!r} has no B200 path (the fine-step IDEAL_SSFM "
-        "oracle is out of the hot path's scope, SURVEY.md 2.1)")
+    raise ValueError(f"variant {cfg.variant!r} has no block pipeline "
+                     "(IDEAL_SSFM runs the fine-step propagator, channel.py)")
 
 
 def _config_key(cfg, rate: float, coeffs, n_sb: int) -> tuple:
@@ -226,6 +225,11 @@ def run_dbp(w, cfg, coeffs=None, counter=None, *, dtype: str = "c128",
     torch = _torch()
     w.require_finite()
     validate_config(cfg)
+    if cfg.variant == "IDEAL_SSFM":
+        # fine-step inverse propagation of the whole sequence (dbp.py:451-454)
+        from .channel import SimSettings, backward_propagate
+        sim = SimSettings(step_km=cfg.link.total_length_km / cfg.n_steps, noise_enabled=False)
+        return backward_propagate(w, cfg.link, sim, dtype=dtype, device=device)
     n_sb = _variant_geometry(cfg, coeffs)
     n = w.num_samples
     if cfg.block_size > n:

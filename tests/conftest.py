@@ -104,3 +104,44 @@ def cuda():
         pytest.fail("GPU test selected but no CUDA device is visible")
     import torch
     return torch.device("cuda", 0)
+
+
+SSFM_CASES = ("fwd", "bwd", "noise", "adaptive", "large", "resume", "ideal_dbp")
+
+
+class SsfmGolden:
+    """tests/golden/ssfm_<name>.npz: input, rate, link/sim fields and the
+    reference's propagate_link / backward_propagate / IDEAL_SSFM output."""
+
+    def __init__(self, name):
+        import json
+        d = np.load(GOLDEN / f"ssfm_{name}.npz")
+        self.name = name
+        self.field = np.vstack([d["x"], d["y"]])
+        self.rate = float(d["rate"])
+        self.out = np.vstack([d["ox"], d["oy"]])
+        self.meta = json.loads(str(d["meta"]))
+
+    @property
+    def backward(self):
+        return self.name in ("bwd", "ideal_dbp")
+
+    def link(self):
+        from paper_2409_14489_b200.config import LinkConfig
+        m = self.meta
+        return LinkConfig(num_spans=m["num_spans"], span_length_km=m["span_length_km"],
+                          alpha_db_per_km=m["alpha_db_per_km"],
+                          dispersion_d_ps_nm_km=m["dispersion_d_ps_nm_km"],
+                          gamma_w_km=m["gamma_w_km"],
+                          edfa_noise_figure_db=m["edfa_noise_figure_db"])
+
+    def sim(self):
+        from paper_2409_14489_b200.channel import SimSettings
+        m = self.meta
+        return SimSettings(step_km=m["step_km"], max_phase_rad=m["max_phase_rad"],
+                           max_step_km=m["max_step_km"], noise_enabled=m["noise_enabled"],
+                           noise_seed=m["noise_seed"])
+
+    def wave(self):
+        from paper_2409_14489_b200.config import DualPolWaveform
+        return DualPolWaveform(self.field[0].copy(), self.field[1].copy(), self.rate, 0.0)

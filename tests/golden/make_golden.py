@@ -268,6 +268,55 @@ def main():
         np.savez_compressed(HERE / "cfg4_coeffs.npz", **arrays)
         print("  wrote cfg4_coeffs.npz")
 
+    # --- forward / backward fine-step propagation:
+    #     propagate_link, backward_propagate (channel.py:176-256) and the
+    #     IDEAL_SSFM variant of run_dbp (dbp.py:451-454)
+    def save_ssfm(name, w_in, lk, sim, out, **extra):
+        meta = dict(num_spans=lk.num_spans, span_length_km=lk.span_length_km,
+                    alpha_db_per_km=lk.alpha_db_per_km,
+                    dispersion_d_ps_nm_km=lk.dispersion_d_ps_nm_km,
+                    gamma_w_km=lk.gamma_w_km,
+                    edfa_noise_figure_db=lk.edfa_noise_figure_db,
+                    step_km=sim.step_km, max_phase_rad=sim.max_phase_rad,
+                    max_step_km=sim.max_step_km, noise_enabled=sim.noise_enabled,
+                    noise_seed=sim.noise_seed, **extra)
+        np.savez_compressed(HERE / f"ssfm_{name}.npz", x=w_in.x, y=w_in.y,
+                            rate=w_in.sample_rate, ox=out.x, oy=out.y,
+                            meta=json.dumps(meta))
+        print(f"  wrote ssfm_{name}.npz")
+
+    if want("ssfm"):
+        two = fd.LinkConfig(num_spans=2, span_length_km=80.0)
+        wdm = fd.WdmConfig(baud_rate=32e9, launch_power_dbm_per_channel=3.0)
+        w, _ = fd.generate_wdm(wdm, 1024, sim_rate=64e9, seed=2)
+        sim = fd.SimSettings(step_km=1.0, noise_enabled=False)
+        fwd = fd.propagate_link(w, two, sim)
+        save_ssfm("fwd", w, two, sim, fwd)
+        save_ssfm("bwd", fwd, two, sim, fd.backward_propagate(fwd, two, sim))
+        simn = fd.SimSettings(step_km=2.0, noise_enabled=True, noise_seed=5)
+        save_ssfm("noise", w, two, simn, fd.propagate_link(w, two, simn))
+        sima = fd.SimSettings(max_phase_rad=2e-3, max_step_km=4.0, noise_enabled=False)
+        wa, _ = fd.generate_wdm(fd.WdmConfig(baud_rate=32e9,
+                                             launch_power_dbm_per_channel=6.0),
+                                2048, sim_rate=64e9, seed=3)
+        save_ssfm("adaptive", wa, two, sima, fd.propagate_link(wa, two, sima))
+        # n = 2^15: a multi-tile four-step geometry (configs[0] layout)
+        wl, _ = fd.generate_wdm(fd.WdmConfig(64e9, 1, 0.0, 0.05, "16-qam", 2.0),
+                                2 ** 14, sim_rate=128e9, seed=9)
+        siml = fd.SimSettings(step_km=4.0, noise_enabled=False)
+        save_ssfm("large", wl, link(2), siml, fd.propagate_link(wl, link(2), siml))
+        # resume from a checkpoint after span 1
+        snaps = {}
+        fd.propagate_link(w, two, sim, checkpoint=lambda s, v: snaps.setdefault(s, v))
+        save_ssfm("resume", snaps[1], two, sim,
+                  fd.propagate_link(snaps[1], two, sim, first_span=1), first_span=1)
+        # IDEAL_SSFM run_dbp on the configs[0] waveform (30 fine steps)
+        cfg = fd.DbpConfig(link=link(15), variant="IDEAL_SSFM", n_steps=30,
+                           n_subbands=1, block_size=4096, overlap=2680, oversampling=2.0)
+        save_ssfm("ideal_dbp", w1, link(15),
+                  fd.SimSettings(step_km=link(15).total_length_km / 30, noise_enabled=False),
+                  fd.run_dbp(w1, cfg), n_steps=30)
+
     print(f"done in {time.time() - t0:.1f} s")
 
 

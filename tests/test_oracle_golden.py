@@ -83,3 +83,18 @@ def test_oracle_snr_reproduces_reference():
                                       float(g.extra("launch_power_w")))
         s = orc.snr_db(sym, g.extra("tx_symbols"))
         assert abs(s - float(g.extra("snr_db"))) < 1e-9
+
+
+@pytest.mark.parametrize("name", ["fwd", "bwd", "noise", "adaptive", "large", "resume",
+                                  "ideal_dbp"])
+def test_ssfm_oracle_matches_reference(name):
+    # oracle/ssfm_oracle.py vs the reference's propagate_link /
+    # backward_propagate / run_dbp(IDEAL_SSFM) (tests/golden/ssfm_*.npz)
+    from conftest import SsfmGolden
+    from oracle import ssfm_oracle as so
+    g = SsfmGolden(name)
+    if g.backward:
+        out = so.backward(g.field, g.rate, g.meta)
+    else:
+        out = so.propagate(g.field, g.rate, g.meta, g.meta.get("first_span", 0))
+    assert rel_rms(out, g.out) < 1e-13
