@@ -31,7 +31,7 @@ extern "C" {
 
 typedef struct {
   int32_t dtype;            /* cbessfm_dtype                                   */
-  int64_t n;                /* samples per polarisation, a power of two >= 2   */
+  int64_t n;                /* samples per polarisation, power of two, 2..2^22 */
   int32_t batch;            /* waveforms                                       */
   int32_t n_spans;          /* spans to run                                    */
   int32_t steps_per_span;   /* fine steps per span (span_step_sizes)           */

@@ -3,7 +3,7 @@
 // backward_propagate (channel.py:176-256), the IDEAL_SSFM variant of
 // run_dbp (dbp.py:451-454).
 //
-// The whole waveform (n up to 2^23 per polarisation) is transformed with a
+// The whole waveform (n up to 2^22 per polarisation) is transformed with a
 // four-step FFT, n = n1 * n2, data kept in natural time order [n1][n2]:
 //   forward:  column FFTs of length n1, twiddle W_n^(j2 k1), row FFTs of
 //             length n2 -> spectrum X[k1 + n1 k2] stored at (k1, k2);
@@ -34,8 +34,29 @@ namespace cbessfm {
 namespace ssfm {
 namespace cg = cooperative_groups;
 
-constexpr int kThreads = 512;
-constexpr int kTileElems = 8192;  // complex elements per tile, both polarisations
+#ifndef CB_SSFM_THREADS  // experiment knob (build.py --variant ... --define)
+#define CB_SSFM_THREADS 1024
+#endif
+constexpr int kThreads = CB_SSFM_THREADS;
+constexpr int kTileElems = 4096;  // complex elements per tile, both polarisations
+constexpr int kMaxLog2N = 22;     // n1, n2 <= 2048
+
+// Shared-memory layout of a tile: sequence m of length L starts at
+// m * seq_stride(L) and element i sits at pad(i). One pad slot per 128 B
+// row plus one per sequence keeps the Stockham stride-RAD writes and the
+// column-strip transposes free of bank conflicts.
+template <typename R>
+__host__ __device__ constexpr int pad_shift() {
+  return sizeof(R) == 8 ? 4 : 3;
+}
+template <typename R>
+__device__ __forceinline__ int spad(int i) {
+  return i + (i >> pad_shift<R>());
+}
+template <typename R>
+__host__ __device__ constexpr int seq_stride(int L) {
+  return L + (L >> pad_shift<R>()) + 1;
+}
 
 template <typename R>
 struct Params {
@@ -44,6 +65,7 @@ struct Params {
   int batch;
   int n1, n2;              // column length, row length
   int rows, cols;          // rows per row tile, columns per column tile
+  int lg_n2, lg_rows, lg_cols;
   const Cx<R>* tw_hi;      // W_n^(h << lo_bits)
   const Cx<R>* tw_lo;      // W_n^l, l < 2^lo_bits
   int lo_bits;
@@ -60,29 +82,31 @@ struct Params {
 };
 
 // One Stockham pass of radix RAD and stride ns over M sequences of length L
-// (sequence m at buf + m * L): inputs j + r L/RAD, twiddled by
+// (sequence m at buf + m * seq_stride(L), padded): inputs j + r L/RAD, twiddled by
 // W_(RAD ns)^(r k), k = j mod ns, outputs (j/ns) ns RAD + k + r ns.
 // Reads all of the thread's butterflies before a barrier, then writes.
-template <typename R, int RAD, bool INV>
-__device__ __forceinline__ void stockham_pass(Cx<R>* buf, int M, int L, int ns,
-                                              const Cx<R>* __restrict__ twL) {
-  constexpr int KMAX = kTileElems / (RAD * kThreads);
-  const int LR = L / RAD, nb = M * LR, tid = threadIdx.x;
-  const int lg_lr = __ffs(LR) - 1, lg_ns = __ffs(ns) - 1;
-  const int tstep = L / (RAD * ns);
+// L and ns are compile-time: every pass is specialised (no runtime shifts,
+// the butterfly arrays stay in registers).
+template <typename R, int RAD, bool INV, int L, int NS>
+__device__ __forceinline__ void stockham_pass(Cx<R>* buf, int M, const Cx<R>* __restrict__ twL) {
+  constexpr int LR = L / RAD, SL = seq_stride<R>(L), TSTEP = L / (RAD * NS);
+  constexpr int KMAX = (kTileElems / RAD + kThreads - 1) / kThreads;
+  const int nb = M * LR, tid = threadIdx.x;
   Cx<R> v[KMAX][RAD];
 #pragma unroll
   for (int q = 0; q < KMAX; ++q) {
     const int u = tid + q * kThreads;
     if (u < nb) {
-      const int m = u >> lg_lr, j = u & (LR - 1), kk = j & (ns - 1);
-      const Cx<R>* b = buf + (size_t)m * L + j;
+      const int m = u / LR, j = u % LR, kk = j % NS;
+      const Cx<R>* b = buf + m * SL;
 #pragma unroll
-      for (int r = 0; r < RAD; ++r) v[q][r] = b[r * LR];
+      for (int r = 0; r < RAD; ++r) v[q][r] = b[spad<R>(j + r * LR)];
+      if (NS > 1) {
 #pragma unroll
-      for (int r = 1; r < RAD; ++r) {
-        const Cx<R> w = ldg(twL + r * kk * tstep);
-        v[q][r] = INV ? cmulc(v[q][r], w) : cmul(v[q][r], w);
+        for (int r = 1; r < RAD; ++r) {
+          const Cx<R> w = ldg(twL + r * kk * TSTEP);
+          v[q][r] = INV ? cmulc(v[q][r], w) : cmul(v[q][r], w);
+        }
       }
     }
   }
@@ -91,34 +115,62 @@ __device__ __forceinline__ void stockham_pass(Cx<R>* buf, int M, int L, int ns,
   for (int q = 0; q < KMAX; ++q) {
     const int u = tid + q * kThreads;
     if (u < nb) {
-      const int m = u >> lg_lr, j = u & (LR - 1), kk = j & (ns - 1);
-      Cx<R>* b = buf + (size_t)m * L + ((j >> lg_ns) << lg_ns) * RAD + kk;
+      const int m = u / LR, j = u % LR, kk = j % NS;
+      Cx<R>* b = buf + m * SL;
+      const int o = (j / NS) * NS * RAD + kk;
       if (RAD == 2) {
-        b[0] = v[q][0] + v[q][1];
-        b[ns] = v[q][0] - v[q][1];
+        b[spad<R>(o)] = v[q][0] + v[q][1];
+        b[spad<R>(o + NS)] = v[q][0] - v[q][1];
       } else {
         const Cx<R> t0 = v[q][0] + v[q][2], t1 = v[q][0] - v[q][2];
         const Cx<R> t2 = v[q][1] + v[q][3], d = v[q][1] - v[q][3];
         const Cx<R> t3 = INV ? mk(-d.y, d.x) : mk(d.y, -d.x);  // +-j (a1 - a3)
-        b[0] = t0 + t2;
-        b[ns] = t1 + t3;
-        b[2 * ns] = t0 - t2;
-        b[3 * ns] = t1 - t3;
+        b[spad<R>(o)] = t0 + t2;
+        b[spad<R>(o + NS)] = t1 + t3;
+        b[spad<R>(o + 2 * NS)] = t0 - t2;
+        b[spad<R>(o + 3 * NS)] = t1 - t3;
       }
     }
   }
   __syncthreads();
 }
 
-// Unnormalised DFT (INV: conjugate kernel) of M sequences of length L.
-template <typename R, bool INV>
-__device__ __noinline__ void cta_fft(Cx<R>* buf, int M, int L, const Cx<R>* __restrict__ twL) {
-  int ns = 1;
-  if ((__ffs(L) - 1) & 1) {
-    stockham_pass<R, 2, INV>(buf, M, L, 1, twL);
-    ns = 2;
+template <typename R, bool INV, int L, int NS>
+__device__ __forceinline__ void radix4_passes(Cx<R>* buf, int M, const Cx<R>* twL) {
+  if constexpr (NS < L) {
+    stockham_pass<R, 4, INV, L, NS>(buf, M, twL);
+    radix4_passes<R, INV, L, NS * 4>(buf, M, twL);
   }
-  for (; ns < L; ns *= 4) stockham_pass<R, 4, INV>(buf, M, L, ns, twL);
+}
+
+// Unnormalised DFT (INV: conjugate kernel) of M sequences of length L.
+template <typename R, bool INV, int L>
+__device__ __noinline__ void cta_fft_l(Cx<R>* buf, int M, const Cx<R>* __restrict__ twL) {
+  constexpr int LG = __builtin_ctz(L);
+  if constexpr (LG & 1) {
+    stockham_pass<R, 2, INV, L, 1>(buf, M, twL);
+    radix4_passes<R, INV, L, 2>(buf, M, twL);
+  } else {
+    radix4_passes<R, INV, L, 1>(buf, M, twL);
+  }
+}
+
+template <typename R, bool INV>
+__device__ __forceinline__ void cta_fft(Cx<R>* buf, int M, int L, const Cx<R>* twL) {
+  switch (L) {
+    case 2: cta_fft_l<R, INV, 2>(buf, M, twL); break;
+    case 4: cta_fft_l<R, INV, 4>(buf, M, twL); break;
+    case 8: cta_fft_l<R, INV, 8>(buf, M, twL); break;
+    case 16: cta_fft_l<R, INV, 16>(buf, M, twL); break;
+    case 32: cta_fft_l<R, INV, 32>(buf, M, twL); break;
+    case 64: cta_fft_l<R, INV, 64>(buf, M, twL); break;
+    case 128: cta_fft_l<R, INV, 128>(buf, M, twL); break;
+    case 256: cta_fft_l<R, INV, 256>(buf, M, twL); break;
+    case 512: cta_fft_l<R, INV, 512>(buf, M, twL); break;
+    case 1024: cta_fft_l<R, INV, 1024>(buf, M, twL); break;
+    case 2048: cta_fft_l<R, INV, 2048>(buf, M, twL); break;
+    default: break;  // L == 1: identity
+  }
 }
 
 template <typename R>
@@ -129,33 +181,38 @@ __device__ __forceinline__ Cx<R> tw_n(const Params<R>& p, int64_t e) {
 // Row phase: FFT_n2, the spectral half steps, IFFT_n2 (channel.py:206, :211).
 template <typename R>
 __device__ void row_phase(const Params<R>& p, Cx<R>* buf, const Cx<R>* ha, const Cx<R>* hb) {
-  const int per_wave = p.n1 / p.rows;
-  const int tile_len = p.rows * p.n2;  // per polarisation
+  const int per_wave = p.n1 >> p.lg_rows;
+  const int tile_len = p.rows << p.lg_n2;  // per polarisation
+  const int SL = seq_stride<R>(p.n2);
+  // element e of the tile: pol, row r, column c -> sequence pol*rows + r
+  auto at = [&](int e) {
+    return buf + (e >> p.lg_n2) * SL + spad<R>(e & (p.n2 - 1));
+  };
   for (int t = blockIdx.x; t < p.batch * per_wave; t += gridDim.x) {
     const int b = t / per_wave;
-    const int64_t r0 = (int64_t)(t % per_wave) * p.rows;
-    Cx<R>* base = p.data + (int64_t)b * 2 * p.n + r0 * p.n2;
+    const int64_t r0 = (int64_t)(t % per_wave) << p.lg_rows;
+    Cx<R>* base = p.data + (int64_t)b * 2 * p.n + (r0 << p.lg_n2);
     for (int e = threadIdx.x; e < 2 * tile_len; e += kThreads) {
       const int pol = e >= tile_len, i = e - pol * tile_len;
-      buf[e] = base[pol * p.n + i];
+      *at(e) = base[pol * p.n + i];
     }
     __syncthreads();
     cta_fft<R, false>(buf, 2 * p.rows, p.n2, p.tw2);
     if (ha || hb) {
-      const int64_t h0 = r0 * p.n2;
+      const int64_t h0 = r0 << p.lg_n2;
       for (int e = threadIdx.x; e < 2 * tile_len; e += kThreads) {
         const int pol = e >= tile_len, i = e - pol * tile_len;
-        Cx<R> v = buf[e];
+        Cx<R> v = *at(e);
         if (ha) v = cmul(v, ldg(ha + h0 + i));
         if (hb) v = cmul(v, ldg(hb + h0 + i));
-        buf[e] = v;
+        *at(e) = v;
       }
       __syncthreads();
     }
     cta_fft<R, true>(buf, 2 * p.rows, p.n2, p.tw2);
     for (int e = threadIdx.x; e < 2 * tile_len; e += kThreads) {
       const int pol = e >= tile_len, i = e - pol * tile_len;
-      base[pol * p.n + i] = buf[e];
+      base[pol * p.n + i] = *at(e);
     }
     __syncthreads();
   }
@@ -169,28 +226,29 @@ enum Mid { kNone = 0, kNonlinear = 1, kSpanEnd = 2 };
 template <typename R>
 __device__ void col_phase(const Params<R>& p, Cx<R>* buf, bool inv_in, int mid, R nl,
                           const Cx<R>* noise, bool pre_div, bool fwd_out) {
-  const int per_wave = p.n2 / p.cols;
-  const int seq = p.n1;              // sequence length
-  const int tile_len = p.cols * seq; // per polarisation
-  const R inv_n = (R)1 / (R)p.n;     // exact: n is a power of two
+  const int per_wave = p.n2 >> p.lg_cols;
+  const int seq = p.n1;                  // sequence length
+  const int tile_len = p.cols * seq;     // per polarisation
+  const int SL = seq_stride<R>(seq);
+  const R inv_n = (R)1 / (R)p.n;         // exact: n is a power of two
   for (int t = blockIdx.x; t < p.batch * per_wave; t += gridDim.x) {
     const int b = t / per_wave;
-    const int c0 = (t % per_wave) * p.cols;
+    const int c0 = (t % per_wave) << p.lg_cols;
     Cx<R>* base = p.data + (int64_t)b * 2 * p.n + c0;
-    // element e: pol, row k1, column c (fastest) -> buf[(pol cols + c) n1 + k1]
+    // element e: pol, row k1, column c (fastest) -> sequence pol*cols + c
     for (int e = threadIdx.x; e < 2 * tile_len; e += kThreads) {
       const int pol = e >= tile_len, i = e - pol * tile_len;
-      const int k1 = i / p.cols, c = i - k1 * p.cols;
-      Cx<R> v = base[pol * p.n + (int64_t)k1 * p.n2 + c];
+      const int k1 = i >> p.lg_cols, c = i & (p.cols - 1);
+      Cx<R> v = base[pol * p.n + ((int64_t)k1 << p.lg_n2) + c];
       if (inv_in) v = cmulc(v, tw_n(p, (int64_t)(c0 + c) * k1));
-      buf[(pol * p.cols + c) * seq + k1] = v;
+      buf[(pol * p.cols + c) * SL + spad<R>(k1)] = v;
     }
     __syncthreads();
     if (inv_in) cta_fft<R, true>(buf, 2 * p.cols, seq, p.tw1);
     for (int e = threadIdx.x; e < tile_len; e += kThreads) {
-      const int c = e / seq, j1 = e - c * seq;
-      Cx<R>* px = buf + c * seq + j1;
-      Cx<R>* py = buf + (p.cols + c) * seq + j1;
+      const int c = e / seq, j1 = e & (seq - 1);
+      Cx<R>* px = buf + c * SL + spad<R>(j1);
+      Cx<R>* py = buf + (p.cols + c) * SL + spad<R>(j1);
       Cx<R> x = *px, y = *py;
       if (inv_in) {
         x = scale(x, inv_n);
@@ -209,7 +267,7 @@ __device__ void col_phase(const Params<R>& p, Cx<R>* buf, bool inv_in, int mid, 
         x = scale(x, p.gain);
         y = scale(y, p.gain);
         if (noise) {
-          const int64_t at = (int64_t)b * 2 * p.n + (int64_t)j1 * p.n2 + c0 + c;
+          const int64_t at = (int64_t)b * 2 * p.n + ((int64_t)j1 << p.lg_n2) + c0 + c;
           x = x + ldg(noise + at);
           y = y + ldg(noise + at + p.n);
         }
@@ -225,17 +283,17 @@ __device__ void col_phase(const Params<R>& p, Cx<R>* buf, bool inv_in, int mid, 
     if (fwd_out) cta_fft<R, false>(buf, 2 * p.cols, seq, p.tw1);
     for (int e = threadIdx.x; e < 2 * tile_len; e += kThreads) {
       const int pol = e >= tile_len, i = e - pol * tile_len;
-      const int k1 = i / p.cols, c = i - k1 * p.cols;
-      Cx<R> v = buf[(pol * p.cols + c) * seq + k1];
+      const int k1 = i >> p.lg_cols, c = i & (p.cols - 1);
+      Cx<R> v = buf[(pol * p.cols + c) * SL + spad<R>(k1)];
       if (fwd_out) v = cmul(v, tw_n(p, (int64_t)(c0 + c) * k1));
-      base[pol * p.n + (int64_t)k1 * p.n2 + c] = v;
+      base[pol * p.n + ((int64_t)k1 << p.lg_n2) + c] = v;
     }
     __syncthreads();
   }
 }
 
 template <typename R>
-__global__ void __launch_bounds__(kThreads, 1) ssfm_kernel(Params<R> p) {
+__global__ void __launch_bounds__(kThreads, 1024 / kThreads) ssfm_kernel(Params<R> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Cx<R>* buf = reinterpret_cast<Cx<R>*>(smem_raw);
   cg::grid_group grid = cg::this_grid();
@@ -286,7 +344,9 @@ Geo geometry(int64_t n, int batch, size_t esz, int target_tiles) {
   while (g.cols * 2 <= g.n2 && 2 * (g.cols * 2) * g.n1 <= kTileElems &&
          ((int64_t)batch * g.n2 / (g.cols * 2) >= target_tiles || g.cols < 4))
     g.cols *= 2;
-  g.smem = esz * (size_t)std::max(2 * g.rows * g.n2, 2 * g.cols * g.n1);
+  const int ps = esz == 16 ? 4 : 3;
+  auto stride = [&](int L) { return L + (L >> ps) + 1; };
+  g.smem = esz * (size_t)std::max(2 * g.rows * stride(g.n2), 2 * g.cols * stride(g.n1));
   return g;
 }
 
@@ -369,6 +429,9 @@ cbessfm_status run(const cbessfm_ssfm_desc* d, void* data, const void* noise, cu
   p.n2 = g.n2;
   p.rows = g.rows;
   p.cols = g.cols;
+  p.lg_n2 = __builtin_ctz(g.n2);
+  p.lg_rows = __builtin_ctz(g.rows);
+  p.lg_cols = __builtin_ctz(g.cols);
   p.tw_hi = reinterpret_cast<const Cx<R>*>(dhi);
   p.tw_lo = reinterpret_cast<const Cx<R>*>(dlo);
   p.lo_bits = lo_bits;
@@ -403,7 +466,7 @@ cbessfm_status cbessfm_ssfm_info_get(int32_t dtype, int64_t n, int32_t batch, in
   g_err.clear();
   if (!info || n < 2 || (n & (n - 1)) || batch < 1)
     return fail(CBESSFM_ERR_INVALID, "n must be a power of two >= 2, batch >= 1");
-  if (n > (int64_t(1) << 23)) return fail(CBESSFM_ERR_UNSUPPORTED, "n above 2^23");
+  if (n > (int64_t(1) << kMaxLog2N)) return fail(CBESSFM_ERR_UNSUPPORTED, "n above 2^22");
   int sms = 148;
   if (device >= 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   const size_t esz = dtype == CBESSFM_C64 ? 8 : 16;
@@ -427,7 +490,7 @@ cbessfm_status cbessfm_ssfm_run(const cbessfm_ssfm_desc* d, void* data, const vo
     return fail(CBESSFM_ERR_INVALID, "bad dtype");
   if (d->n < 2 || (d->n & (d->n - 1)))
     return fail(CBESSFM_ERR_UNSUPPORTED, "the GPU propagator needs a power-of-two length");
-  if (d->n > (int64_t(1) << 23)) return fail(CBESSFM_ERR_UNSUPPORTED, "n above 2^23");
+  if (d->n > (int64_t(1) << kMaxLog2N)) return fail(CBESSFM_ERR_UNSUPPORTED, "n above 2^22");
   if (d->batch < 1 || d->n_spans < 0 || d->steps_per_span < 1 || d->n_tables < 1 || !d->half ||
       !d->step_table || !d->nl_coef)
     return fail(CBESSFM_ERR_INVALID, "bad propagation description");

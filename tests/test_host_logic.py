@@ -242,15 +242,17 @@ def test_header_abi_version_matches_binding():
     assert [f for f, _ in _native.Desc._fields_][-1] == "n_sets"
 
 
-@pytest.mark.parametrize("n", [2, 64, 1 << 12, 1 << 17, 1 << 21, 1 << 23])
+@pytest.mark.parametrize("n", [2, 64, 1 << 12, 1 << 17, 1 << 21, 1 << 22])
 def test_ssfm_four_step_geometry(n):
-    # csrc/cbessfm_ssfm.cu: n = n1 * n2, every tile fits the 8192-element
+    # csrc/cbessfm_ssfm.cu: n = n1 * n2, every tile fits the 4096-element
     # shared-memory budget (host-only query, no GPU)
     from paper_2409_14489_b200 import _native
     for dt in (_native.C64, _native.C128):
         info = _native.ssfm_info(dt, n, 1, -1)
         assert info.n1 * info.n2 == n
-        assert 2 * info.rows_per_tile * info.n2 <= 8192
-        assert 2 * info.cols_per_tile * info.n1 <= 8192
+        assert 2 * info.rows_per_tile * info.n2 <= 4096
+        assert 2 * info.cols_per_tile * info.n1 <= 4096
     with pytest.raises(ValueError):
         _native.ssfm_info(_native.C128, 3 * n, 1, -1)
+    with pytest.raises(ValueError):
+        _native.ssfm_info(_native.C128, 1 << 23, 1, -1)   # above the 2^22 limit
