@@ -68,6 +68,13 @@ class SsfmInfo(C.Structure):
                 ("smem_bytes", C.c_int64)]
 
 
+class StepKernel(C.Structure):
+    _fields_ = [("closed_form", C.c_int32), ("gamma_w_km", C.c_double),
+                ("alpha_np_km", C.c_double), ("beat_scale", C.c_double),
+                ("span_km", C.c_double), ("num_spans", C.c_int32),
+                ("n_segments", C.c_int32), ("segments", C.POINTER(C.c_double))]
+
+
 # every symbol include/*.h declares: name -> (restype, argtypes)
 SIGNATURES = {
     "cbessfm_version": (C.c_int32, []),
@@ -89,6 +96,14 @@ SIGNATURES = {
     "cbessfm_ssfm_info_get": (C.c_int, [C.c_int32, C.c_int64, C.c_int32, C.c_int32,
                                         C.POINTER(SsfmInfo)]),
     "cbessfm_ssfm_last_error": (C.c_char_p, []),
+    # include/cbessfm_coeff.h
+    "cbessfm_coeff_grid": (C.c_int, [C.POINTER(StepKernel), C.c_int64, C.POINTER(C.c_double),
+                                     C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_double),
+                                     C.c_int32]),
+    "cbessfm_step_kernel_eval": (C.c_int, [C.POINTER(StepKernel), C.c_int64,
+                                           C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                           C.POINTER(C.c_double), C.c_int32]),
+    "cbessfm_coeff_last_error": (C.c_char_p, []),
 }
 
 _lib = None

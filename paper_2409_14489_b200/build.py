@@ -21,7 +21,8 @@ LIB = PKG / "libcbessfm.so"
 HEADERS = [CSRC / "cbessfm_kernel.cuh", CSRC / "cbessfm_launch.cuh",
            PKG.parent / "include" / "cbessfm.h",
            PKG.parent / "include" / "cbessfm_peaks.h",
-           PKG.parent / "include" / "cbessfm_ssfm.h"]
+           PKG.parent / "include" / "cbessfm_ssfm.h",
+           PKG.parent / "include" / "cbessfm_coeff.h"]
 REALS = ("float", "double")
 SUBBANDS = tuple(range(1, 10))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -86,6 +87,8 @@ def build(jobs: int | None = None, verbose: bool = False, profile: bool = False,
                   BUILD / "nlpr.log"))
     tasks.append((CSRC / "cbessfm_ssfm.cu", BUILD / "ssfm.o", [], HEADERS,
                   BUILD / "ssfm.log"))
+    tasks.append((CSRC / "cbessfm_coeff.cu", BUILD / "coeff.o", [], HEADERS,
+                  BUILD / "coeff.log"))
     with ThreadPoolExecutor(jobs) as ex:
         results = list(ex.map(_compile, tasks))
     errors = [e for _, e in results if e]

@@ -100,6 +100,14 @@ class DbpConfig:
     def step_length_km(self) -> float:
         return self.link.total_length_km / max(self.n_steps, 1)
 
+    def step_geometry(self):
+        """Geometry of one (span-aligned, representative) step (dbp.py:94-102)."""
+        from .coefficients import StepGeometry
+        return StepGeometry(length_km=self.step_length_km, span_km=self.link.span_length_km,
+                            alpha_db_km=self.link.alpha_db_per_km,
+                            beta2_ps2_km=self.link.beta2_ps2_km,
+                            gamma_w_km=self.link.gamma_w_km, rho=self.splitting_ratio)
+
 
 def validate_config(cfg) -> None:
     """The invariants of DbpConfig.__post_init__ (dbp.py:64-88).

@@ -98,3 +98,21 @@ def test_ssfm_oracle_matches_reference(name):
     else:
         out = so.propagate(g.field, g.rate, g.meta, g.meta.get("first_span", 0))
     assert rel_rms(out, g.out) < 1e-13
+
+
+@pytest.mark.parametrize("tag", ["s15_b1_r5_", "s5_b3_r5_", "s2_b3_r7_", "s3_b5_r10_"])
+def test_coefficient_oracle_matches_reference_sets(tag):
+    # oracle/coeff_oracle.py vs make_dbp_coefficient_set as the reference ran
+    # it for the configs[2] sweep (closed form: s15/s5 at rho 0.5; piecewise:
+    # s2 (7.5 spans per step), rho != 0.5)
+    from oracle import coeff_oracle as co
+    d = np.load(GOLDEN / "sweep_coeffs.npz")
+    ref = load_coeffs(d, tag)
+    n_st, n_sb, rho = int(tag[1:tag.index("_")]), ref.n_sb, int(tag.split("_r")[1][:-1]) / 10
+    from paper_2409_14489_b200.config import LinkConfig
+    link = dict(num_spans=15, span_length_km=80.0, alpha_db_per_km=0.2, gamma_w_km=1.3,
+                beta2_ps2_km=LinkConfig(15, 80.0, gamma_w_km=1.3).beta2_ps2_km)
+    got = co.dbp_set(link, n_st, n_sb, rho, 128e9, ref.reference_power_w, 7)
+    for h in range(n_sb):
+        c = ref.coeffs[h]
+        assert np.abs(got[h] - c).max() < 1e-11 * np.abs(c).max(), h
