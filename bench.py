@@ -381,9 +381,10 @@ def main():
         # double-buffered host outputs, so step k+1's H2D overlaps step k's
         # kernel tail and D2H; every step still copies its whole input in
         # and its whole result out
+        inflight = int(os.environ.get("BENCH_E2E_INFLIGHT", "2"))
         hx = x.cpu().pin_memory()
-        houts = [torch.empty_like(hx).pin_memory() for _ in range(2)]
-        sides = [torch.cuda.Stream(cdev) for _ in range(2)]
+        houts = [torch.empty_like(hx).pin_memory() for _ in range(inflight)]
+        sides = [torch.cuda.Stream(cdev) for _ in range(inflight)]
 
         def e2e_steps(k):
             start = torch.cuda.Event()
@@ -391,7 +392,7 @@ def main():
             for side in sides:
                 side.wait_event(start)
             for i in range(k):
-                eng.run_host(hx, houts[i % 2], stream=sides[i % 2])
+                eng.run_host(hx, houts[i % inflight], stream=sides[i % inflight])
             for side in sides:
                 done = torch.cuda.Event()
                 done.record(side)

@@ -75,6 +75,13 @@ class StepKernel(C.Structure):
                 ("n_segments", C.c_int32), ("segments", C.POINTER(C.c_double))]
 
 
+class RxDesc(C.Structure):
+    _fields_ = [("dtype", C.c_int32), ("n", C.c_int64), ("sample_rate", C.c_double),
+                ("n_channels", C.c_int32), ("channel_freq", C.POINTER(C.c_double)),
+                ("bandwidth", C.c_double), ("baud", C.c_double), ("rolloff", C.c_double),
+                ("launch_power_w", C.c_double), ("device", C.c_int32)]
+
+
 # every symbol include/*.h declares: name -> (restype, argtypes)
 SIGNATURES = {
     "cbessfm_version": (C.c_int32, []),
@@ -104,6 +111,12 @@ SIGNATURES = {
                                            C.POINTER(C.c_double), C.POINTER(C.c_double),
                                            C.POINTER(C.c_double), C.c_int32]),
     "cbessfm_coeff_last_error": (C.c_char_p, []),
+    # include/cbessfm_rx.h
+    "cbessfm_rx_symbol_count": (C.c_int64, [C.POINTER(RxDesc)]),
+    "cbessfm_rx_symbols": (C.c_int, [C.POINTER(RxDesc), C.c_void_p, C.c_void_p, C.c_void_p]),
+    "cbessfm_rx_snr": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p,
+                                 C.POINTER(C.c_double), C.c_void_p]),
+    "cbessfm_rx_last_error": (C.c_char_p, []),
 }
 
 _lib = None

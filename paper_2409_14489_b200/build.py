@@ -22,7 +22,8 @@ HEADERS = [CSRC / "cbessfm_kernel.cuh", CSRC / "cbessfm_launch.cuh",
            PKG.parent / "include" / "cbessfm.h",
            PKG.parent / "include" / "cbessfm_peaks.h",
            PKG.parent / "include" / "cbessfm_ssfm.h",
-           PKG.parent / "include" / "cbessfm_coeff.h"]
+           PKG.parent / "include" / "cbessfm_coeff.h",
+           PKG.parent / "include" / "cbessfm_rx.h", CSRC / "cbessfm_fft4.cuh"]
 REALS = ("float", "double")
 SUBBANDS = tuple(range(1, 10))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -89,6 +90,8 @@ def build(jobs: int | None = None, verbose: bool = False, profile: bool = False,
                   BUILD / "ssfm.log"))
     tasks.append((CSRC / "cbessfm_coeff.cu", BUILD / "coeff.o", [], HEADERS,
                   BUILD / "coeff.log"))
+    tasks.append((CSRC / "cbessfm_rx.cu", BUILD / "rx.o", [], HEADERS,
+                  BUILD / "rx.log"))
     with ThreadPoolExecutor(jobs) as ex:
         results = list(ex.map(_compile, tasks))
     errors = [e for _, e in results if e]
