@@ -50,6 +50,7 @@ struct Params {
   int n1, n2;              // column length, row length
   int rows, cols;          // rows per row tile, columns per column tile
   int lg_n2, lg_rows, lg_cols;
+  int buf_elems;           // elements of each of the two tile buffers
   const Cx<R>* tw_hi;      // W_n^(h << lo_bits)
   const Cx<R>* tw_lo;      // W_n^l, l < 2^lo_bits
   int lo_bits;
@@ -65,96 +66,73 @@ struct Params {
   const Cx<R>* noise;      // [n_spans][batch][2][n] or null
 };
 
-// One Stockham pass of radix RAD and stride ns over M sequences of length L
-// (sequence m at buf + m * seq_stride(L), padded): inputs j + r L/RAD, twiddled by
-// W_(RAD ns)^(r k), k = j mod ns, outputs (j/ns) ns RAD + k + r ns.
-// Reads all of the thread's butterflies before a barrier, then writes.
-// L and ns are compile-time: every pass is specialised (no runtime shifts,
-// the butterfly arrays stay in registers).
+// One Stockham pass of radix RAD and stride NS over M sequences of length L
+// (sequence m at m * seq_stride(L), padded), from src to dst: inputs
+// j + r L/RAD, twiddled by W_(RAD NS)^(r k), k = j mod NS, outputs
+// (j/NS) NS RAD + k + r NS. Ping-pong buffers: one barrier per pass and no
+// value lives across it (a butterfly kept in registers over a barrier is
+// what ptxas spills once the tile loop hoists its addressing).
 template <typename R, int RAD, bool INV, int L, int NS>
-__device__ __forceinline__ void stockham_pass(Cx<R>* buf, int M, const Cx<R>* __restrict__ twL) {
+__device__ __forceinline__ void stockham_pass(const Cx<R>* src, Cx<R>* dst, int M,
+                                              const Cx<R>* __restrict__ twL, const int* zero) {
   constexpr int LR = L / RAD, SL = seq_stride<R>(L), TSTEP = L / (RAD * NS);
-  constexpr int KMAX = (kTileElems / RAD + kThreads - 1) / kThreads;
-  const int nb = M * LR, tid = threadIdx.x;
-  Cx<R> v[KMAX][RAD];
+  // the shared zero read keeps ptxas from hoisting every pass's addressing
+  // out of the tile loop
+  const unsigned nb = M * LR;
+  for (unsigned u = threadIdx.x + *(volatile const int*)zero; u < nb; u += kThreads) {
+    const unsigned m = u / LR, j = u % LR, kk = j % NS;
+    const Cx<R>* b = src + m * SL;
+    Cx<R> v[RAD];
 #pragma unroll
-  for (int q = 0; q < KMAX; ++q) {
-    const int u = tid + q * kThreads;
-    if (u < nb) {
-      const int m = u / LR, j = u % LR, kk = j % NS;
-      const Cx<R>* b = buf + m * SL;
+    for (int r = 0; r < RAD; ++r) v[r] = b[spad<R>(j + r * LR)];
+    if (NS > 1) {
 #pragma unroll
-      for (int r = 0; r < RAD; ++r) v[q][r] = b[spad<R>(j + r * LR)];
-      if (NS > 1) {
-#pragma unroll
-        for (int r = 1; r < RAD; ++r) {
-          const Cx<R> w = ldg(twL + r * kk * TSTEP);
-          v[q][r] = INV ? cmulc(v[q][r], w) : cmul(v[q][r], w);
-        }
+      for (int r = 1; r < RAD; ++r) {
+        const Cx<R> w = ldg(twL + r * kk * TSTEP);
+        v[r] = INV ? cmulc(v[r], w) : cmul(v[r], w);
       }
     }
-  }
-  __syncthreads();
+    dft_reg<R, RAD, INV>(v);  // in place, outputs in bit-reversed order
+    Cx<R>* o = dst + m * SL;
+    const int base = (j / NS) * NS * RAD + kk;
 #pragma unroll
-  for (int q = 0; q < KMAX; ++q) {
-    const int u = tid + q * kThreads;
-    if (u < nb) {
-      const int m = u / LR, j = u % LR, kk = j % NS;
-      Cx<R>* b = buf + m * SL;
-      const int o = (j / NS) * NS * RAD + kk;
-      if (RAD == 2) {
-        b[spad<R>(o)] = v[q][0] + v[q][1];
-        b[spad<R>(o + NS)] = v[q][0] - v[q][1];
-      } else {
-        const Cx<R> t0 = v[q][0] + v[q][2], t1 = v[q][0] - v[q][2];
-        const Cx<R> t2 = v[q][1] + v[q][3], d = v[q][1] - v[q][3];
-        const Cx<R> t3 = INV ? mk(-d.y, d.x) : mk(d.y, -d.x);  // +-j (a1 - a3)
-        b[spad<R>(o)] = t0 + t2;
-        b[spad<R>(o + NS)] = t1 + t3;
-        b[spad<R>(o + 2 * NS)] = t0 - t2;
-        b[spad<R>(o + 3 * NS)] = t1 - t3;
-      }
-    }
+    for (int r = 0; r < RAD; ++r) o[spad<R>(base + r * NS)] = v[bitrev<RAD>(r)];
   }
   __syncthreads();
 }
 
-template <typename R, bool INV, int L, int NS>
-__device__ __forceinline__ void radix4_passes(Cx<R>* buf, int M, const Cx<R>* twL) {
+template <typename R, bool INV, int L, int NS, int PASS>
+__device__ __forceinline__ void radix4_passes(Cx<R>* a, Cx<R>* b, int M, const Cx<R>* twL,
+                                              const int* z) {
   if constexpr (NS < L) {
-    stockham_pass<R, 4, INV, L, NS>(buf, M, twL);
-    radix4_passes<R, INV, L, NS * 4>(buf, M, twL);
+    if constexpr (PASS & 1)
+      stockham_pass<R, 4, INV, L, NS>(b, a, M, twL, z);
+    else
+      stockham_pass<R, 4, INV, L, NS>(a, b, M, twL, z);
+    radix4_passes<R, INV, L, NS * 4, PASS + 1>(a, b, M, twL, z);
   }
 }
 
-// Unnormalised DFT (INV: conjugate kernel) of M sequences of length L.
+// Passes of an FFT of length L: one radix-2 pass when log2 L is odd, then
+// radix-4 passes.
+template <int L>
+constexpr int fft_passes() {
+  return (__builtin_ctz(L) & 1) + __builtin_ctz(L) / 2;
+}
+
+// Unnormalised DFT (INV: conjugate kernel) of M sequences of length L that
+// start in buffer a; returns the buffer holding the result (a after an even
+// number of passes, b after an odd one).
 template <typename R, bool INV, int L>
-__device__ __noinline__ void cta_fft_l(Cx<R>* buf, int M, const Cx<R>* __restrict__ twL) {
-  constexpr int LG = __builtin_ctz(L);
-  if constexpr (LG & 1) {
-    stockham_pass<R, 2, INV, L, 1>(buf, M, twL);
-    radix4_passes<R, INV, L, 2>(buf, M, twL);
+__device__ __forceinline__ Cx<R>* cta_fft_l(Cx<R>* a, Cx<R>* b, int M,
+                                            const Cx<R>* __restrict__ twL, const int* z) {
+  if constexpr (__builtin_ctz(L) & 1) {
+    stockham_pass<R, 2, INV, L, 1>(a, b, M, twL, z);
+    radix4_passes<R, INV, L, 2, 1>(a, b, M, twL, z);
   } else {
-    radix4_passes<R, INV, L, 1>(buf, M, twL);
+    radix4_passes<R, INV, L, 1, 0>(a, b, M, twL, z);
   }
-}
-
-template <typename R, bool INV>
-__device__ __forceinline__ void cta_fft(Cx<R>* buf, int M, int L, const Cx<R>* twL) {
-  switch (L) {
-    case 2: cta_fft_l<R, INV, 2>(buf, M, twL); break;
-    case 4: cta_fft_l<R, INV, 4>(buf, M, twL); break;
-    case 8: cta_fft_l<R, INV, 8>(buf, M, twL); break;
-    case 16: cta_fft_l<R, INV, 16>(buf, M, twL); break;
-    case 32: cta_fft_l<R, INV, 32>(buf, M, twL); break;
-    case 64: cta_fft_l<R, INV, 64>(buf, M, twL); break;
-    case 128: cta_fft_l<R, INV, 128>(buf, M, twL); break;
-    case 256: cta_fft_l<R, INV, 256>(buf, M, twL); break;
-    case 512: cta_fft_l<R, INV, 512>(buf, M, twL); break;
-    case 1024: cta_fft_l<R, INV, 1024>(buf, M, twL); break;
-    case 2048: cta_fft_l<R, INV, 2048>(buf, M, twL); break;
-    default: break;  // L == 1: identity
-  }
+  return (fft_passes<L>() & 1) ? b : a;
 }
 
 template <typename R>
@@ -164,29 +142,37 @@ __device__ __forceinline__ Cx<R> tw_n(const Params<R>& p, int64_t e) {
 
 // Row phase: FFT_n2, the spectral half steps, IFFT_n2 (channel.py:206, :211);
 // fwd / inv select the transforms (a plain four-step FFT or IFFT uses one).
-template <typename R>
-__device__ void row_phase(const Params<R>& p, Cx<R>* buf, const Cx<R>* ha, const Cx<R>* hb,
+// N2 == p.n2 at compile time (kernels are instantiated per transform length).
+template <typename R, int N2>
+__device__ __noinline__ void row_phase(const Params<R>& p, Cx<R>* buf, const Cx<R>* ha, const Cx<R>* hb,
                           bool fwd = true, bool inv = true) {
+  __shared__ int s_zero;
+  if (threadIdx.x == 0) s_zero = 0;
+  __syncthreads();
   const int per_wave = p.n1 >> p.lg_rows;
   const int tile_len = p.rows << p.lg_n2;  // per polarisation
   const int SL = seq_stride<R>(p.n2);
+  Cx<R>* const bufA = buf;
+  Cx<R>* const bufB = buf + p.buf_elems;
+  Cx<R>* cur = bufA;
   // element e of the tile: pol, row r, column c -> sequence pol*rows + r
   auto at = [&](int e) {
-    return buf + (e >> p.lg_n2) * SL + spad<R>(e & (p.n2 - 1));
+    return cur + (e >> p.lg_n2) * SL + spad<R>(e & (p.n2 - 1));
   };
   for (int t = blockIdx.x; t < p.batch * per_wave; t += gridDim.x) {
     const int b = t / per_wave;
     const int64_t r0 = (int64_t)(t % per_wave) << p.lg_rows;
     Cx<R>* base = p.data + (int64_t)b * 2 * p.n + (r0 << p.lg_n2);
-    for (int e = threadIdx.x; e < 2 * tile_len; e += kThreads) {
+    cur = bufA;
+    for (int e = threadIdx.x + *(volatile int*)&s_zero; e < 2 * tile_len; e += kThreads) {
       const int pol = e >= tile_len, i = e - pol * tile_len;
       *at(e) = base[pol * p.n + i];
     }
     __syncthreads();
-    if (fwd) cta_fft<R, false>(buf, 2 * p.rows, p.n2, p.tw2);
+    if (fwd) cur = cta_fft_l<R, false, N2>(cur, cur == bufA ? bufB : bufA, 2 * p.rows, p.tw2, &s_zero);
     if (ha || hb) {
       const int64_t h0 = r0 << p.lg_n2;
-      for (int e = threadIdx.x; e < 2 * tile_len; e += kThreads) {
+      for (int e = threadIdx.x + *(volatile int*)&s_zero; e < 2 * tile_len; e += kThreads) {
         const int pol = e >= tile_len, i = e - pol * tile_len;
         Cx<R> v = *at(e);
         if (ha) v = cmul(v, ldg(ha + h0 + i));
@@ -195,8 +181,8 @@ __device__ void row_phase(const Params<R>& p, Cx<R>* buf, const Cx<R>* ha, const
       }
       __syncthreads();
     }
-    if (inv) cta_fft<R, true>(buf, 2 * p.rows, p.n2, p.tw2);
-    for (int e = threadIdx.x; e < 2 * tile_len; e += kThreads) {
+    if (inv) cur = cta_fft_l<R, true, N2>(cur, cur == bufA ? bufB : bufA, 2 * p.rows, p.tw2, &s_zero);
+    for (int e = threadIdx.x + *(volatile int*)&s_zero; e < 2 * tile_len; e += kThreads) {
       const int pol = e >= tile_len, i = e - pol * tile_len;
       base[pol * p.n + i] = *at(e);
     }
@@ -209,32 +195,38 @@ enum Mid { kNone = 0, kNonlinear = 1, kSpanEnd = 2 };
 // Column phase. inv_in: conj twiddle + IFFT_n1 + 1/n (completes the
 // inverse transform); then the time-domain operation; fwd_out: FFT_n1 +
 // twiddle (starts the next forward transform).
-template <typename R>
-__device__ void col_phase(const Params<R>& p, Cx<R>* buf, bool inv_in, int mid, R nl,
+template <typename R, int N1>
+__device__ __noinline__ void col_phase(const Params<R>& p, Cx<R>* buf, bool inv_in, int mid, R nl,
                           const Cx<R>* noise, bool pre_div, bool fwd_out) {
+  __shared__ int s_zero;
+  if (threadIdx.x == 0) s_zero = 0;
+  __syncthreads();
   const int per_wave = p.n2 >> p.lg_cols;
   const int seq = p.n1;                  // sequence length
   const int tile_len = p.cols * seq;     // per polarisation
   const int SL = seq_stride<R>(seq);
   const R inv_n = (R)1 / (R)p.n;         // exact: n is a power of two
+  Cx<R>* const bufA = buf;
+  Cx<R>* const bufB = buf + p.buf_elems;
   for (int t = blockIdx.x; t < p.batch * per_wave; t += gridDim.x) {
     const int b = t / per_wave;
     const int c0 = (t % per_wave) << p.lg_cols;
+    Cx<R>* cur = bufA;
     Cx<R>* base = p.data + (int64_t)b * 2 * p.n + c0;
     // element e: pol, row k1, column c (fastest) -> sequence pol*cols + c
-    for (int e = threadIdx.x; e < 2 * tile_len; e += kThreads) {
+    for (int e = threadIdx.x + *(volatile int*)&s_zero; e < 2 * tile_len; e += kThreads) {
       const int pol = e >= tile_len, i = e - pol * tile_len;
       const int k1 = i >> p.lg_cols, c = i & (p.cols - 1);
       Cx<R> v = base[pol * p.n + ((int64_t)k1 << p.lg_n2) + c];
       if (inv_in) v = cmulc(v, tw_n(p, (int64_t)(c0 + c) * k1));
-      buf[(pol * p.cols + c) * SL + spad<R>(k1)] = v;
+      cur[(pol * p.cols + c) * SL + spad<R>(k1)] = v;
     }
     __syncthreads();
-    if (inv_in) cta_fft<R, true>(buf, 2 * p.cols, seq, p.tw1);
-    for (int e = threadIdx.x; e < tile_len; e += kThreads) {
+    if (inv_in) cur = cta_fft_l<R, true, N1>(cur, bufB, 2 * p.cols, p.tw1, &s_zero);
+    for (int e = threadIdx.x + *(volatile int*)&s_zero; e < tile_len; e += kThreads) {
       const int c = e / seq, j1 = e & (seq - 1);
-      Cx<R>* px = buf + c * SL + spad<R>(j1);
-      Cx<R>* py = buf + (p.cols + c) * SL + spad<R>(j1);
+      Cx<R>* px = cur + c * SL + spad<R>(j1);
+      Cx<R>* py = cur + (p.cols + c) * SL + spad<R>(j1);
       Cx<R> x = *px, y = *py;
       if (inv_in) {
         x = scale(x, inv_n);
@@ -266,11 +258,11 @@ __device__ void col_phase(const Params<R>& p, Cx<R>* buf, bool inv_in, int mid, 
       *py = y;
     }
     __syncthreads();
-    if (fwd_out) cta_fft<R, false>(buf, 2 * p.cols, seq, p.tw1);
-    for (int e = threadIdx.x; e < 2 * tile_len; e += kThreads) {
+    if (fwd_out) cur = cta_fft_l<R, false, N1>(cur, cur == bufA ? bufB : bufA, 2 * p.cols, p.tw1, &s_zero);
+    for (int e = threadIdx.x + *(volatile int*)&s_zero; e < 2 * tile_len; e += kThreads) {
       const int pol = e >= tile_len, i = e - pol * tile_len;
       const int k1 = i >> p.lg_cols, c = i & (p.cols - 1);
-      Cx<R> v = buf[(pol * p.cols + c) * SL + spad<R>(k1)];
+      Cx<R> v = cur[(pol * p.cols + c) * SL + spad<R>(k1)];
       if (fwd_out) v = cmul(v, tw_n(p, (int64_t)(c0 + c) * k1));
       base[pol * p.n + ((int64_t)k1 << p.lg_n2) + c] = v;
     }
@@ -283,6 +275,7 @@ __device__ void col_phase(const Params<R>& p, Cx<R>* buf, bool inv_in, int mid, 
 
 struct Geo {
   int n1, n2, rows, cols;
+  int buf_elems;  // elements per tile buffer (two buffers: Stockham ping-pong)
   size_t smem;
 };
 
@@ -302,7 +295,8 @@ inline Geo geometry(int64_t n, int batch, size_t esz, int target_tiles) {
     g.cols *= 2;
   const int ps = esz == 16 ? 4 : 3;
   auto stride = [&](int L) { return L + (L >> ps) + 1; };
-  g.smem = esz * (size_t)std::max(2 * g.rows * stride(g.n2), 2 * g.cols * stride(g.n1));
+  g.buf_elems = std::max(2 * g.rows * stride(g.n2), 2 * g.cols * stride(g.n1));
+  g.smem = 2 * esz * (size_t)g.buf_elems;
   return g;
 }
 
@@ -362,6 +356,7 @@ struct Fft4Tables {
     p->lg_n2 = __builtin_ctz(g.n2);
     p->lg_rows = __builtin_ctz(g.rows);
     p->lg_cols = __builtin_ctz(g.cols);
+    p->buf_elems = g.buf_elems;
     p->tw_hi = reinterpret_cast<const Cx<R>*>(dhi);
     p->tw_lo = reinterpret_cast<const Cx<R>*>(dlo);
     p->lo_bits = lo_bits;
@@ -375,6 +370,24 @@ struct Fft4Tables {
     dhi = dlo = d1 = d2 = nullptr;
   }
 };
+
+// Compile-time four-step split of n = 2^LG (same rule as geometry()).
+template <int LG>
+struct Split {
+  static constexpr int N2 = 1 << ((LG + 1) / 2);
+  static constexpr int N1 = 1 << (LG - (LG + 1) / 2);
+};
+
+// Kernel pointer for LG = 1..kMaxLog2N: F<LG>::get() per length.
+template <template <int> class F, int LG = 1>
+inline auto dispatch_lg(int lg) -> decltype(F<1>::get()) {
+  if constexpr (LG > kMaxLog2N) {
+    return nullptr;
+  } else {
+    if (lg == LG) return F<LG>::get();
+    return dispatch_lg<F, LG + 1>(lg);
+  }
+}
 
 }  // namespace ssfm
 }  // namespace cbessfm

@@ -25,21 +25,36 @@ namespace cbessfm {
 namespace rx {
 using namespace ssfm;
 
-template <typename R>
+template <typename R, int LG>
 __global__ void __launch_bounds__(kThreads, 1024 / kThreads)
-    col_kernel(ssfm::Params<R> p, int inv_in, int fwd_out, int pre_div) {
+    col_kernel(const __grid_constant__ ssfm::Params<R> p, int inv_in, int fwd_out, int pre_div) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  col_phase<R>(p, reinterpret_cast<Cx<R>*>(smem_raw), inv_in != 0, kNone, (R)0, nullptr,
-               pre_div != 0, fwd_out != 0);
+  col_phase<R, Split<LG>::N1>(p, reinterpret_cast<Cx<R>*>(smem_raw), inv_in != 0, kNone, (R)0,
+                              nullptr, pre_div != 0, fwd_out != 0);
+}
+
+template <typename R, int LG>
+__global__ void __launch_bounds__(kThreads, 1024 / kThreads)
+    row_kernel(const __grid_constant__ ssfm::Params<R> p, int fwd, int inv) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  row_phase<R, Split<LG>::N2>(p, reinterpret_cast<Cx<R>*>(smem_raw), (const Cx<R>*)nullptr,
+                              (const Cx<R>*)nullptr, fwd != 0, inv != 0);
 }
 
 template <typename R>
-__global__ void __launch_bounds__(kThreads, 1024 / kThreads)
-    row_kernel(ssfm::Params<R> p, int fwd, int inv) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  row_phase<R>(p, reinterpret_cast<Cx<R>*>(smem_raw), (const Cx<R>*)nullptr,
-               (const Cx<R>*)nullptr, fwd != 0, inv != 0);
-}
+struct ColFor {
+  template <int LG>
+  struct At {
+    static const void* get() { return (const void*)col_kernel<R, LG>; }
+  };
+};
+template <typename R>
+struct RowFor {
+  template <int LG>
+  struct At {
+    static const void* get() { return (const void*)row_kernel<R, LG>; }
+  };
+};
 
 struct Grid {
   int64_t n;       // length
@@ -206,22 +221,27 @@ cbessfm_status cuda_fail(cudaError_t e, const char* what) {
 
 template <typename R>
 cudaError_t launch_transform(ssfm::Params<R>& p, const Geo& g, bool inverse, bool div, cudaStream_t st) {
-  auto ck = col_kernel<R>;
-  auto rk = row_kernel<R>;
+  const int lg = __builtin_ctzll(p.n);
+  const void* ck = dispatch_lg<ColFor<R>::template At>(lg);
+  const void* rk = dispatch_lg<RowFor<R>::template At>(lg);
+  if (!ck || !rk) return cudaErrorInvalidValue;
   cudaError_t e;
   if ((e = cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem)) ||
       (e = cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem)))
     return e;
   const unsigned col_tiles = (unsigned)((int64_t)p.batch * g.n2 / g.cols);
   const unsigned row_tiles = (unsigned)((int64_t)p.batch * g.n1 / g.rows);
+  int one = 1, zero = 0, dv = div ? 1 : 0;
+  void* cfwd[] = {&p, &zero, &one, &zero};
+  void* rfwd[] = {&p, &one, &zero};
+  void* rinv[] = {&p, &zero, &one};
+  void* cinv[] = {&p, &one, &zero, &dv};
   if (!inverse) {
-    ck<<<col_tiles, kThreads, g.smem, st>>>(p, 0, 1, 0);
-    rk<<<row_tiles, kThreads, g.smem, st>>>(p, 1, 0);
-  } else {
-    rk<<<row_tiles, kThreads, g.smem, st>>>(p, 0, 1);
-    ck<<<col_tiles, kThreads, g.smem, st>>>(p, 1, 0, div ? 1 : 0);
+    if ((e = cudaLaunchKernel(ck, dim3(col_tiles), dim3(kThreads), cfwd, g.smem, st))) return e;
+    return cudaLaunchKernel(rk, dim3(row_tiles), dim3(kThreads), rfwd, g.smem, st);
   }
-  return cudaGetLastError();
+  if ((e = cudaLaunchKernel(rk, dim3(row_tiles), dim3(kThreads), rinv, g.smem, st))) return e;
+  return cudaLaunchKernel(ck, dim3(col_tiles), dim3(kThreads), cinv, g.smem, st);
 }
 
 template <typename R>

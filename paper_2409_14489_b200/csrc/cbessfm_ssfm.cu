@@ -34,31 +34,40 @@ namespace cbessfm {
 namespace ssfm {
 namespace cg = cooperative_groups;
 
-template <typename R>
-__global__ void __launch_bounds__(kThreads, 1024 / kThreads) ssfm_kernel(Params<R> p) {
+template <typename R, int LG>
+__global__ void __launch_bounds__(kThreads, 1024 / kThreads) ssfm_kernel(const __grid_constant__ Params<R> p) {
+  constexpr int N1 = Split<LG>::N1, N2 = Split<LG>::N2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Cx<R>* buf = reinterpret_cast<Cx<R>*>(smem_raw);
   cg::grid_group grid = cg::this_grid();
   const size_t tab = (size_t)p.n;
   for (int span = 0; span < p.n_spans; ++span) {
     if (span == 0)  // spec = fft(field) (channel.py:206), after / g when backward
-      col_phase<R>(p, buf, false, kNone, (R)0, nullptr, p.backward != 0, true);
+      col_phase<R, N1>(p, buf, false, kNone, (R)0, nullptr, p.backward != 0, true);
     for (int s = 0; s < p.k; ++s) {
       grid.sync();
       const Cx<R>* ha = s ? p.half + tab * p.step_table[s - 1] : nullptr;
-      row_phase<R>(p, buf, ha, p.half + tab * p.step_table[s]);
+      row_phase<R, N2>(p, buf, ha, p.half + tab * p.step_table[s]);
       grid.sync();
-      col_phase<R>(p, buf, true, kNonlinear, p.nl_coef[s], nullptr, false, true);
+      col_phase<R, N1>(p, buf, true, kNonlinear, p.nl_coef[s], nullptr, false, true);
     }
     grid.sync();
-    row_phase<R>(p, buf, p.half + tab * p.step_table[p.k - 1], (const Cx<R>*)nullptr);
+    row_phase<R, N2>(p, buf, p.half + tab * p.step_table[p.k - 1], (const Cx<R>*)nullptr);
     grid.sync();
     const bool more = span + 1 < p.n_spans;
     const Cx<R>* nz = p.noise ? p.noise + (int64_t)span * p.batch * 2 * p.n : nullptr;
-    col_phase<R>(p, buf, true, kSpanEnd, (R)0, nz, more && p.backward, more);
+    col_phase<R, N1>(p, buf, true, kSpanEnd, (R)0, nz, more && p.backward, more);
     if (more) grid.sync();
   }
 }
+
+template <typename R>
+struct KernelFor {
+  template <int LG>
+  struct At {
+    static const void* get() { return (const void*)ssfm_kernel<R, LG>; }
+  };
+};
 
 thread_local std::string g_err;
 
@@ -73,7 +82,8 @@ cbessfm_status run(const cbessfm_ssfm_desc* d, void* data, const void* noise, cu
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->device);
   const Geo g = geometry(n, d->batch, sizeof(Cx<R>), 2 * sms);
-  auto kern = ssfm_kernel<R>;
+  const void* kern = dispatch_lg<KernelFor<R>::template At>(__builtin_ctzll(n));
+  if (!kern) return fail(CBESSFM_ERR_UNSUPPORTED, "no propagator kernel for this length");
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)g.smem);
   if (e != cudaSuccess) return fail(CBESSFM_ERR_CUDA, cudaGetErrorString(e));
@@ -118,7 +128,7 @@ cbessfm_status run(const cbessfm_ssfm_desc* d, void* data, const void* noise, cu
   p.gain = (R)d->gain;
   p.noise = reinterpret_cast<const Cx<R>*>(noise);
   void* args[] = {&p};
-  e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kThreads), args, g.smem, st);
+  e = cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kThreads), args, g.smem, st);
   for (void* ptr : {dh, ds, dn}) cudaFreeAsync(ptr, st);
   tw.release(st);
   // the host staging vectors are read by the async copies
