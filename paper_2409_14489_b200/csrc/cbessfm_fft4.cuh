@@ -113,11 +113,30 @@ __device__ __forceinline__ void radix4_passes(Cx<R>* a, Cx<R>* b, int M, const C
   }
 }
 
-// Passes of an FFT of length L: one radix-2 pass when log2 L is odd, then
-// radix-4 passes.
-template <int L>
+template <typename R, bool INV, int L, int NS, int PASS>
+__device__ __forceinline__ void radix8_passes(Cx<R>* a, Cx<R>* b, int M, const Cx<R>* twL,
+                                              const int* z) {
+  if constexpr (NS < L) {
+    if constexpr (PASS & 1)
+      stockham_pass<R, 8, INV, L, NS>(b, a, M, twL, z);
+    else
+      stockham_pass<R, 8, INV, L, NS>(a, b, M, twL, z);
+    radix8_passes<R, INV, L, NS * 8, PASS + 1>(a, b, M, twL, z);
+  }
+}
+
+// FP32 tiles run radix-8 passes (8 complex values fit the 64-register
+// budget), FP64 tiles radix-4 (radix-8 doubles would spill); the leftover
+// factor of L leads.
+template <typename R>
+constexpr int tile_radix_log() {
+  return sizeof(R) == 4 ? 3 : 2;
+}
+
+template <typename R, int L>
 constexpr int fft_passes() {
-  return (__builtin_ctz(L) & 1) + __builtin_ctz(L) / 2;
+  constexpr int B = tile_radix_log<R>(), LG = __builtin_ctz(L);
+  return (LG % B != 0) + LG / B;
 }
 
 // Unnormalised DFT (INV: conjugate kernel) of M sequences of length L that
@@ -126,13 +145,14 @@ constexpr int fft_passes() {
 template <typename R, bool INV, int L>
 __device__ __forceinline__ Cx<R>* cta_fft_l(Cx<R>* a, Cx<R>* b, int M,
                                             const Cx<R>* __restrict__ twL, const int* z) {
-  if constexpr (__builtin_ctz(L) & 1) {
-    stockham_pass<R, 2, INV, L, 1>(a, b, M, twL, z);
-    radix4_passes<R, INV, L, 2, 1>(a, b, M, twL, z);
-  } else {
-    radix4_passes<R, INV, L, 1, 0>(a, b, M, twL, z);
-  }
-  return (fft_passes<L>() & 1) ? b : a;
+  constexpr int B = tile_radix_log<R>(), REM = __builtin_ctz(L) % B;
+  if constexpr (REM != 0) stockham_pass<R, (1 << REM), INV, L, 1>(a, b, M, twL, z);
+  constexpr int NS0 = REM ? (1 << REM) : 1, P0 = REM ? 1 : 0;
+  if constexpr (B == 3)
+    radix8_passes<R, INV, L, NS0, P0>(a, b, M, twL, z);
+  else
+    radix4_passes<R, INV, L, NS0, P0>(a, b, M, twL, z);
+  return (fft_passes<R, L>() & 1) ? b : a;
 }
 
 template <typename R>

@@ -27,7 +27,7 @@ def main():
     for dt, ct in (("c128", torch.complex128), ("c64", torch.complex64)):
         x = torch.from_numpy(field).cuda().to(ct).contiguous()
         tx = None
-        for _ in range(3):
+        for _ in range(20):                    # warm-up (lazy module loads, pool)
             sym = rxm.channel_symbols_tensor(x, rate, Wdm, Wdm.channel_freqs, 100e9)
             tx = sym.clone() if tx is None else tx
             rxm.snr_tensor(sym, tx)
