@@ -256,3 +256,47 @@ def test_ssfm_four_step_geometry(n):
         _native.ssfm_info(_native.C128, 3 * n, 1, -1)
     with pytest.raises(ValueError):
         _native.ssfm_info(_native.C128, 1 << 23, 1, -1)   # above the 2^22 limit
+
+
+def test_span_step_sizes_mirror_the_oracle():
+    # channel.span_step_sizes (host) == oracle restatement of channel.py:114-136
+    from oracle import ssfm_oracle as so
+    from paper_2409_14489_b200 import channel as ch
+    from paper_2409_14489_b200.config import LinkConfig
+    lk = LinkConfig(num_spans=2, span_length_km=80.0)
+    for sim, kw in ((ch.SimSettings(step_km=0.8), dict(step_km=0.8)),
+                    (ch.SimSettings(max_phase_rad=2e-3, max_step_km=4.0),
+                     dict(max_phase_rad=2e-3, max_step_km=4.0))):
+        got = ch.span_step_sizes(lk, sim, 3e-3)
+        ref = so.span_steps(80.0, lk.alpha_np_km, lk.gamma_w_km, 3e-3, **kw)
+        np.testing.assert_array_equal(got, ref)
+        assert abs(got.sum() - 80.0) < 1e-9
+
+
+def test_propagator_step_tables_follow_run_spans_order():
+    # first-use table order, reversed and negated for the inverse (channel.py:194-205)
+    from paper_2409_14489_b200 import channel as ch
+    from paper_2409_14489_b200.config import LinkConfig
+    lk = LinkConfig(num_spans=1, span_length_km=80.0)
+    steps = np.array([10.0, 30.0, 10.0, 30.0])
+    tab, idx, nl = ch._step_tables(64, 64e9, lk, steps, inverse=False)
+    assert tab.shape == (2, 64) and list(idx) == [0, 1, 0, 1]
+    tabi, idxi, nli = ch._step_tables(64, 64e9, lk, steps, inverse=True)
+    assert list(idxi) == [0, 1, 0, 1] and np.allclose(nli, -nl[::-1])
+    half, leff = ch.gvd_half_operator(64, 64e9, lk, 30.0, inverse=True)
+    np.testing.assert_array_equal(tabi[0], half)
+
+
+@pytest.mark.parametrize("name", ["cfg1_nsb1", "cfg2_nsb5", "cfg1_nsb2_frac", "cfg4_nsb5_st50"])
+def test_coefficient_set_metadata_matches_reference(name):
+    # geometry fingerprint, phase norm and step scales of the host-side set
+    # assembly (dbp.py:272-289, kernel.py:456-465) equal the reference's
+    from paper_2409_14489_b200 import coefficients as cf
+    g = golden(name)
+    taps = {h: np.zeros_like(c) for h, c in g.coeffs.coeffs.items()}
+    s = cf._assemble_set(g.cfg, g.wave.sample_rate, g.coeffs.reference_power_w, taps)
+    assert s.geometry_hash == g.coeffs.geometry_hash
+    assert s.phase_norm_rad == g.coeffs.phase_norm_rad
+    np.testing.assert_array_equal(s.step_scales, g.coeffs.step_scales)
+    assert cf.coefficient_memory(0, g.cfg.step_geometry(), 1.0, g.wave.sample_rate,
+                                 g.cfg.n_subbands, safety=1.5) >= 1
