@@ -29,6 +29,33 @@ _DTYPES = {"c64": _native.C64, "complex64": _native.C64,
 
 _plan_cache: "OrderedDict[tuple, _native.NativePlan]" = OrderedDict()
 _plan_lock = threading.Lock()
+
+# pinned host staging for run_dbp, one pair per (device, dtype, n); a call
+# that finds its pair busy (another thread) allocates a private one
+_staging: dict = {}
+_staging_lock = threading.Lock()
+
+
+class _staging_buffers:
+    def __init__(self, device, cdt, n):
+        self.key = (device, cdt, n)
+        self.own = None
+
+    def __enter__(self):
+        torch = _torch()
+        with _staging_lock:
+            pair = _staging.pop(self.key, None)
+        if pair is None:
+            pair = tuple(torch.empty((1, 2, self.key[2]), dtype=self.key[1]).pin_memory()
+                         for _ in range(2))
+        self.own = pair
+        return pair
+
+    def __exit__(self, *exc):
+        with _staging_lock:
+            if self.key not in _staging and len(_staging) < 8:
+                _staging[self.key] = self.own
+        return False
 _PLAN_CACHE_SIZE = 32
 
 
@@ -250,14 +277,22 @@ def run_dbp(w, cfg, coeffs=None, counter=None, *, dtype: str = "c128",
         record_time_domain_blocks(counter, cfg.block_size, cfg.n_steps, taps,
                                   cfg.variant == "EDC", n_blocks)
     cdt = torch.complex64 if dtype in ("c64", "complex64") else torch.complex128
-    host = torch.from_numpy(np.stack([np.asarray(w.x), np.asarray(w.y)])[None])
-    dev = torch.device("cuda", plan.device)
-    x = host.to(dev, non_blocking=False).to(cdt)
-    out = torch.empty_like(x)
-    with torch.cuda.device(dev):
-        launch(plan, x, out)
-        res = out[0].to(torch.complex128).cpu().numpy()
-    return type(w)(res[0], res[1], w.sample_rate, w.center_freq)
+    # host -> pinned staging (dtype cast in the same pass) -> the native
+    # pipelined H2D / kernel / D2H entry -> fresh host arrays
+    with _staging_buffers(plan.device, cdt, n) as (pin_in, pin_out):
+        np_in = pin_in.numpy()
+        np.copyto(np_in[0, 0], np.asarray(w.x), casting="same_kind")
+        np.copyto(np_in[0, 1], np.asarray(w.y), casting="same_kind")
+        dev = torch.device("cuda", plan.device)
+        with torch.cuda.device(dev):
+            stream = torch.cuda.current_stream(dev)
+            plan.run_host(in_ptr=pin_in.data_ptr(), out_ptr=pin_out.data_ptr(), n=n, batch=1,
+                          chunks=8, stream=stream.cuda_stream)
+            stream.synchronize()
+        res = pin_out.numpy()[0]
+        x_out = res[0].astype(np.complex128)      # copies: the result owns its memory
+        y_out = res[1].astype(np.complex128)
+    return type(w)(x_out, y_out, w.sample_rate, w.center_freq)
 
 
 def _sets_plan(cfg, rate: float, coeff_sets, dtype: str, device: int):
