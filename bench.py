@@ -384,7 +384,7 @@ def main():
         inflight = int(os.environ.get("BENCH_E2E_INFLIGHT", "2"))
         hx = x.cpu().pin_memory()
         houts = [torch.empty_like(hx).pin_memory() for _ in range(inflight)]
-        sides = [torch.cuda.Stream(cdev) for _ in range(inflight)]
+        sides = [torch.cuda.Stream(dev) for _ in range(inflight)]
 
         def e2e_steps(k):
             start = torch.cuda.Event()
