@@ -382,6 +382,7 @@ def main():
         # kernel tail and D2H; every step still copies its whole input in
         # and its whole result out
         inflight = int(os.environ.get("BENCH_E2E_INFLIGHT", "2"))
+        chunks = int(os.environ.get("BENCH_E2E_CHUNKS", "8"))
         hx = x.cpu().pin_memory()
         houts = [torch.empty_like(hx).pin_memory() for _ in range(inflight)]
         sides = [torch.cuda.Stream(dev) for _ in range(inflight)]
@@ -392,7 +393,7 @@ def main():
             for side in sides:
                 side.wait_event(start)
             for i in range(k):
-                eng.run_host(hx, houts[i % inflight], stream=sides[i % inflight])
+                eng.run_host(hx, houts[i % inflight], stream=sides[i % inflight], chunks=chunks)
             for side in sides:
                 done = torch.cuda.Event()
                 done.record(side)
