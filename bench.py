@@ -82,10 +82,15 @@ def symbols_per_wave(wl=None):
 
 
 def config_block(args, world):
+    if getattr(args, "shard", "waveform") == "time":
+        par = (f"time shards x{world}: contiguous block ranges of one waveform, each rank "
+               "reading its N_ov/2 halos, no collective in the step loop")
+    else:
+        par = f"waveform-parallel x{world} (no collective in the step loop)"
     return {"workload": WL["text"], "baseline_config_index": WL["index"],
             "n_samples_per_pol": WL["n"], "waveforms_per_gpu": args.batch,
             "two_d_symbols_per_waveform": symbols_per_wave(),
-            "parallelism": f"waveform-parallel x{world} (no collective in the step loop)",
+            "parallelism": par,
             "l2": "flushed (256 MiB write) between timed steps"}
 
 
@@ -280,6 +285,9 @@ def main():
                     help="waveforms per GPU per step (default: the workload's)")
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS),
                     help="BASELINE config the step runs (default configs[1])")
+    ap.add_argument("--shard", default="auto", choices=("auto", "waveform", "time"),
+                    help="N>1 partitioning: whole waveforms per rank, or time shards of "
+                         "one waveform (auto: time for the configs[3] workloads)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true",
@@ -293,6 +301,10 @@ def main():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.shard == "auto":
+        args.shard = "time" if (world > 1 and WL["index"] == 3) else "waveform"
+    if args.shard == "time":
+        args.batch = 1      # configs[3]: one long waveform split in time (strong scaling)
     if args.batch is None:
         # configs[4] is a fixed batch sharded over the GPUs (strong scaling);
         # the others run one waveform per GPU (weak scaling)
@@ -333,9 +345,28 @@ def main():
     # waveforms are synthesised one at a time straight into HBM (configs[4]
     # is 64 x 2^23 samples; the host never holds the whole batch)
     x = torch.empty((args.batch, 2, WL["n"]), dtype=ct, device=dev)
+    time_shard = args.shard == "time"
     for b in range(args.batch):
-        x[b] = torch.from_numpy(gaussian_wdm(WL["n"], RATE, seed=1000 * rank + b)).to(dev)
+        seed = b if time_shard else 1000 * rank + b     # time shards cut one waveform
+        x[b] = torch.from_numpy(gaussian_wdm(WL["n"], RATE, seed=seed)).to(dev)
     out = torch.empty_like(x)
+    if time_shard:
+        # this rank's blocks [b0, b1) and its halo'd circular input slice
+        # (planner.plan_shards / BlockSchedule.input_range)
+        from paper_2409_14489_b200.distributed import shard_work
+        work = shard_work(WL["n"], cfg.block_size, cfg.overlap, 1, world, rank)
+        idx = (torch.arange(work.in_length, device=dev) + work.in_origin) % WL["n"]
+        x = x[:, :, idx].contiguous()
+        out = torch.empty((1, 2, work.out_end - work.out_begin), dtype=ct, device=dev)
+
+    def step(xx=None, oo=None):
+        xx = x if xx is None else xx
+        oo = out if oo is None else oo
+        if time_shard:
+            pb.launch(eng.plan, xx, oo, n=WL["n"], block_range=work.shard.blocks,
+                      in_origin=work.in_origin, out_origin=work.out_begin)
+        else:
+            eng.run_device(xx, oo)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -352,14 +383,14 @@ def main():
         sampler.__enter__()
         time.sleep(0.5)
     for _ in range(args.warmup):
-        eng.run_device(x, out)
+        step()
     barrier()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     for i in range(args.steps):
         flush.fill_(i & 0xFF)                    # evict the waveform from L2
         evs[i][0].record(stream)
-        eng.run_device(x, out)
+        step()
         evs[i][1].record(stream)
     barrier()
     if sampler:
@@ -370,13 +401,43 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
     per_step_ms = t_ms / args.steps
-    sym_per_step = world * args.batch * symbols_per_wave()
+    sym_per_step = (1 if time_shard else world * args.batch) * symbols_per_wave()
     value = sym_per_step / (per_step_ms * 1e-3)
 
     # end to end through the public API with pinned host buffers
     e2e = None
     big = x.numel() * x.element_size() > (4 << 30)   # configs[4]: 2 x 8.6 GB pinned
-    if not (args.no_e2e or args.profile or big):
+    if time_shard and not (args.no_e2e or args.profile):
+        # per step: H2D of this rank's halo'd slice from pinned memory, the
+        # kernel on its block range, D2H of its kept samples (max over ranks)
+        hx = x.cpu().pin_memory()
+        hout = torch.empty(out.shape, dtype=ct).pin_memory()
+        dx = torch.empty_like(x)
+        for _ in range(3):
+            dx.copy_(hx, non_blocking=True)
+            step(dx, out)
+            hout.copy_(out, non_blocking=True)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            dx.copy_(hx, non_blocking=True)
+            step(dx, out)
+            hout.copy_(out, non_blocking=True)
+        e1.record(stream)
+        barrier()
+        te = e0.elapsed_time(e1)
+        if dist is not None:
+            tt = torch.tensor([te], device=cdev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": sym_per_step / (te / args.steps * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(hx.numel() * hx.element_size()),
+               "d2h_bytes_per_step": int(hout.numel() * hout.element_size()),
+               "path": "per rank: pinned halo'd input slice H2D, cbessfm_run on its block "
+                       "range, kept samples D2H"}
+    elif not (args.no_e2e or args.profile or big):
         # a streaming receiver: two steps in flight on two streams with
         # double-buffered host outputs, so step k+1's H2D overlaps step k's
         # kernel tail and D2H; every step still copies its whole input in
@@ -423,6 +484,11 @@ def main():
     gather = None
     if dist is not None:
         flat = torch.view_as_real(out).reshape(-1).to(cdev)
+        if time_shard:      # shards differ by up to one block: pad to the largest
+            from paper_2409_14489_b200.distributed import shard_work as _sw
+            spans = [_sw(WL["n"], cfg.block_size, cfg.overlap, 1, world, r) for r in range(world)]
+            most = max(2 * 2 * (s.out_end - s.out_begin) for s in spans)
+            flat = torch.nn.functional.pad(flat, (0, most - flat.numel()))
         allg = torch.empty(world * flat.numel(), dtype=flat.dtype, device=cdev)
         for _ in range(3):
             dist.all_gather_into_tensor(allg, flat)
@@ -449,6 +515,10 @@ def main():
     rm_2d, b_2d = roofline_numbers(args.dtype)
     launch_s = per_step_ms * 1e-3                 # one kernel launch per step
     sym_launch = args.batch * symbols_per_wave()
+    if time_shard:          # this rank's share of the waveform's blocks
+        from paper_2409_14489_b200.planner import BlockSchedule
+        nb = BlockSchedule(WL["n"], cfg.block_size, cfg.overlap).n_blocks
+        sym_launch = symbols_per_wave() * (work.shard.blocks[1] - work.shard.blocks[0]) / nb
     fma_kinds = (0, 1) if args.dtype == "c64" else (2,)
     fma_peak = max(_native.fma_peak(k) for k in fma_kinds)
     achieved_rm = rm_2d * sym_launch / launch_s
@@ -476,7 +546,8 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step_ms,
             "higher_is_better": True,
-            "scaling": "strong" if WL["batch"] > 1 else "weak", "vs_baseline": None,
+            "scaling": "strong" if (WL["batch"] > 1 or time_shard) else "weak",
+            "vs_baseline": None,
             "dtype": "c64 (f32)" if args.dtype == "c64" else "c128 (f64)",
             "data": "synthetic (seeded band-limited Gaussian WDM, configs[1] grid)",
             "config": config_block(args, world), "impl": "ours",
