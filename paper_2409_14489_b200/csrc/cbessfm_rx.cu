@@ -15,7 +15,11 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/cbessfm_rx.h"
@@ -167,7 +171,7 @@ struct Plan {
   std::vector<double> g;
 };
 
-cbessfm_status plan(const cbessfm_rx_desc* d, Plan* pl) {
+cbessfm_status plan(const cbessfm_rx_desc* d, Plan* pl, bool need_g = true) {
   if (!d) return fail(CBESSFM_ERR_INVALID, "null rx description");
   if (d->n < 2 || (d->n & (d->n - 1)))
     return fail(CBESSFM_ERR_UNSUPPORTED, "the GPU receiver needs a power-of-two length");
@@ -198,6 +202,7 @@ cbessfm_status plan(const cbessfm_rx_desc* d, Plan* pl) {
   if (L < 2 || (L & (L - 1)))
     return fail(CBESSFM_ERR_UNSUPPORTED, "the GPU receiver needs a power-of-two symbol count");
   pl->L = L;
+  if (!need_g) return CBESSFM_OK;
   // sqrt(raised_cosine_spectrum(fftfreq(m, 1/rate_c))) (signals.py:186-201, :268)
   pl->g.resize(m);
   const double pass_edge = (1 - d->rolloff) * d->baud / 2, stop_edge = (1 + d->rolloff) * d->baud / 2;
@@ -244,6 +249,55 @@ cudaError_t launch_transform(ssfm::Params<R>& p, const Geo& g, bool inverse, boo
   return cudaLaunchKernel(ck, dim3(col_tiles), dim3(kThreads), cinv, g.smem, st);
 }
 
+// Twiddle tables per transform geometry and device, built once and kept
+// (a receiver is called per waveform with the same grid).
+template <typename R>
+struct CachedTables {
+  Fft4Tables<R> t;
+  ssfm::Params<R> p{};
+};
+
+template <typename R>
+cudaError_t cached_params(int64_t n, const Geo& g, int device, cudaStream_t st,
+                          ssfm::Params<R>* out) {
+  static std::mutex mu;
+  static std::map<std::tuple<int64_t, int, int, int, int>, std::unique_ptr<CachedTables<R>>> cache;
+  const auto key = std::make_tuple(n, g.n1, g.rows, g.cols, device);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    auto entry = std::make_unique<CachedTables<R>>();
+    cudaError_t e = entry->t.build(n, g, st, &entry->p);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return e;
+    it = cache.emplace(key, std::move(entry)).first;
+  }
+  *out = it->second->p;
+  return cudaSuccess;
+}
+
+// The matched-filter response on the channel grid, uploaded once per
+// (grid, pulse, device).
+cudaError_t cached_filter(const Plan& pl, const cbessfm_rx_desc* d, cudaStream_t st,
+                          const void** out) {
+  static std::mutex mu;
+  static std::map<std::tuple<int64_t, double, double, double, double, int>, void*> cache;
+  const auto key = std::make_tuple(pl.m, d->sample_rate / (double)d->n, d->baud, d->rolloff,
+                                   (double)d->n, d->device);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    void* dg = nullptr;
+    cudaError_t e = cudaMalloc(&dg, pl.g.size() * sizeof(double));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(dg, pl.g.data(), pl.g.size() * sizeof(double), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return e;
+    it = cache.emplace(key, dg).first;
+  }
+  *out = it->second;
+  return cudaSuccess;
+}
+
 template <typename R>
 cbessfm_status symbols(const cbessfm_rx_desc* d, const Plan& pl, const void* in, void* out,
                        cudaStream_t st) {
@@ -252,15 +306,16 @@ cbessfm_status symbols(const cbessfm_rx_desc* d, const Plan& pl, const void* in,
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->device);
   const Geo gs = geometry(pl.n, 1, sizeof(C), 2 * sms);
   const Geo gl = geometry(pl.L, d->n_channels, sizeof(C), 2 * sms);
-  void *spec = nullptr, *dcidx = nullptr, *dg = nullptr;
+  void *spec = nullptr, *dcidx = nullptr;
+  const void* dg = nullptr;
   cudaError_t e;
   if ((e = cudaMallocAsync(&spec, 2 * pl.n * sizeof(C), st)) ||
       (e = cudaMemcpyAsync(spec, in, 2 * pl.n * sizeof(C), cudaMemcpyDeviceToDevice, st)) ||
-      (e = upload(pl.cidx, &dcidx, st)) || (e = upload(pl.g, &dg, st)))
+      (e = upload(pl.cidx, &dcidx, st)) || (e = cached_filter(pl, d, st, &dg)))
     return cuda_fail(e, "rx staging");
   ssfm::Params<R> ps{}, pls{};
-  Fft4Tables<R> ts, tl;
-  if ((e = ts.build(pl.n, gs, st, &ps)) || (e = tl.build(pl.L, gl, st, &pls)))
+  if ((e = cached_params<R>(pl.n, gs, d->device, st, &ps)) ||
+      (e = cached_params<R>(pl.L, gl, d->device, st, &pls)))
     return cuda_fail(e, "rx twiddles");
   ps.data = reinterpret_cast<C*>(spec);
   ps.batch = 1;
@@ -278,9 +333,6 @@ cbessfm_status symbols(const cbessfm_rx_desc* d, const Plan& pl, const void* in,
   if ((e = launch_transform<R>(pls, gl, true, true, st))) return cuda_fail(e, "symbol IFFT");
   cudaFreeAsync(spec, st);
   cudaFreeAsync(dcidx, st);
-  cudaFreeAsync(dg, st);
-  ts.release(st);
-  tl.release(st);
   if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "rx");
   return CBESSFM_OK;
 }
@@ -294,7 +346,7 @@ int64_t cbessfm_rx_symbol_count(const cbessfm_rx_desc* d) {
   using namespace cbessfm::rx;
   g_err.clear();
   Plan pl;
-  if (plan(d, &pl) != CBESSFM_OK) return -1;
+  if (plan(d, &pl, false) != CBESSFM_OK) return -1;
   return pl.L;
 }
 
