@@ -88,7 +88,7 @@ __device__ __forceinline__ void stockham_pass(const Cx<R>* src, Cx<R>* dst, int 
     if (NS > 1) {
 #pragma unroll
       for (int r = 1; r < RAD; ++r) {
-        const Cx<R> w = ldg(twL + r * kk * TSTEP);
+        const Cx<R> w = twL[r * kk * TSTEP];  // staged in shared memory
         v[r] = INV ? cmulc(v[r], w) : cmul(v[r], w);
       }
     }
@@ -175,6 +175,10 @@ __device__ __noinline__ void row_phase(const Params<R>& p, Cx<R>* buf, const Cx<
   Cx<R>* const bufA = buf;
   Cx<R>* const bufB = buf + p.buf_elems;
   Cx<R>* cur = bufA;
+  // the length-n2 twiddles, staged once per phase behind the tile buffers
+  Cx<R>* const tws = buf + 2 * p.buf_elems;
+  for (int i = threadIdx.x; i < N2; i += kThreads) tws[i] = ldg(p.tw2 + i);
+  __syncthreads();
   // element e of the tile: pol, row r, column c -> sequence pol*rows + r
   auto at = [&](int e) {
     return cur + (e >> p.lg_n2) * SL + spad<R>(e & (p.n2 - 1));
@@ -189,7 +193,7 @@ __device__ __noinline__ void row_phase(const Params<R>& p, Cx<R>* buf, const Cx<
       *at(e) = base[pol * p.n + i];
     }
     __syncthreads();
-    if (fwd) cur = cta_fft_l<R, false, N2>(cur, cur == bufA ? bufB : bufA, 2 * p.rows, p.tw2, &s_zero);
+    if (fwd) cur = cta_fft_l<R, false, N2>(cur, cur == bufA ? bufB : bufA, 2 * p.rows, tws, &s_zero);
     if (ha || hb) {
       const int64_t h0 = r0 << p.lg_n2;
       for (int e = threadIdx.x + *(volatile int*)&s_zero; e < 2 * tile_len; e += kThreads) {
@@ -201,7 +205,7 @@ __device__ __noinline__ void row_phase(const Params<R>& p, Cx<R>* buf, const Cx<
       }
       __syncthreads();
     }
-    if (inv) cur = cta_fft_l<R, true, N2>(cur, cur == bufA ? bufB : bufA, 2 * p.rows, p.tw2, &s_zero);
+    if (inv) cur = cta_fft_l<R, true, N2>(cur, cur == bufA ? bufB : bufA, 2 * p.rows, tws, &s_zero);
     for (int e = threadIdx.x + *(volatile int*)&s_zero; e < 2 * tile_len; e += kThreads) {
       const int pol = e >= tile_len, i = e - pol * tile_len;
       base[pol * p.n + i] = *at(e);
@@ -228,6 +232,9 @@ __device__ __noinline__ void col_phase(const Params<R>& p, Cx<R>* buf, bool inv_
   const R inv_n = (R)1 / (R)p.n;         // exact: n is a power of two
   Cx<R>* const bufA = buf;
   Cx<R>* const bufB = buf + p.buf_elems;
+  Cx<R>* const tws = buf + 2 * p.buf_elems;  // length-n1 twiddles, staged once
+  for (int i = threadIdx.x; i < N1; i += kThreads) tws[i] = ldg(p.tw1 + i);
+  __syncthreads();
   for (int t = blockIdx.x; t < p.batch * per_wave; t += gridDim.x) {
     const int b = t / per_wave;
     const int c0 = (t % per_wave) << p.lg_cols;
@@ -242,7 +249,7 @@ __device__ __noinline__ void col_phase(const Params<R>& p, Cx<R>* buf, bool inv_
       cur[(pol * p.cols + c) * SL + spad<R>(k1)] = v;
     }
     __syncthreads();
-    if (inv_in) cur = cta_fft_l<R, true, N1>(cur, bufB, 2 * p.cols, p.tw1, &s_zero);
+    if (inv_in) cur = cta_fft_l<R, true, N1>(cur, bufB, 2 * p.cols, tws, &s_zero);
     for (int e = threadIdx.x + *(volatile int*)&s_zero; e < tile_len; e += kThreads) {
       const int c = e / seq, j1 = e & (seq - 1);
       Cx<R>* px = cur + c * SL + spad<R>(j1);
@@ -278,7 +285,7 @@ __device__ __noinline__ void col_phase(const Params<R>& p, Cx<R>* buf, bool inv_
       *py = y;
     }
     __syncthreads();
-    if (fwd_out) cur = cta_fft_l<R, false, N1>(cur, cur == bufA ? bufB : bufA, 2 * p.cols, p.tw1, &s_zero);
+    if (fwd_out) cur = cta_fft_l<R, false, N1>(cur, cur == bufA ? bufB : bufA, 2 * p.cols, tws, &s_zero);
     for (int e = threadIdx.x + *(volatile int*)&s_zero; e < 2 * tile_len; e += kThreads) {
       const int pol = e >= tile_len, i = e - pol * tile_len;
       const int k1 = i >> p.lg_cols, c = i & (p.cols - 1);
@@ -316,7 +323,8 @@ inline Geo geometry(int64_t n, int batch, size_t esz, int target_tiles) {
   const int ps = esz == 16 ? 4 : 3;
   auto stride = [&](int L) { return L + (L >> ps) + 1; };
   g.buf_elems = std::max(2 * g.rows * stride(g.n2), 2 * g.cols * stride(g.n1));
-  g.smem = 2 * esz * (size_t)g.buf_elems;
+  // two tile buffers (Stockham ping-pong) + the staged per-length twiddles
+  g.smem = esz * (2 * (size_t)g.buf_elems + (size_t)std::max(g.n1, g.n2));
   return g;
 }
 
