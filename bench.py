@@ -113,10 +113,12 @@ def _oracle_worker(args):
     key = (wname, seed)
     if key not in _WORKER_CACHE:
         cfg, coeffs = workload_cfg()
-        _WORKER_CACHE[key] = (cfg, coeffs, gaussian_wdm(WL["n"], RATE, seed=seed))
-    cfg, coeffs, field = _WORKER_CACHE[key]
+        field = gaussian_wdm(WL["n"], RATE, seed=seed)
+        # output buffer allocated once, uninitialised like dbp.py:469's empty_like
+        _WORKER_CACHE[key] = (cfg, coeffs, field, np.empty_like(field))
+    cfg, coeffs, field, out = _WORKER_CACHE[key]
     t0 = time.perf_counter()
-    orc.run_cb_blocks(field, cfg, RATE, coeffs, b0, b1)
+    orc.run_cb_blocks(field, cfg, RATE, coeffs, b0, b1, out=out)
     return time.perf_counter() - t0
 
 
@@ -159,10 +161,21 @@ def run_reference(args, rank, world):
     nb = BlockSchedule(WL["n"], WL["block"], WL["overlap"]).n_blocks
     parts = min(cores, nb)
     name = next(k for k, v in WORKLOADS.items() if v is WL)
-    ranges = [(nb * i // parts, nb * (i + 1) // parts, 0, name) for i in range(parts)]
     ctx = mp.get_context("spawn")
     times = []
+
+    def split(nblk):
+        return [(nblk * i // parts, nblk * (i + 1) // parts, 0, name) for i in range(parts)]
+
     with ctx.Pool(parts) as pool:
+        # a step is a bounded sample of the waveform's blocks: the whole
+        # --steps/--warmup run is kept to about 150 s of host time
+        t0 = time.perf_counter()
+        pool.map(_oracle_worker, split(nb), chunksize=1)       # also loads the workers
+        t_full = time.perf_counter() - t0
+        budget = 150.0 / max(1, args.warmup + args.steps)
+        used = nb if t_full <= budget else max(parts, int(nb * budget / t_full))
+        ranges = split(used)
         for i in range(args.warmup + args.steps):
             t0 = time.perf_counter()
             pool.map(_oracle_worker, ranges, chunksize=1)
@@ -170,7 +183,7 @@ def run_reference(args, rank, world):
             if i >= args.warmup:
                 times.append(dt)
     per = sum(times) / len(times)
-    value = symbols_per_wave() / per
+    value = symbols_per_wave() * used / nb / per
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -178,8 +191,8 @@ def run_reference(args, rank, world):
             "impl": "reference",
             "config": dict(config_block(args, world), waveforms_per_gpu=1),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": parts, "kind": "port",
-                             "sample": f"one configs[1] waveform per step, {nb} blocks "
-                                       f"split over {parts} processes"},
+                             "sample": f"{used} of the {nb} blocks of one {name} waveform per "
+                                       f"step, split over {parts} processes"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
