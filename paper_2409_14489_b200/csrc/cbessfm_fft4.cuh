@@ -51,9 +51,7 @@ struct Params {
   int rows, cols;          // rows per row tile, columns per column tile
   int lg_n2, lg_rows, lg_cols;
   int buf_elems;           // elements of each of the two tile buffers
-  const Cx<R>* tw_hi;      // W_n^(h << lo_bits)
-  const Cx<R>* tw_lo;      // W_n^l, l < 2^lo_bits
-  int lo_bits;
+  const Cx<R>* twn;        // [n1][n2]: W_n^(j2 k1) at (k1, j2), laid out like the data
   const Cx<R>* tw1;        // W_n1^m
   const Cx<R>* tw2;        // W_n2^m
   const Cx<R>* half;       // [n_tables][n1][n2]
@@ -155,9 +153,27 @@ __device__ __forceinline__ Cx<R>* cta_fft_l(Cx<R>* a, Cx<R>* b, int M,
   return (fft_passes<R, L>() & 1) ? b : a;
 }
 
+// The four-step twiddle W_n^(j2 k1) of element (k1, j2): one coalesced
+// load from a table with the data's layout.
 template <typename R>
-__device__ __forceinline__ Cx<R> tw_n(const Params<R>& p, int64_t e) {
-  return cmul(ldg(p.tw_hi + (e >> p.lo_bits)), ldg(p.tw_lo + (e & ((1 << p.lo_bits) - 1))));
+__device__ __forceinline__ Cx<R> tw_n(const Params<R>& p, int k1, int j2) {
+  return ldg(p.twn + ((int64_t)k1 << p.lg_n2) + j2);
+}
+
+// twn[k1 n2 + j2] = exp(-2 pi i ((j2 k1) mod n) / n): sincospi of an exactly
+// representable argument (n is a power of two), about 1 ulp.
+template <typename R>
+__global__ void fill_twn(Cx<R>* twn, int64_t n, int n2, int lg_n2) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t k1 = i >> lg_n2, j2 = i & (n2 - 1);
+  const int64_t e = (k1 * j2) & (n - 1);
+  R s, c;
+  if constexpr (sizeof(R) == 8)
+    sincospi(-2.0 * (double)e / (double)n, &s, &c);
+  else
+    sincospif(-2.0f * (float)e / (float)n, &s, &c);
+  twn[i] = mk(c, s);
 }
 
 // Row phase: FFT_n2, the spectral half steps, IFFT_n2 (channel.py:206, :211);
@@ -245,7 +261,7 @@ __device__ __noinline__ void col_phase(const Params<R>& p, Cx<R>* buf, bool inv_
       const int pol = e >= tile_len, i = e - pol * tile_len;
       const int k1 = i >> p.lg_cols, c = i & (p.cols - 1);
       Cx<R> v = base[pol * p.n + ((int64_t)k1 << p.lg_n2) + c];
-      if (inv_in) v = cmulc(v, tw_n(p, (int64_t)(c0 + c) * k1));
+      if (inv_in) v = cmulc(v, tw_n(p, k1, c0 + c));
       cur[(pol * p.cols + c) * SL + spad<R>(k1)] = v;
     }
     __syncthreads();
@@ -290,7 +306,7 @@ __device__ __noinline__ void col_phase(const Params<R>& p, Cx<R>* buf, bool inv_
       const int pol = e >= tile_len, i = e - pol * tile_len;
       const int k1 = i >> p.lg_cols, c = i & (p.cols - 1);
       Cx<R> v = cur[(pol * p.cols + c) * SL + spad<R>(k1)];
-      if (fwd_out) v = cmul(v, tw_n(p, (int64_t)(c0 + c) * k1));
+      if (fwd_out) v = cmul(v, tw_n(p, k1, c0 + c));
       base[pol * p.n + ((int64_t)k1 << p.lg_n2) + c] = v;
     }
     __syncthreads();
@@ -361,21 +377,19 @@ std::vector<R> to_r(const std::vector<long double>& v) {
 // here until release(), which the caller issues after synchronising.
 template <typename R>
 struct Fft4Tables {
-  std::vector<R> hi, lo, t1, t2;
-  void *dhi = nullptr, *dlo = nullptr, *d1 = nullptr, *d2 = nullptr;
+  std::vector<R> t1, t2;
+  void *dn = nullptr, *d1 = nullptr, *d2 = nullptr;
 
   cudaError_t build(int64_t n, const Geo& g, cudaStream_t st, Params<R>* p) {
-    int lo_bits = 0;
-    while ((int64_t(1) << (2 * lo_bits)) < n) ++lo_bits;
-    const int64_t n_lo = int64_t(1) << lo_bits, n_hi = (n + n_lo - 1) / n_lo;
-    hi = to_r<R>(unit_ld(n, n_hi, n_lo));
-    lo = to_r<R>(unit_ld(n, n_lo, 1));
     t1 = to_r<R>(unit_ld(g.n1, g.n1, 1));
     t2 = to_r<R>(unit_ld(g.n2, g.n2, 1));
     cudaError_t e;
-    if ((e = upload(hi, &dhi, st)) != cudaSuccess || (e = upload(lo, &dlo, st)) != cudaSuccess ||
+    if ((e = cudaMallocAsync(&dn, n * sizeof(Cx<R>), st)) != cudaSuccess ||
         (e = upload(t1, &d1, st)) != cudaSuccess || (e = upload(t2, &d2, st)) != cudaSuccess)
       return e;
+    fill_twn<R><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(reinterpret_cast<Cx<R>*>(dn), n,
+                                                            g.n2, __builtin_ctz(g.n2));
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     p->n = n;
     p->n1 = g.n1;
     p->n2 = g.n2;
@@ -385,17 +399,15 @@ struct Fft4Tables {
     p->lg_rows = __builtin_ctz(g.rows);
     p->lg_cols = __builtin_ctz(g.cols);
     p->buf_elems = g.buf_elems;
-    p->tw_hi = reinterpret_cast<const Cx<R>*>(dhi);
-    p->tw_lo = reinterpret_cast<const Cx<R>*>(dlo);
-    p->lo_bits = lo_bits;
+    p->twn = reinterpret_cast<const Cx<R>*>(dn);
     p->tw1 = reinterpret_cast<const Cx<R>*>(d1);
     p->tw2 = reinterpret_cast<const Cx<R>*>(d2);
     return cudaSuccess;
   }
   void release(cudaStream_t st) {
-    for (void* ptr : {dhi, dlo, d1, d2})
+    for (void* ptr : {dn, d1, d2})
       if (ptr) cudaFreeAsync(ptr, st);
-    dhi = dlo = d1 = d2 = nullptr;
+    dn = d1 = d2 = nullptr;
   }
 };
 
