@@ -22,7 +22,10 @@ namespace ssfm {
 #define CB_SSFM_THREADS 1024
 #endif
 constexpr int kThreads = CB_SSFM_THREADS;
-constexpr int kTileElems = 4096;  // complex elements per tile, both polarisations
+#ifndef CB_SSFM_TILE      // experiment knob
+#define CB_SSFM_TILE 4096
+#endif
+constexpr int kTileElems = CB_SSFM_TILE;  // complex elements per tile, both polarisations
 constexpr int kMaxLog2N = 22;     // n1, n2 <= 2048
 
 // Shared-memory layout of a tile: sequence m of length L starts at
@@ -181,7 +184,7 @@ __global__ void fill_twn(Cx<R>* twn, int64_t n, int n2, int lg_n2) {
 // N2 == p.n2 at compile time (kernels are instantiated per transform length).
 template <typename R, int N2>
 __device__ __noinline__ void row_phase(const Params<R>& p, Cx<R>* buf, const Cx<R>* ha, const Cx<R>* hb,
-                          bool fwd = true, bool inv = true) {
+                          bool fwd = true, bool inv = true, bool staged = false) {
   __shared__ int s_zero;
   if (threadIdx.x == 0) s_zero = 0;
   __syncthreads();
@@ -191,10 +194,13 @@ __device__ __noinline__ void row_phase(const Params<R>& p, Cx<R>* buf, const Cx<
   Cx<R>* const bufA = buf;
   Cx<R>* const bufB = buf + p.buf_elems;
   Cx<R>* cur = bufA;
-  // the length-n2 twiddles, staged once per phase behind the tile buffers
-  Cx<R>* const tws = buf + 2 * p.buf_elems;
-  for (int i = threadIdx.x; i < N2; i += kThreads) tws[i] = ldg(p.tw2 + i);
-  __syncthreads();
+  // the length-n2 twiddles live behind the tile buffers and the n1 ones
+  // (staged here unless the caller staged both for the whole kernel)
+  Cx<R>* const tws = buf + 2 * p.buf_elems + p.n1;
+  if (!staged) {
+    for (int i = threadIdx.x; i < N2; i += kThreads) tws[i] = ldg(p.tw2 + i);
+    __syncthreads();
+  }
   // element e of the tile: pol, row r, column c -> sequence pol*rows + r
   auto at = [&](int e) {
     return cur + (e >> p.lg_n2) * SL + spad<R>(e & (p.n2 - 1));
@@ -237,7 +243,8 @@ enum Mid { kNone = 0, kNonlinear = 1, kSpanEnd = 2 };
 // twiddle (starts the next forward transform).
 template <typename R, int N1>
 __device__ __noinline__ void col_phase(const Params<R>& p, Cx<R>* buf, bool inv_in, int mid, R nl,
-                          const Cx<R>* noise, bool pre_div, bool fwd_out) {
+                          const Cx<R>* noise, bool pre_div, bool fwd_out,
+                          bool staged = false) {
   __shared__ int s_zero;
   if (threadIdx.x == 0) s_zero = 0;
   __syncthreads();
@@ -248,9 +255,11 @@ __device__ __noinline__ void col_phase(const Params<R>& p, Cx<R>* buf, bool inv_
   const R inv_n = (R)1 / (R)p.n;         // exact: n is a power of two
   Cx<R>* const bufA = buf;
   Cx<R>* const bufB = buf + p.buf_elems;
-  Cx<R>* const tws = buf + 2 * p.buf_elems;  // length-n1 twiddles, staged once
-  for (int i = threadIdx.x; i < N1; i += kThreads) tws[i] = ldg(p.tw1 + i);
-  __syncthreads();
+  Cx<R>* const tws = buf + 2 * p.buf_elems;  // length-n1 twiddles
+  if (!staged) {
+    for (int i = threadIdx.x; i < N1; i += kThreads) tws[i] = ldg(p.tw1 + i);
+    __syncthreads();
+  }
   for (int t = blockIdx.x; t < p.batch * per_wave; t += gridDim.x) {
     const int b = t / per_wave;
     const int c0 = (t % per_wave) << p.lg_cols;
@@ -339,8 +348,9 @@ inline Geo geometry(int64_t n, int batch, size_t esz, int target_tiles) {
   const int ps = esz == 16 ? 4 : 3;
   auto stride = [&](int L) { return L + (L >> ps) + 1; };
   g.buf_elems = std::max(2 * g.rows * stride(g.n2), 2 * g.cols * stride(g.n1));
-  // two tile buffers (Stockham ping-pong) + the staged per-length twiddles
-  g.smem = esz * (2 * (size_t)g.buf_elems + (size_t)std::max(g.n1, g.n2));
+  // two tile buffers (Stockham ping-pong) + the staged length-n1 and
+  // length-n2 twiddles
+  g.smem = esz * (2 * (size_t)g.buf_elems + (size_t)g.n1 + (size_t)g.n2);
   return g;
 }
 

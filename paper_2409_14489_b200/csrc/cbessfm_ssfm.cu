@@ -40,23 +40,30 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) ssfm_kernel(const _
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Cx<R>* buf = reinterpret_cast<Cx<R>*>(smem_raw);
   cg::grid_group grid = cg::this_grid();
+  {  // both per-length twiddle tables, staged once for every phase of the run
+    Cx<R>* tw = buf + 2 * p.buf_elems;
+    for (int i = threadIdx.x; i < N1; i += kThreads) tw[i] = ldg(p.tw1 + i);
+    for (int i = threadIdx.x; i < N2; i += kThreads) tw[N1 + i] = ldg(p.tw2 + i);
+    __syncthreads();
+  }
   const size_t tab = (size_t)p.n;
   for (int span = 0; span < p.n_spans; ++span) {
     if (span == 0)  // spec = fft(field) (channel.py:206), after / g when backward
-      col_phase<R, N1>(p, buf, false, kNone, (R)0, nullptr, p.backward != 0, true);
+      col_phase<R, N1>(p, buf, false, kNone, (R)0, nullptr, p.backward != 0, true, true);
     for (int s = 0; s < p.k; ++s) {
       grid.sync();
       const Cx<R>* ha = s ? p.half + tab * p.step_table[s - 1] : nullptr;
-      row_phase<R, N2>(p, buf, ha, p.half + tab * p.step_table[s]);
+      row_phase<R, N2>(p, buf, ha, p.half + tab * p.step_table[s], true, true, true);
       grid.sync();
-      col_phase<R, N1>(p, buf, true, kNonlinear, p.nl_coef[s], nullptr, false, true);
+      col_phase<R, N1>(p, buf, true, kNonlinear, p.nl_coef[s], nullptr, false, true, true);
     }
     grid.sync();
-    row_phase<R, N2>(p, buf, p.half + tab * p.step_table[p.k - 1], (const Cx<R>*)nullptr);
+    row_phase<R, N2>(p, buf, p.half + tab * p.step_table[p.k - 1], (const Cx<R>*)nullptr, true,
+                     true, true);
     grid.sync();
     const bool more = span + 1 < p.n_spans;
     const Cx<R>* nz = p.noise ? p.noise + (int64_t)span * p.batch * 2 * p.n : nullptr;
-    col_phase<R, N1>(p, buf, true, kSpanEnd, (R)0, nz, more && p.backward, more);
+    col_phase<R, N1>(p, buf, true, kSpanEnd, (R)0, nz, more && p.backward, more, true);
     if (more) grid.sync();
   }
 }

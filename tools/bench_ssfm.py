@@ -5,6 +5,7 @@ CUDA-event timed; prints one JSON line per case. The reference takes 41.5 s
 (configs[0], n = 2^17) to ~52 min (configs[3], n = 2^21) per waveform on one
 core."""
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -25,7 +26,9 @@ def main():
     dtypes = sys.argv[1:] or ["c128"]
     for dt in dtypes:
         ct = torch.complex128 if dt == "c128" else torch.complex64
-        for text, n, rate, spans, nch in CASES:
+        only = os.environ.get("BENCH_SSFM_CASES")      # e.g. "0,1"
+        cases = [CASES[int(i)] for i in only.split(",")] if only else CASES
+        for text, n, rate, spans, nch in cases:
             lk = LinkConfig(num_spans=spans, span_length_km=80.0, gamma_w_km=1.3)
             sim = ch.SimSettings(step_km=0.8, noise_enabled=False)
             steps = ch.span_step_sizes(lk, sim, 1e-3)
