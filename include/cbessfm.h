@@ -153,6 +153,14 @@ cbessfm_status cbessfm_run_host(const cbessfm_plan* plan, const cbessfm_host_io*
 cbessfm_status cbessfm_nlpr(int32_t dtype, int32_t n_subbands, int32_t n_prime, const void* in,
                             void* out, const double* mimo, double theta_scale, void* stream);
 
+/* Replace the coefficient-set tables of a plan (same geometry, same n_sets):
+ * mimo [n_sets][P][Q/2+1] and theta_scale [n_sets][n_steps], HOST, laid
+ * out as in cbessfm_desc. Ordered on `stream` and synchronous; an
+ * optimiser re-evaluating candidate taps reuses one plan this way instead
+ * of rebuilding it (the dispersion tables and twiddles do not change). */
+cbessfm_status cbessfm_plan_update_sets(cbessfm_plan* plan, const double* mimo,
+                                        const double* theta_scale, void* stream);
+
 /* Free the plan's device tables. */
 cbessfm_status cbessfm_plan_destroy(cbessfm_plan* plan);
 

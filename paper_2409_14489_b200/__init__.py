@@ -17,7 +17,7 @@ from .complexity import (CostCounter, CostReport, cb_essfm_cost,
                          count_runtime_multiplies, essfm_time_domain_cost)
 from .config import (VARIANTS, CoefficientSet, DbpConfig, DualPolWaveform,
                      LinkConfig)
-from .engine import (DbpEngine, MimoTransfer, build_mimo_transfer,
+from .engine import (DbpEngine, MimoTransfer, SetEvaluator, build_mimo_transfer,
                      channel_memory_samples, get_plan, gvd_step, launch,
                      nlpr_step, run_dbp, run_dbp_sets, run_dbp_sets_tensor,
                      run_dbp_tensor)

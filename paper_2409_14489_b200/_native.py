@@ -93,6 +93,8 @@ SIGNATURES = {
     "cbessfm_run_host": (C.c_int, [C.c_void_p, C.POINTER(HostIo), C.c_void_p]),
     "cbessfm_nlpr": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                C.POINTER(C.c_double), C.c_double, C.c_void_p]),
+    "cbessfm_plan_update_sets": (C.c_int, [C.c_void_p, C.POINTER(C.c_double),
+                                           C.POINTER(C.c_double), C.c_void_p]),
     "cbessfm_plan_destroy": (C.c_int, [C.c_void_p]),
     "cbessfm_last_error": (C.c_char_p, []),
     "cbessfm_debug_phase_times": (C.c_int32, [C.c_void_p, C.POINTER(C.c_int64), C.c_int32]),
@@ -215,6 +217,14 @@ class NativePlan:
         io = HostIo(in_ptr, out_ptr, n, batch, chunks)
         check(self._lib.cbessfm_run_host(self.handle, C.byref(io), C.c_void_p(stream)),
               "cbessfm_run_host")
+
+    def update_sets(self, mimo: np.ndarray, theta_scale: np.ndarray, stream: int = 0) -> None:
+        """Overwrite the coefficient-set tables (cbessfm_plan_update_sets)."""
+        mi = np.ascontiguousarray(mimo, np.complex128)
+        th = np.ascontiguousarray(theta_scale, np.float64)
+        check(self._lib.cbessfm_plan_update_sets(self.handle, _dptr(mi.view(np.float64)),
+                                                 _dptr(th), C.c_void_p(stream)),
+              "cbessfm_plan_update_sets")
 
     def __del__(self):
         h = getattr(self, "handle", None)

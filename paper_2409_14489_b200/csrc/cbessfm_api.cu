@@ -171,6 +171,23 @@ cudaError_t upload_real(const double* host, size_t count, void** dev) {
   return cudaMemcpy(*dev, tmp.data(), bytes, cudaMemcpyHostToDevice);
 }
 
+// Overwrite the coefficient-set tables (MIMO spectra, theta scales) of an
+// existing plan in place; same rounding as upload_complex / upload_real.
+template <typename R>
+cudaError_t rewrite_sets(cbessfm_plan* p, const double* mimo, const double* theta,
+                         cudaStream_t st) {
+  const size_t H1 = (size_t)p->Q / 2 + 1;
+  const size_t nm = (size_t)p->n_sets * p->P * H1, nt = (size_t)p->n_sets * p->n_steps;
+  std::vector<R> m(2 * nm), t(nt);
+  for (size_t i = 0; i < 2 * nm; ++i) m[i] = (R)mimo[i];
+  for (size_t i = 0; i < nt; ++i) t[i] = (R)theta[i];
+  cudaError_t e = cudaMemcpyAsync(p->mimo, m.data(), m.size() * sizeof(R), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && nt)
+    e = cudaMemcpyAsync(p->theta, t.data(), t.size() * sizeof(R), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the staging vectors die here
+  return e;
+}
+
 template <typename R>
 cbessfm_status upload_all(cbessfm_plan* p, const cbessfm_desc* d) {
   const size_t PQ = (size_t)p->P * p->Q;
@@ -487,6 +504,18 @@ cbessfm_status cbessfm_run_host(const cbessfm_plan* cp, const cbessfm_host_io* i
   for (cudaEvent_t ev : evs) cudaEventDestroy(ev);  // released once complete
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "cbessfm_run_host");
   return CBESSFM_OK;
+}
+
+cbessfm_status cbessfm_plan_update_sets(cbessfm_plan* p, const double* mimo,
+                                        const double* theta_scale, void* stream) {
+  g_err.clear();
+  if (!p || !mimo || (p->n_steps > 0 && !theta_scale))
+    return fail(CBESSFM_ERR_INVALID, "null plan or tables");
+  if (p->n_steps == 0) return fail(CBESSFM_ERR_INVALID, "plan has no nonlinear steps");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const cudaError_t e = p->dtype == CBESSFM_C64 ? rewrite_sets<float>(p, mimo, theta_scale, st)
+                                                : rewrite_sets<double>(p, mimo, theta_scale, st);
+  return e == cudaSuccess ? CBESSFM_OK : cuda_fail(e, "update coefficient sets");
 }
 
 cbessfm_status cbessfm_plan_destroy(cbessfm_plan* p) {

@@ -345,6 +345,58 @@ def run_dbp_sets_tensor(x, cfg, coeff_sets, sample_rate: float, out=None, stream
     return out
 
 
+class SetEvaluator:
+    """Evaluate batches of S candidate coefficient sets on a device-resident
+    waveform with one plan: the first call uploads the dispersion tables
+    and twiddles, later calls only rewrite the MIMO spectra and theta
+    scales (cbessfm_plan_update_sets) -- the loop an optimiser runs
+    (optimize.py:129-167). Returns [S, 2, n] per call."""
+
+    def __init__(self, cfg, sample_rate: float, n_sets: int, dtype: str = "c128",
+                 device: int | None = None):
+        torch = _torch()
+        validate_config(cfg)
+        if n_sets < 1:
+            raise ValueError("n_sets must be >= 1")
+        self.cfg, self.rate, self.n_sets, self.dtype = cfg, sample_rate, n_sets, dtype
+        self.device = torch.cuda.current_device() if device is None else device
+        self.plan = None
+
+    def _tables(self, coeff_sets):
+        if len(coeff_sets) != self.n_sets:
+            raise ValueError(f"expected {self.n_sets} coefficient sets")
+        n_sb = _variant_geometry(self.cfg, coeff_sets[0])
+        q = self.cfg.block_size // n_sb
+        mimo, theta = [], []
+        for c in coeff_sets:                       # build_tables' checks (dbp.py:340-342)
+            if c.n_sb != n_sb:
+                raise ValueError("coefficient set built for a different n_subbands")
+            scales = np.asarray(c.step_scales, float)
+            if scales.size < self.cfg.n_steps:
+                raise ValueError("coefficient set has fewer step scales than steps")
+            mimo.append(mimo_spectra(c, q))
+            theta.append(scales[:self.cfg.n_steps] / c.reference_power_w / q)
+        return np.stack(mimo), np.stack(theta)
+
+    def __call__(self, x, coeff_sets, out=None, stream=None):
+        torch = _torch()
+        coeff_sets = list(coeff_sets)
+        if self.plan is None:
+            self.plan = _sets_plan(self.cfg, self.rate, coeff_sets, self.dtype, self.device)
+        else:
+            mimo, theta = self._tables(coeff_sets)
+            with torch.cuda.device(self.device):
+                st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+                self.plan.update_sets(mimo, theta, st)
+        if x.dim() == 3:
+            x = x[0]
+        n = x.shape[-1]
+        if out is None:
+            out = torch.empty((self.n_sets, 2, n), dtype=x.dtype, device=x.device)
+        launch(self.plan, x.unsqueeze(0).expand(self.n_sets, 2, n), out, stream=stream)
+        return out
+
+
 def run_dbp_sets(w, cfg, coeff_sets, counter=None, *, dtype: str = "c128",
                  device: int | None = None) -> list:
     """run_dbp(w, cfg, c) for every c in coeff_sets, as one launch; returns

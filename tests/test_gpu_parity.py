@@ -266,3 +266,28 @@ def test_coefficient_sets_in_one_launch(cuda):
     assert rel_rms(np.vstack([outs[1].x, outs[1].y]), np.vstack([outs[0].x, outs[0].y])) > 1e-4
     with pytest.raises(ValueError):
         pb.run_dbp_sets(g.wave, replace(g.cfg, n_steps=0), sets)
+
+
+def test_set_evaluator_reuses_its_plan(cuda):
+    # SetEvaluator: plan built once, later batches only rewrite the MIMO /
+    # theta tables (cbessfm_plan_update_sets); every batch == the oracle
+    import torch
+    g = golden("cfg1_nsb3_st2")
+    field = np.vstack([g.wave.x, g.wave.y])
+    x = torch.from_numpy(field).to(cuda)
+    rng = np.random.default_rng(11)
+    ev = pb.SetEvaluator(g.cfg, g.wave.sample_rate, 3, dtype="c128")
+    plan0 = None
+    for it in range(3):
+        sets = []
+        for s in range(3):
+            taps = {h: c * (1 + 3e-2 * rng.normal(size=c.size)) for h, c in g.coeffs.coeffs.items()}
+            taps[0] = 0.5 * (taps[0] + taps[0][::-1])
+            sets.append(replace(g.coeffs, coeffs=taps))
+        out = ev(x, sets).cpu().numpy()
+        plan0 = plan0 or ev.plan
+        assert ev.plan is plan0
+        for c, o in zip(sets, out):
+            assert rel_rms(o, orc.run_cb_blocks(field, g.cfg, g.wave.sample_rate, c)) < 1e-12
+    with pytest.raises(ValueError):
+        ev(x, sets[:2])
