@@ -382,6 +382,19 @@ std::vector<R> to_r(const std::vector<long double>& v) {
 }
 
 
+// Stream-ordered frees of device buffers on scope exit (error paths too).
+struct StreamFrees {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit StreamFrees(cudaStream_t s) : st(s) {}
+  void add(void* p) {
+    if (p) ptrs.push_back(p);
+  }
+  ~StreamFrees() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+};
+
 // Device twiddle tables of one four-step geometry. build() uploads them on
 // `st` and fills the transform fields of p; the host staging vectors live
 // here until release(), which the caller issues after synchronising.

@@ -308,11 +308,15 @@ cbessfm_status symbols(const cbessfm_rx_desc* d, const Plan& pl, const void* in,
   const Geo gl = geometry(pl.L, d->n_channels, sizeof(C), 2 * sms);
   void *spec = nullptr, *dcidx = nullptr;
   const void* dg = nullptr;
-  cudaError_t e;
-  if ((e = cudaMallocAsync(&spec, 2 * pl.n * sizeof(C), st)) ||
-      (e = cudaMemcpyAsync(spec, in, 2 * pl.n * sizeof(C), cudaMemcpyDeviceToDevice, st)) ||
-      (e = upload(pl.cidx, &dcidx, st)) || (e = cached_filter(pl, d, st, &dg)))
-    return cuda_fail(e, "rx staging");
+  StreamFrees frees(st);
+  cudaError_t e = cudaMallocAsync(&spec, 2 * pl.n * sizeof(C), st);
+  frees.add(spec);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(spec, in, 2 * pl.n * sizeof(C), cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = upload(pl.cidx, &dcidx, st);
+  frees.add(dcidx);
+  if (e == cudaSuccess) e = cached_filter(pl, d, st, &dg);
+  if (e != cudaSuccess) return cuda_fail(e, "rx staging");
   ssfm::Params<R> ps{}, pls{};
   if ((e = cached_params<R>(pl.n, gs, d->device, st, &ps)) ||
       (e = cached_params<R>(pl.L, gl, d->device, st, &pls)))
@@ -331,8 +335,6 @@ cbessfm_status symbols(const cbessfm_rx_desc* d, const Plan& pl, const void* in,
   pls.batch = d->n_channels;
   pls.gain = (R)std::sqrt(d->launch_power_w / 2);  // metrics.py:138-140
   if ((e = launch_transform<R>(pls, gl, true, true, st))) return cuda_fail(e, "symbol IFFT");
-  cudaFreeAsync(spec, st);
-  cudaFreeAsync(dcidx, st);
   if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "rx");
   return CBESSFM_OK;
 }

@@ -104,7 +104,12 @@ cbessfm_status run(const cbessfm_ssfm_desc* d, void* data, const void* noise, cu
   // host tables: four-step twiddles (Fft4Tables), permuted halves
   Params<R> p;
   Fft4Tables<R> tw;
-  if ((e = tw.build(n, g, st, &p)) != cudaSuccess)
+  StreamFrees frees(st);
+  e = tw.build(n, g, st, &p);
+  frees.add(tw.dn);
+  frees.add(tw.d1);
+  frees.add(tw.d2);
+  if (e != cudaSuccess)
     return fail(CBESSFM_ERR_CUDA, std::string("ssfm twiddle upload: ") + cudaGetErrorString(e));
   std::vector<R> half(2 * (size_t)d->n_tables * n);
   for (int tb = 0; tb < d->n_tables; ++tb)
@@ -120,8 +125,13 @@ cbessfm_status run(const cbessfm_ssfm_desc* d, void* data, const void* noise, cu
   for (int s = 0; s < d->steps_per_span; ++s) nl[s] = (R)d->nl_coef[s];
 
   void *dh = nullptr, *ds = nullptr, *dn = nullptr;
-  if ((e = upload(half, &dh, st)) != cudaSuccess || (e = upload(steps, &ds, st)) != cudaSuccess ||
-      (e = upload(nl, &dn, st)) != cudaSuccess)
+  e = upload(half, &dh, st);
+  if (e == cudaSuccess) e = upload(steps, &ds, st);
+  if (e == cudaSuccess) e = upload(nl, &dn, st);
+  frees.add(dh);
+  frees.add(ds);
+  frees.add(dn);
+  if (e != cudaSuccess)
     return fail(CBESSFM_ERR_CUDA, std::string("ssfm table upload: ") + cudaGetErrorString(e));
 
   p.data = reinterpret_cast<Cx<R>*>(data);
@@ -136,8 +146,7 @@ cbessfm_status run(const cbessfm_ssfm_desc* d, void* data, const void* noise, cu
   p.noise = reinterpret_cast<const Cx<R>*>(noise);
   void* args[] = {&p};
   e = cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kThreads), args, g.smem, st);
-  for (void* ptr : {dh, ds, dn}) cudaFreeAsync(ptr, st);
-  tw.release(st);
+  // the StreamFrees guard releases the tables after the launch, in stream order
   // the host staging vectors are read by the async copies
   const cudaError_t s2 = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return fail(CBESSFM_ERR_CUDA, std::string("ssfm launch: ") + cudaGetErrorString(e));
