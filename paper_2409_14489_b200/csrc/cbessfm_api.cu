@@ -450,7 +450,10 @@ cbessfm_status cbessfm_run_host(const cbessfm_plan* cp, const cbessfm_host_io* i
   cudaStream_t s_in = p->host_streams[0], s_out = p->host_streams[1];
   void *din = nullptr, *dout = nullptr;
   if ((e = cudaMallocAsync(&din, rows * rowb, st)) != cudaSuccess) return cuda_fail(e, "alloc in");
-  if ((e = cudaMallocAsync(&dout, rows * rowb, st)) != cudaSuccess) return cuda_fail(e, "alloc out");
+  if ((e = cudaMallocAsync(&dout, rows * rowb, st)) != cudaSuccess) {
+    cudaFreeAsync(din, st);
+    return cuda_fail(e, "alloc out");
+  }
   std::vector<cudaEvent_t> evs;
   auto event = [&](cudaStream_t s2) {
     cudaEvent_t ev;
@@ -473,35 +476,41 @@ cbessfm_status cbessfm_run_host(const cbessfm_plan* cp, const cbessfm_host_io* i
   // same schedule as DbpEngine.run_host: wrap piece first, then `chunks`
   // sample ranges; blocks whose windows end inside the copied prefix run
   // as soon as it lands, the last chunk takes the remaining blocks
-  const int64_t wrap = half > 0 ? n - half : n;
-  if (half > 0 && (e = h2d(wrap, n)) != cudaSuccess) return cuda_fail(e, "h2d");
-  int64_t b_prev = 0, lo = 0;
-  for (int c = 1; c <= chunks; ++c) {
-    const int64_t hi = c == chunks ? n : (n * c) / chunks;
-    int64_t b1 = c == chunks ? nb : (hi + half - p->N >= 0 ? (hi + half - p->N) / keep + 1 : 0);
-    b1 = std::max(b_prev, std::min(b1, nb));
-    if (std::min(hi, wrap) > lo && (e = h2d(lo, std::min(hi, wrap))) != cudaSuccess)
-      return cuda_fail(e, "h2d");
-    cudaEvent_t ev_in = event(s_in);
-    if (b1 > b_prev) {
-      cudaStream_t sk = p->host_streams[1 + c];
-      cudaStreamWaitEvent(sk, ev_in, 0);
-      cbessfm_io dio{din, 2 * n, n, 0, dout, 2 * n, n, 0, n, batch, b_prev, b1};
-      const cbessfm_status r = cbessfm_run(p, &dio, sk);
-      if (r != CBESSFM_OK) return r;
-      cudaEvent_t ev_k = event(sk);
-      cudaStreamWaitEvent(s_out, ev_k, 0);
-      const int64_t o0 = b_prev * keep, o1 = std::min(b1 * keep, n);
-      if ((e = d2h(o0, o1)) != cudaSuccess) return cuda_fail(e, "d2h");
+  auto enqueue = [&]() -> cbessfm_status {
+    const int64_t wrap = half > 0 ? n - half : n;
+    if (half > 0 && (e = h2d(wrap, n)) != cudaSuccess) return cuda_fail(e, "h2d");
+    int64_t b_prev = 0, lo = 0;
+    for (int c = 1; c <= chunks; ++c) {
+      const int64_t hi = c == chunks ? n : (n * c) / chunks;
+      int64_t b1 = c == chunks ? nb : (hi + half - p->N >= 0 ? (hi + half - p->N) / keep + 1 : 0);
+      b1 = std::max(b_prev, std::min(b1, nb));
+      if (std::min(hi, wrap) > lo && (e = h2d(lo, std::min(hi, wrap))) != cudaSuccess)
+        return cuda_fail(e, "h2d");
+      cudaEvent_t ev_in = event(s_in);
+      if (b1 > b_prev) {
+        cudaStream_t sk = p->host_streams[1 + c];
+        cudaStreamWaitEvent(sk, ev_in, 0);
+        cbessfm_io dio{din, 2 * n, n, 0, dout, 2 * n, n, 0, n, batch, b_prev, b1};
+        const cbessfm_status r = cbessfm_run(p, &dio, sk);
+        if (r != CBESSFM_OK) return r;
+        cudaEvent_t ev_k = event(sk);
+        cudaStreamWaitEvent(s_out, ev_k, 0);
+        const int64_t o0 = b_prev * keep, o1 = std::min(b1 * keep, n);
+        if ((e = d2h(o0, o1)) != cudaSuccess) return cuda_fail(e, "d2h");
+      }
+      b_prev = b1;
+      lo = hi;
     }
-    b_prev = b1;
-    lo = hi;
-  }
-  cudaEvent_t done = event(s_out);
-  cudaStreamWaitEvent(st, done, 0);
+    return CBESSFM_OK;
+  };
+  const cbessfm_status status = enqueue();
+  // join every pipeline stream into the caller's stream (also after an
+  // error), then release the staging buffers in stream order
+  for (int i = 0; i < 2 + chunks; ++i) cudaStreamWaitEvent(st, event(p->host_streams[i]), 0);
   cudaFreeAsync(din, st);
   cudaFreeAsync(dout, st);
   for (cudaEvent_t ev : evs) cudaEventDestroy(ev);  // released once complete
+  if (status != CBESSFM_OK) return status;
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "cbessfm_run_host");
   return CBESSFM_OK;
 }
