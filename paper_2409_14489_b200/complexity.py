@@ -36,6 +36,14 @@ class CostReport:
                                     abs_tol=1e-9):
             raise ValueError("breakdown does not sum to the totals")
 
+    def csv_row(self, variant: str, n_steps: int, n_subbands: int, block_size: int,
+                overlap: int, oversampling: float) -> dict:
+        """One cost-table row (complexity.py:61-65 column order)."""
+        cols = ("variant", "N_st", "N_sb", "N", "N_ov", "n", "RM_per_2D", "RA_per_2D")
+        vals = (variant, n_steps, n_subbands, block_size, overlap, oversampling,
+                self.rm_per_2d, self.ra_per_2d)
+        return {c: v for c, v in zip(cols, vals)}
+
 
 def _cfft(size: int) -> tuple[float, float]:
     lg = math.log2(size)

@@ -151,3 +151,61 @@ def test_ideal_ssfm_restores_nonlinear_channel(link, cuda):
     out = pb.run_dbp(rx, pb.DbpConfig(link=link, variant="IDEAL_SSFM", n_steps=960,
                                       block_size=4096, oversampling=2.0))
     assert rel_rms(_f(out), _f(w)) < 1e-2
+
+
+# --- pkg/tests/test_complexity.py:70-130: the runtime counter on GPU runs
+
+@pytest.fixture(scope="module")
+def counted_setup(cuda):
+    lk = LinkConfig(num_spans=2, span_length_km=80.0)
+    rx = ch.propagate_link(_wave(4096, 0.0, 31), lk,
+                           ch.SimSettings(max_phase_rad=2e-3, noise_enabled=False))
+    return lk, rx
+
+
+def run_counted(lk, rx, variant, n_steps, n_sb, block, overlap):
+    cfg = pb.DbpConfig(link=lk, variant=variant, n_steps=n_steps, n_subbands=n_sb,
+                       block_size=block, overlap=overlap, oversampling=2.0)
+    coeffs = None
+    if variant not in ("EDC", "IDEAL_SSFM") and n_steps:
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", RuntimeWarning)
+            coeffs = cf.make_dbp_coefficient_set(cfg, rx.sample_rate, 1e-3, oversample=16)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        return cfg, pb.count_runtime_multiplies(rx, cfg, coeffs)
+
+
+def test_counter_matches_formula_exact_tiling(counted_setup):
+    lk, rx = counted_setup
+    for variant, n_sb in (("EDC", 1), ("OSSFM", 1), ("ESSFM", 1), ("CB_ESSFM", 2)):
+        n_steps = 0 if variant == "EDC" else 2
+        cfg, rep = run_counted(lk, rx, variant, n_steps, n_sb, 2048, 1024)
+        if variant == "CB_ESSFM":
+            ref = pb.cb_essfm_cost(2048, 1024, 2.0, n_steps, n_sb)
+        else:
+            taps = 0
+            if variant == "ESSFM":
+                with warnings.catch_warnings():
+                    warnings.simplefilter("ignore", RuntimeWarning)
+                    taps = (cf.make_dbp_coefficient_set(cfg, rx.sample_rate, 1e-3,
+                                                        oversample=16).coeffs[0].size - 1) // 2
+            ref = pb.essfm_time_domain_cost(2048, 1024, 2.0, n_steps, taps)
+        assert rep.rm_per_2d == pytest.approx(ref.rm_per_2d, rel=1e-9), variant
+        assert rep.ra_per_2d == pytest.approx(ref.ra_per_2d, rel=1e-9), variant
+
+
+def test_counter_partial_final_block_within_one_percent(counted_setup):
+    lk, rx = counted_setup
+    cfg, rep = run_counted(lk, rx, "CB_ESSFM", 2, 2, 2048, 512)
+    ref = pb.cb_essfm_cost(2048, 512, 2.0, 2, 2)
+    overshoot = int(np.ceil(4096 / 1536)) * 1536 / 4096
+    assert rep.rm_per_2d == pytest.approx(ref.rm_per_2d * overshoot, rel=0.01)
+
+
+def test_counter_rejects_ideal_ssfm(counted_setup):
+    lk, rx = counted_setup
+    cfg = pb.DbpConfig(link=lk, variant="IDEAL_SSFM", n_steps=100, block_size=2048,
+                       oversampling=2.0)
+    with pytest.raises(ValueError):
+        pb.count_runtime_multiplies(rx, cfg)
