@@ -111,3 +111,69 @@ def test_standard_set_and_errors(cuda):
         cf.make_dbp_coefficient_set(replace(g.cfg, variant="EDC", n_subbands=1), 1e9, 1e-3)
     with pytest.raises(ValueError):
         cf.analytic_coefficients(cf.StepGeometry(80.0, 80.0), 0.0, 0, 1e9, 1e-3)
+
+
+# --- pkg/tests/test_kernel.py:108-202 replayed on the GPU builder
+
+GEOM240 = dict(length_km=240.0, span_km=80.0)
+
+
+def test_kernel_zero_frequency_is_effective_length(cuda):
+    g = cf.StepGeometry(**GEOM240)
+    got = cf.step_kernel(0.0, 0.0, g)
+    a, lsp = g.alpha_np_km, g.span_km
+    expect = g.gamma_w_km * g.num_spans * (1 - np.exp(-a * lsp)) / a
+    assert abs(got - expect) / expect < 1e-12 and abs(got.imag) < 1e-12 * abs(got)
+    assert abs(got / g.gamma_w_km - g.effective_length_km) < 1e-9
+
+
+def test_kernel_time_reversal(cuda):
+    g = cf.StepGeometry(**GEOM240)
+    rng = np.random.default_rng(14)
+    mu, nu = rng.uniform(-SUB_RATE, SUB_RATE, 30), rng.uniform(-SUB_RATE, SUB_RATE, 30)
+    a, b = cf.step_kernel(mu, nu, g), cf.step_kernel(-mu, -nu, g)
+    assert np.abs(a - b).max() < 1e-12 * np.abs(a).max()
+
+
+def test_step_kernel_splitting_ratio_is_pure_phase(cuda):
+    mu, nu = 7.1e9, -3.3e9
+    raw = cf.step_kernel(mu, nu, cf.StepGeometry(**GEOM240))
+    g = cf.StepGeometry(length_km=240.0, span_km=80.0, rho=0.2)
+    stepped = cf.step_kernel(mu, nu, g)
+    assert abs(abs(stepped) - abs(raw)) < 1e-9 * abs(raw)
+    b = 2 * np.pi ** 2 * g.beta2_ps2_km * 1e-24 * nu * (mu - nu)
+    assert abs(stepped - raw * np.exp(-2j * b * (0.5 - g.rho) * g.length_km)) < 1e-9 * abs(raw)
+
+
+def test_coefficients_even_in_lag(cuda):
+    c0 = cf.analytic_coefficients(cf.StepGeometry(**GEOM240), 0.0, 15, SUB_RATE, 1e-3)
+    assert np.abs(c0 - c0[::-1]).max() < 1e-10 * np.abs(c0).max()
+
+
+def test_coefficients_linear_in_gamma_and_power(cuda):
+    g = cf.StepGeometry(**GEOM240)
+    base = cf.analytic_coefficients(g, 0.0, 8, SUB_RATE, 1e-3)
+    assert np.abs(cf.analytic_coefficients(g, 0.0, 8, SUB_RATE, 3e-3) - 3 * base).max() < \
+        1e-12 * np.abs(base).max()
+    g2 = cf.StepGeometry(length_km=240.0, span_km=80.0, gamma_w_km=2 * g.gamma_w_km)
+    assert np.abs(cf.analytic_coefficients(g2, 0.0, 8, SUB_RATE, 1e-3) - 2 * base).max() < \
+        1e-12 * np.abs(base).max()
+
+
+def test_memory_rule():
+    g = cf.StepGeometry(**GEOM240)
+    assert 2 * cf.coefficient_memory(0, g, 1.0, 1.125 * 93e9, 2) + 1 == 45
+    assert 2 * cf.coefficient_memory(1, g, 1.0, 1.125 * 93e9, 2) + 1 == 91
+    assert cf.coefficient_memory(0, cf.StepGeometry(length_km=1.0, span_km=80.0), 1.0, 1e9, 1) >= 1
+
+
+def test_interband_coefficients_asymmetric_support(cuda):
+    c1 = cf.analytic_coefficients(cf.StepGeometry(**GEOM240), SUB_RATE, 60, SUB_RATE, 1e-3)
+    lags = np.arange(-60, 61)
+    assert abs(float(np.sum(lags * np.abs(c1)) / np.sum(np.abs(c1)))) > 1.0
+
+
+@pytest.mark.parametrize("bad", [-1, 0])
+def test_coefficient_rejects_bad_memory(cuda, bad):
+    with pytest.raises(ValueError):
+        cf.analytic_coefficients(cf.StepGeometry(**GEOM240), 0.0, bad, SUB_RATE, 1e-3)
