@@ -93,3 +93,46 @@ def test_snr_cap_and_errors(cuda):
         rxm.channel_symbols(w, _wdm(g), bandwidth=1e15)          # wider than the grid
     with pytest.raises(ValueError):
         rxm.channel_symbols(w, _wdm(g, n_ch=9, spacing=100e9))   # outer channels off-grid
+
+
+# --- pkg/tests/test_metrics.py:18-66 replayed on the GPU SNR reduction
+
+def _symbols(n=4096, seed=0):
+    rng = np.random.default_rng(seed)
+    lv = np.array([-3, -1, 1, 3]) / np.sqrt(10.0)
+    return lv[rng.integers(0, 4, (2, n))] + 1j * lv[rng.integers(0, 4, (2, n))]
+
+
+def test_snr_of_identical_inputs_is_capped(cuda):
+    tx = _symbols()
+    res = rxm.snr(tx, tx)
+    assert res.exact_match and res.snr_db == 100.0
+
+
+def test_snr_matches_known_noise_level(cuda):
+    tx = _symbols(n=200_000)
+    rng = np.random.default_rng(1)
+    sigma = 10 ** (-25 / 20)
+    noise = (rng.normal(size=tx.shape) + 1j * rng.normal(size=tx.shape)) * sigma / np.sqrt(2)
+    res = rxm.snr(tx + noise, tx)
+    assert abs(res.snr_db - 25.0) < 0.05 and not res.exact_match
+    assert res.num_symbols == 200_000
+
+
+def test_snr_is_scale_invariant(cuda):
+    tx = _symbols(seed=2)
+    rng = np.random.default_rng(3)
+    rx = tx + 0.01 * (rng.normal(size=tx.shape) + 1j * rng.normal(size=tx.shape))
+    assert abs(rxm.snr(rx, tx).snr_db - rxm.snr(rx * np.exp(0.7j), tx).snr_db) < 1e-9
+
+
+def test_mean_phase_and_per_polarisation_snr(cuda):
+    tx = _symbols(seed=4)
+    assert abs(rxm.snr(tx * np.exp(0.31j), tx).mean_phase_removed - 0.31) < 1e-12
+    rx = tx.copy()
+    rng = np.random.default_rng(6)
+    rx[1] += 0.1 * (rng.normal(size=tx.shape[1]) + 1j * rng.normal(size=tx.shape[1]))
+    res = rxm.snr(rx, tx)
+    assert res.snr_x_db > res.snr_y_db + 20
+    with pytest.raises(ValueError):
+        rxm.snr(1j * np.ones((2, 4)), np.zeros((2, 4)))

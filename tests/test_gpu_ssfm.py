@@ -144,3 +144,15 @@ def test_errors(cuda):
     bad.x[3] = np.nan
     with pytest.raises(ValueError):
         ch.propagate_link(bad, g.link(), g.sim())
+
+
+def test_checkpoint_resume_is_bit_exact_with_ase(cuda):
+    # pkg/tests/test_channel.py:131-140: resuming from the span-2 snapshot
+    # reproduces the uninterrupted noisy run bit for bit
+    lk = LinkConfig(num_spans=3, span_length_km=80.0)
+    sim = ch.SimSettings(max_phase_rad=2e-3, noise_enabled=True, noise_seed=3)
+    w = SsfmGolden("fwd").wave()
+    snaps = {}
+    full = ch.propagate_link(w, lk, sim, checkpoint=lambda k, s: snaps.update({k: s}))
+    resumed = ch.propagate_link(snaps[2], lk, sim, first_span=2)
+    assert np.array_equal(full.x, resumed.x) and np.array_equal(full.y, resumed.y)

@@ -300,3 +300,30 @@ def test_coefficient_set_metadata_matches_reference(name):
     np.testing.assert_array_equal(s.step_scales, g.coeffs.step_scales)
     assert cf.coefficient_memory(0, g.cfg.step_geometry(), 1.0, g.wave.sample_rate,
                                  g.cfg.n_subbands, safety=1.5) >= 1
+
+
+def test_edfa_gain_and_ase_variance():
+    # pkg/tests/test_channel.py:102-126 on channel.edfa (host)
+    from paper_2409_14489_b200 import channel as ch
+    from paper_2409_14489_b200.config import DualPolWaveform
+    n, rate = 200_000, 64e9
+    w = DualPolWaveform(np.zeros(n, complex), np.zeros(n, complex), rate, 0.0)
+    out = ch.edfa(w, 16.0, 4.5, seed=(0, 1), carrier_hz=193.4e12)
+    expect = 6.62607015e-34 * 193.4e12 * (10 ** 1.6 * 10 ** 0.45 - 1) / 2 * rate
+    assert abs(np.mean(np.abs(out.x) ** 2) - expect) / expect < 0.02
+    assert abs(np.mean(np.abs(out.y) ** 2) - expect) / expect < 0.02
+    again = ch.edfa(w, 16.0, 4.5, seed=(0, 1), carrier_hz=193.4e12)
+    assert np.array_equal(out.x, again.x)
+    one = DualPolWaveform(np.ones(32, complex), np.zeros(32, complex), 1e9, 0.0)
+    assert np.allclose(ch.edfa(one, 20.0, 4.5, seed=0, noise_enabled=False).x, 10.0 * one.x,
+                       rtol=1e-12)
+    with pytest.raises(ValueError):
+        ch.edfa(one, -1.0, 4.5, seed=0)
+
+
+def test_sim_settings_xor():
+    from paper_2409_14489_b200 import channel as ch
+    with pytest.raises(ValueError):
+        ch.SimSettings(step_km=0.1, max_phase_rad=1e-3)
+    s = ch.SimSettings()
+    assert s.step_km == 0.1 and s.max_phase_rad is None
