@@ -164,9 +164,10 @@ cbessfm_status cbessfm_plan_update_sets(cbessfm_plan* plan, const double* mimo,
 /* Free the plan's device tables. */
 cbessfm_status cbessfm_plan_destroy(cbessfm_plan* plan);
 
-/* Debug: copy up to n phase timestamps (clock64) of CTA 0 of the last
- * launch into out. Only builds compiled with -DCB_PHASE_PROFILE record
- * them; other builds return 0. */
+/* Debug: copy up to n slots of the last launch's profile into out: 256
+ * phase timestamps (clock64) of CTA 0, then 3 per cluster c at 256 + 3c
+ * (globaltimer ns at start and end, SM id). Only builds compiled with
+ * -DCB_PHASE_PROFILE record them; other builds return 0. */
 int32_t cbessfm_debug_phase_times(const cbessfm_plan* plan, int64_t* out, int32_t n);
 
 /* Message of the last failing call on this thread ("" if none). */

@@ -97,6 +97,8 @@ struct cbessfm_plan {
 
 namespace {
 
+constexpr int kDbgSlots = 256 + 3 * 4096;  // phase clocks + per-cluster timeline
+
 // Round a complex double of (near-)unit modulus, scaled by an exact power of
 // two, to a float pair. Among the +-1 ulp neighbours of the nearest pair we
 // keep the one whose modulus is closest to the exact one: twiddles and
@@ -220,9 +222,9 @@ cbessfm_status upload_all(cbessfm_plan* p, const cbessfm_desc* d) {
   if ((e = upload_complex<R>(tp.data(), tp.size() / 2, &p->twp, true)) != cudaSuccess)
     return cuda_fail(e, "upload pass twiddles");
 #ifdef CB_PHASE_PROFILE
-  if ((e = cudaMalloc((void**)&p->dbg, 256 * sizeof(long long))) != cudaSuccess)
+  if ((e = cudaMalloc((void**)&p->dbg, kDbgSlots * sizeof(long long))) != cudaSuccess)
     return cuda_fail(e, "alloc phase clocks");
-  cudaMemset(p->dbg, 0, 256 * sizeof(long long));
+  cudaMemset(p->dbg, 0, kDbgSlots * sizeof(long long));
 #endif
   return CBESSFM_OK;
 }
@@ -537,7 +539,7 @@ const char* cbessfm_last_error(void) { return g_err.c_str(); }
 
 int32_t cbessfm_debug_phase_times(const cbessfm_plan* p, int64_t* out, int32_t n) {
   if (!p || !out || !p->dbg) return 0;
-  if (n > 256) n = 256;
+  if (n > kDbgSlots) n = kDbgSlots;
   return cudaMemcpy(out, p->dbg, sizeof(long long) * n, cudaMemcpyDeviceToHost) == cudaSuccess
              ? n
              : -1;

@@ -47,9 +47,27 @@ namespace cg = cooperative_groups;
   do {                                                                                \
     if (prm.dbg && blockIdx.x == 0 && threadIdx.x == 0 && (i) < 256) prm.dbg[(i)] = clock64(); \
   } while (0)
+// Per-cluster timeline (globaltimer ns at start / end of every cluster's
+// rank-0 CTA, and its SM) after the 256 phase slots: [256 + 3 c + {0,1,2}].
+#define CB_TIMELINE(slot)                                                              \
+  do {                                                                                 \
+    if (prm.dbg && (blockIdx.x % P) == 0 && threadIdx.x == 0 && cid < 4096) {          \
+      unsigned long long t;                                                            \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));                            \
+      prm.dbg[256 + 3 * cid + (slot)] = (long long)t;                                  \
+      if ((slot) == 0) {                                                               \
+        unsigned sm;                                                                   \
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));                                \
+        prm.dbg[256 + 3 * cid + 2] = sm;                                               \
+      }                                                                                \
+    }                                                                                  \
+  } while (0)
 #else
 #define CB_MARK(i) \
   do {             \
+  } while (0)
+#define CB_TIMELINE(slot) \
+  do {                    \
   } while (0)
 #endif
 
@@ -865,6 +883,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
   const Cx<R>* __restrict__ twpH = prm.twp + twp_base(Q, kHalf);  // half-length FFTs
 
   CB_MARK(0);
+  CB_TIMELINE(0);
   // ---- 1. load the polyphase component u[rank + P*t2] of the circular
   //         window starting at (b*keep - half) mod n (dbp.py:473-475)
   {
@@ -1135,6 +1154,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
   fft2<R, Q, NT, kTail, true>(F, twpT, &s_zero);
 
   CB_MARK(5);
+  CB_TIMELINE(1);
   // ---- 6. keep proc[half : half + span] (dbp.py:476-477)
   {
     const int64_t span = min(prm.keep, n - b * prm.keep);
