@@ -232,6 +232,22 @@ def main():
         np.savez_compressed(HERE / "nlpr_kat.npz", **arr)
         print("  wrote nlpr_kat.npz")
 
+    # --- configs[3] step counts 10 and 1 (rho 0.5) on the stored 50-span
+    #     waveform (wave_cfg4.npz, written by the cfg4_nsb5_st50 case)
+    for n_st, ov in ((10, 14290), (1, 10240)):
+        name = f"cfg4_nsb5_st{n_st}"
+        if not want(name):
+            continue
+        wv = np.load(HERE / "wave_cfg4.npz")
+        w4 = fd.DualPolWaveform(wv["x"], wv["y"], float(wv["sample_rate"]),
+                                float(wv["center_freq"]))
+        p4 = fd.WdmConfig(64e9, 5, 100e9, 0.05, "16-qam", 1.0).launch_power_w
+        cfg = fd.DbpConfig(link=link(50), variant="CB_ESSFM", n_steps=n_st,
+                           n_subbands=5, splitting_ratio=0.5, block_size=20480,
+                           overlap=ov, oversampling=1.6)
+        c = coeffs_for(cfg, w4.sample_rate, p4, 15)
+        save_case(name, w4, cfg, c, run(w4, cfg, c), wave="cfg4")
+
     # --- coefficient sets for the BASELINE.json configs[2] sweep grid
     #     (N_st x N_sb x rho on the configs[0] link and rate). The sweep's
     #     parity tests run the GPU and the oracle on the same set; taps are
