@@ -248,6 +248,35 @@ def main():
         c = coeffs_for(cfg, w4.sample_rate, p4, 15)
         save_case(name, w4, cfg, c, run(w4, cfg, c), wave="cfg4")
 
+    # --- optimize_coefficients (optimize.py:129-167) on a small noisy
+    #     training set: the batched-evaluation row's consumer
+    if want("optimize"):
+        lk = fd.LinkConfig(num_spans=2, span_length_km=80.0)
+        wdm = fd.WdmConfig(32e9, 1, 0.0, 0.05, "16-qam", 5.0)
+        train = fd.build_training_set(
+            lk, wdm, 512, sim=fd.SimSettings(max_phase_rad=5e-3, noise_enabled=True),
+            sim_rate_hz=64e9)
+        cfg = fd.DbpConfig(link=lk, variant="CB_ESSFM", n_steps=2, n_subbands=2,
+                           splitting_ratio=0.5, block_size=1024, overlap=0,
+                           oversampling=2.0)
+        init = coeffs_for(cfg, 64e9, wdm.launch_power_w, 3)
+        res = fd.optimize_coefficients(train, cfg, init)
+        arr = coeff_arrays(init)
+        arr = {"init_" + k: v for k, v in arr.items()}
+        arr.update({"res_" + k: v for k, v in coeff_arrays(res.coeffs).items()})
+        arr.update(tr_x=train.train_rx.x, tr_y=train.train_rx.y, va_x=train.val_rx.x,
+                   va_y=train.val_rx.y, tr_sym=train.train_record.channel(0),
+                   va_sym=train.val_record.channel(0), rate=train.train_rx.sample_rate,
+                   improved=res.improved, init_val_mse=res.init_val_mse,
+                   final_val_mse=res.final_val_mse, path=np.array(res.train_mse_path),
+                   baud=wdm.baud_rate, rolloff=wdm.rolloff,
+                   launch_power_w=wdm.launch_power_w,
+                   cfg_json=json.dumps(dict(num_spans=2, span_length_km=80.0, n_steps=2,
+                                            n_subbands=2, splitting_ratio=0.5,
+                                            block_size=1024, overlap=0, oversampling=2.0)))
+        np.savez_compressed(HERE / "optimize_small.npz", **arr)
+        print("  wrote optimize_small.npz")
+
     # --- coefficient sets for the BASELINE.json configs[2] sweep grid
     #     (N_st x N_sb x rho on the configs[0] link and rate). The sweep's
     #     parity tests run the GPU and the oracle on the same set; taps are
