@@ -74,6 +74,7 @@ std::vector<double> pass_tables(int Q, const std::vector<double>& tq, int real_b
   };
   fill(Q, kTail);
   fill(Q, kHead);
+  fill(Q, kMid);
   fill(Q / 2, kHalf);
   return out;
 }

@@ -128,6 +128,22 @@ __device__ __forceinline__ Cx<double> ldg(const Cx<double>* p) {
   return mk(v.x, v.y);
 }
 
+// Streaming loads of per-step tables (dispersion phasors, MIMO spectra):
+// each CTA reads a row once per step, so they bypass L1 allocation and
+// leave the 28 KB of L1 the shared-memory carveout leaves to the twiddle
+// rows every pass re-reads.
+__device__ __forceinline__ Cx<float> ldg_na(const Cx<float>* p) {
+  float a, b;
+  asm("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(a), "=f"(b) : "l"(p));
+  return mk(a, b);
+}
+__device__ __forceinline__ Cx<double> ldg_na(const Cx<double>* p) {
+  double a, b;
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "l"(p));
+  return mk(a, b);
+}
+#define CB_TW_LD "ld.global.nc.L1::evict_last"
+
 // Shared-memory index padding: one spare element every 16 complex entries
 // makes the radix-16 Stockham scatter (lane stride 16 elements) conflict-free.
 __device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
@@ -240,26 +256,41 @@ __device__ __forceinline__ void dft_reg(Cx<R>* v) {
 // coalesced), instead of R-1 scattered 8-byte loads.
 
 // Radix schedules (sub-transform sizes NS = 1, R1, R1*R2, ...):
-//   kTail -- radix-16 passes, leftover radix last  (2048: 16 16 8); used by
-//            the field IFFTs and the outer transforms
-//   kHead -- radix-16 passes, leftover radix first (2048: 8 16 16); used by
-//            the in-step field FFT, so its last pass (radix 16, NS = Q/16)
+//   kTail -- radix-16 passes, leftover radix last  (2048: 16 16 8); field
+//            IFFTs and outer transforms when twiddles come from L2
+//   kHead -- radix-16 passes, leftover radix first (2048: 8 16 16); the
+//            in-step field FFT, so its last pass (radix 16, NS = Q/16)
 //            produces exactly the 16 samples the next step's IFFT first pass
 //            (radix 16, NS = 1) consumes and the two fuse (fft2_boundary)
+//   kMid  -- radix 16 first and last, the leftover radix in between
+//            (2048: 16 8 16, 4096: 16 16 16): every field transform when the
+//            twiddles live in tensor memory. Forward and inverse then share
+//            one set of rows (the inverse conjugates them), which halves the
+//            TMEM columns a thread needs, and the boundary fusion still
+//            holds (last radix = first radix = 16). For Q <= 1024 its
+//            narrow middle pass runs several butterflies per thread and
+//            spills, so small Q keep kTail/kHead.
 //   kHalf -- radix-4 passes for the half-length real-transform FFTs, which
 //            keeps all Q/8 threads busy on Q/2 points
+// kTM may be or'ed into kMid or kHalf: that transform reads its twiddle
+// rows from tensor memory (see "Twiddle rows in tensor memory" below).
 #ifndef CB_HALF_RAD
 #define CB_HALF_RAD 4
 #endif
 constexpr int kMaxRad = 16;
-constexpr int kTail = 0, kHead = 1, kHalf = 2;
+constexpr int kTail = 0, kHead = 1, kHalf = 2, kMid = 3, kTM = 4;
 
 __host__ __device__ constexpr int sched_radix(int L, int ns, int sched) {
-  if (sched == kHalf) return L / ns >= CB_HALF_RAD ? CB_HALF_RAD : L / ns;
-  if (sched == kHead && ns == 1) {
+  const int sc = sched & 3;
+  if (sc == kHalf) return L / ns >= CB_HALF_RAD ? CB_HALF_RAD : L / ns;
+  if (sc == kHead && ns == 1) {
     int head = L;
     while (head > kMaxRad) head /= kMaxRad;
     return head;
+  }
+  if (sc == kMid && ns > 1 && L / ns > kMaxRad) {
+    const int mid = L / ns / kMaxRad;  // left once the last radix-16 pass is set aside
+    return mid >= kMaxRad ? kMaxRad : mid;
   }
   return L / ns >= kMaxRad ? kMaxRad : L / ns;
 }
@@ -270,13 +301,17 @@ __host__ __device__ constexpr int twp_offset(int L, int NS, int sched) {
   return s;
 }
 __host__ __device__ constexpr int twp_size(int L, int sched) { return twp_offset(L, L, sched); }
-// per-pass twiddle rows in Params::twp: [kTail rows of Q][kHead rows of Q][kHalf rows of Q/2]
+// per-pass twiddle rows in Params::twp:
+//   [kTail rows of Q][kHead rows of Q][kMid rows of Q][kHalf rows of Q/2]
 __host__ __device__ constexpr int twp_base(int Q, int sched) {
-  return sched == kTail ? 0 : sched == kHead ? twp_size(Q, kTail)
-                                             : twp_size(Q, kTail) + twp_size(Q, kHead);
+  const int sc = sched & 3;
+  return sc == kTail ? 0
+       : sc == kHead ? twp_size(Q, kTail)
+       : sc == kMid  ? twp_size(Q, kTail) + twp_size(Q, kHead)
+                     : twp_size(Q, kTail) + twp_size(Q, kHead) + twp_size(Q, kMid);
 }
 __host__ __device__ constexpr int twp_total(int Q) {
-  return twp_size(Q, kTail) + twp_size(Q, kHead) + twp_size(Q / 2, kHalf);
+  return twp_base(Q, kHalf) + twp_size(Q / 2, kHalf);
 }
 
 // Twiddle storage of one pass (NS rows k, radix RAD, entries r = 1..RAD-1)
@@ -294,7 +329,7 @@ __device__ __forceinline__ void load_row(const Cx<float>* tw, int k, Cx<float>* 
 #pragma unroll
   for (int q = 0; q < RAD / 2; ++q) {
     float a, b, c, d;
-    asm volatile("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];"
+    asm volatile(CB_TW_LD ".v4.f32 {%0, %1, %2, %3}, [%4];"
                  : "=f"(a), "=f"(b), "=f"(c), "=f"(d)
                  : "l"(tw + q * 2 * NS + 2 * k));
     w[2 * q + 1] = mk(a, b);
@@ -306,9 +341,208 @@ __device__ __forceinline__ void load_row(const Cx<double>* tw, int k, Cx<double>
 #pragma unroll
   for (int r = 1; r < RAD; ++r) {
     double a, b;
-    asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b)
+    asm volatile(CB_TW_LD ".v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b)
                  : "l"(tw + (r - 1) * NS + k));
     w[r] = mk(a, b);
+  }
+}
+
+// ------------------------------------------------------------------------
+// Twiddle rows in tensor memory.
+//
+// The block kernel has no matrix product, so the 256 KB of tensor memory
+// per SM would sit idle; it holds the FFT twiddle rows instead. Every
+// thread needs, for each pass, the same row(s) in every step (its butterfly
+// index is fixed), so at kernel start each thread copies its rows from the
+// L2 tables into its own TMEM lane, and each pass then reads them with one
+// or two tcgen05.ld (a private datapath) instead of RAD/2 16-byte loads
+// through the L1/TEX pipe that the shared-memory passes saturate, and
+// without the L2 latency (the 28 KB of L1 left by the shared-memory
+// carveout cannot hold the working set).
+//
+// TMEM lane = 32 * (warp % 4) + lane, so the NT/128 warps w, w+4, ... share
+// a lane. A pass whose row depends only on the lane stores one copy;
+// otherwise one copy per (warp group g = tid / 128, butterfly slot p).
+// Columns per CTA: 512 / (resident CTAs per SM); the launch sizes dynamic
+// shared memory so that no more CTAs than that can be resident, which keeps
+// the allocation from ever blocking (cbessfm_launch.cuh).
+
+template <int N>
+__device__ __forceinline__ void tm_ld(uint32_t a, uint32_t* v);
+template <int N>
+__device__ __forceinline__ void tm_st(uint32_t a, const uint32_t* v);
+template <>
+__device__ __forceinline__ void tm_ld<2>(uint32_t a, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n\t"
+               "tcgen05.wait::ld.sync.aligned;"
+               : "=r"(v[0]), "=r"(v[1])
+               : "r"(a));
+}
+template <>
+__device__ __forceinline__ void tm_st<2>(uint32_t a, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};"
+               :: "r"(a), "r"(v[0]), "r"(v[1])
+               : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_ld<4>(uint32_t a, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n\t"
+               "tcgen05.wait::ld.sync.aligned;"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(a));
+}
+template <>
+__device__ __forceinline__ void tm_st<4>(uint32_t a, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};"
+               :: "r"(a), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3])
+               : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_ld<8>(uint32_t a, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t"
+               "tcgen05.wait::ld.sync.aligned;"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(a));
+}
+template <>
+__device__ __forceinline__ void tm_st<8>(uint32_t a, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+               :: "r"(a), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_ld<16>(uint32_t a, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n\t"
+               "tcgen05.wait::ld.sync.aligned;"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+               : "r"(a));
+}
+template <>
+__device__ __forceinline__ void tm_st<16>(uint32_t a, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+               :: "r"(a), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+               : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_ld<32>(uint32_t a, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n\t"
+               "tcgen05.wait::ld.sync.aligned;"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+               : "r"(a));
+}
+template <>
+__device__ __forceinline__ void tm_st<32>(uint32_t a, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+               :: "r"(a), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+               : "memory");
+}
+
+// 32-bit words of one row (RAD-1 complex entries) and the columns it spans
+__host__ __device__ constexpr int tm_words(int rbytes, int rad) { return (rad - 1) * rbytes / 2; }
+__host__ __device__ constexpr int tm_width(int words) {
+  return words <= 2 ? 2 : words <= 4 ? 4 : words <= 8 ? 8 : (words + 15) / 16 * 16;
+}
+// Geometry of one pass of a field (kMid, L = Q) or half-length (kHalf,
+// L = Q/2) transform run by NT threads.
+struct TmPass {
+  int rad, per, dep_g, dep_p, copies, width;
+};
+__host__ __device__ constexpr TmPass tm_pass(int rbytes, int Q, int NT, int sched, int ns) {
+  const bool field = (sched & 3) != kHalf;
+  const int L = field ? Q : Q / 2;
+  const int rad = sched_radix(L, ns, sched);
+  const int slots = field ? NT / 2 : NT;
+  const int per = (L / rad) >= slots ? (L / rad) / slots : 1;
+  // field butterfly j = 64 g + 16 (warp % 4) + (tid % 16) + p NT/2;
+  // half-length j = 128 g + 32 (warp % 4) + lane + p NT (bfly() permutes
+  // inside 64-groups only)
+  const int dep_g = NT > 128 && ns > (field ? 64 : 128);
+  const int dep_p = per > 1 && ns > (field ? NT / 2 : NT);
+  const int g = NT > 128 ? NT / 128 : 1;
+  const int copies = (dep_g ? g : 1) * (dep_p ? per : 1);
+  return TmPass{rad, per, dep_g, dep_p, copies, tm_width(tm_words(rbytes, rad))};
+}
+// first TMEM column of pass (sched, NS): kMid passes, then kHalf passes
+__host__ __device__ constexpr int tm_col(int rbytes, int Q, int NT, int sched, int NS) {
+  int c = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    const int sc = pass == 0 ? kMid : kHalf;
+    const int L = pass == 0 ? Q : Q / 2;
+    for (int ns = 1; ns < L; ns *= sched_radix(L, ns, sc)) {
+      if (sc == (sched & 3) && ns == NS) return c;
+      if (ns > 1) {
+        const TmPass t = tm_pass(rbytes, Q, NT, sc, ns);
+        c += t.copies * t.width;
+      }
+    }
+  }
+  return c;
+}
+__host__ __device__ constexpr int tm_total(int rbytes, int Q, int NT) {
+  return tm_col(rbytes, Q, NT, kHalf, Q / 2);
+}
+
+// Copy index of the row thread `tid` uses in slot p of a pass.
+__device__ __forceinline__ int tm_copy(const TmPass& t, int tid, int p) {
+  const int g = t.dep_g ? tid >> 7 : 0;
+  return t.dep_p ? g * t.per + p : g;
+}
+__device__ __forceinline__ uint32_t tm_lane_base(uint32_t tbase) {
+  return tbase + ((uint32_t)((threadIdx.x >> 5) & 3) << 21);
+}
+
+template <typename R>
+__device__ __forceinline__ void tm_pack(const Cx<R>& c, uint32_t* v) {
+  if constexpr (sizeof(R) == 4) {
+    v[0] = __float_as_uint(c.x);
+    v[1] = __float_as_uint(c.y);
+  } else {
+    v[0] = __double2loint(c.x);
+    v[1] = __double2hiint(c.x);
+    v[2] = __double2loint(c.y);
+    v[3] = __double2hiint(c.y);
+  }
+}
+template <typename R>
+__device__ __forceinline__ Cx<R> tm_unpack(const uint32_t* v) {
+  if constexpr (sizeof(R) == 4) {
+    return mk(__uint_as_float(v[0]), __uint_as_float(v[1]));
+  } else {
+    return mk(__hiloint2double((int)v[1], (int)v[0]), __hiloint2double((int)v[3], (int)v[2]));
+  }
+}
+
+// Row (entries 1..RAD-1) from TMEM at column `col` of this thread's lane.
+template <typename R, int RAD>
+__device__ __forceinline__ void tm_load_row(uint32_t lane_base, int col, Cx<R>* w) {
+  constexpr int WORDS = tm_words((int)sizeof(R), RAD);
+  constexpr int W = tm_width(WORDS);
+  uint32_t v[W];
+  if constexpr (W <= 32) {
+    tm_ld<W>(lane_base + col, v);
+  } else {
+#pragma unroll
+    for (int c = 0; c < W; c += 32) tm_ld<32>(lane_base + col + c, v + c);
+  }
+  constexpr int CW = 2 * sizeof(R) / 4;
+#pragma unroll
+  for (int r = 1; r < RAD; ++r) w[r] = tm_unpack<R>(v + (r - 1) * CW);
+}
+template <typename R, int RAD>
+__device__ __forceinline__ void tm_store_row(uint32_t lane_base, int col, const Cx<R>* w) {
+  constexpr int WORDS = tm_words((int)sizeof(R), RAD);
+  constexpr int W = tm_width(WORDS);
+  constexpr int CW = 2 * sizeof(R) / 4;
+  uint32_t v[W];
+#pragma unroll
+  for (int i = 0; i < W; ++i) v[i] = 0u;
+#pragma unroll
+  for (int r = 1; r < RAD; ++r) tm_pack<R>(w[r], v + (r - 1) * CW);
+  if constexpr (W <= 32) {
+    tm_st<W>(lane_base + col, v);
+  } else {
+#pragma unroll
+    for (int c = 0; c < W; c += 32) tm_st<32>(lane_base + col + c, v + c);
   }
 }
 
@@ -402,7 +636,7 @@ struct PhasorHook : NoHook {
   template <typename, int RAD, int NS>
   __device__ __forceinline__ void post(int d0, Cx<R>* v) {
 #pragma unroll
-    for (int r = 0; r < RAD; ++r) v[bitrev<RAD>(r)] = cmul(v[bitrev<RAD>(r)], ldg(ph + d0 + r * NS));
+    for (int r = 0; r < RAD; ++r) v[bitrev<RAD>(r)] = cmul(v[bitrev<RAD>(r)], ldg_na(ph + d0 + r * NS));
   }
 };
 
@@ -516,9 +750,15 @@ __host__ __device__ constexpr int bfly(int t) {
 // Twiddle rows of the butterflies a thread runs in one pass. FIELD: the
 // field FFT mapping (butterfly fbase(t) + p * NT/2 of polarisation fpol(t));
 // otherwise the half-length mapping (butterfly bfly(t + p * NT)).
+// TMEM base address of this CTA's twiddle columns (kernels whose
+// schedules carry kTM allocate it, see tm_setup)
+__shared__ uint32_t cb_tm_base;
+
 template <typename R, int L, int NT, int NS, int SCHED>
 struct PassRows {
-  static constexpr bool kField = SCHED != kHalf;
+  static constexpr bool kField = (SCHED & 3) != kHalf;
+  static constexpr bool kTmem = (SCHED & kTM) != 0;
+  static constexpr int Q = kField ? L : 2 * L;
   static constexpr bool kLast = NS >= L;
   static constexpr int RAD = kLast ? 1 : sched_radix(L, NS, SCHED);
   static constexpr int SLOTS = kField ? NT / 2 : NT;  // threads per butterfly set
@@ -529,7 +769,23 @@ struct PassRows {
   // overlaps the current pass's stores, its barrier and the next pass's
   // shared-memory loads.
   __device__ __forceinline__ void fetch(const Cx<R>* twp) {
-    if constexpr (kHas) {
+    if constexpr (kHas && kTmem) {
+      constexpr TmPass tp = tm_pass((int)sizeof(R), Q, NT, SCHED, NS);
+      constexpr int col = tm_col((int)sizeof(R), Q, NT, SCHED, NS);
+      const uint32_t lb = tm_lane_base(cb_tm_base);
+      const int tid = threadIdx.x;
+      if constexpr (tp.dep_p) {
+#pragma unroll
+        for (int p = 0; p < PER; ++p)
+          tm_load_row<R, RAD>(lb, col + tm_copy(tp, tid, p) * tp.width, w[p]);
+      } else {
+        tm_load_row<R, RAD>(lb, col + tm_copy(tp, tid, 0) * tp.width, w[0]);
+#pragma unroll
+        for (int p = 1; p < PER; ++p)
+#pragma unroll
+          for (int r = 1; r < RAD; ++r) w[p][r] = w[0][r];
+      }
+    } else if constexpr (kHas) {
       const Cx<R>* tw = twp + twp_offset(L, NS, SCHED);
       const int tid = threadIdx.x;
 #pragma unroll
@@ -546,6 +802,42 @@ struct PassRows {
     }
   }
 };
+
+// Kernel-start copy of every pass's rows of schedules kMid and kHalf from
+// the L2 tables (twp, layout twp_base) into this CTA's TMEM columns: each
+// thread writes the copies it will read (lane-shared copies by the first
+// 128 threads only). Followed, in the caller, by wait::st, a fence and a
+// CTA barrier before any tm_load_row.
+template <typename R, int Q, int NT, int SCHED, int NS>
+__device__ __forceinline__ void tm_fill_sched(const Cx<R>* twp_sched) {
+  constexpr int L = (SCHED & 3) == kHalf ? Q / 2 : Q;
+  if constexpr (NS < L) {
+    constexpr int RAD = sched_radix(L, NS, SCHED);
+    if constexpr (NS > 1) {
+      constexpr TmPass tp = tm_pass((int)sizeof(R), Q, NT, SCHED, NS);
+      constexpr int col = tm_col((int)sizeof(R), Q, NT, SCHED, NS);
+      constexpr bool field = (SCHED & 3) != kHalf;
+      const Cx<R>* tw = twp_sched + twp_offset(L, NS, SCHED);
+      const uint32_t lb = tm_lane_base(cb_tm_base);
+      const int tid = threadIdx.x;
+      if (tp.copies > 1 || tid < 128) {
+#pragma unroll
+        for (int p = 0; p < (tp.dep_p ? tp.per : 1); ++p) {
+          int j;
+          if constexpr (field) {
+            j = fbase<NT>(tid) + p * (NT / 2);
+          } else {
+            j = (L / RAD) >= NT ? bfly<L, NS, RAD>(tid + p * NT) : tid;
+          }
+          Cx<R> w[RAD];
+          load_row<RAD, NS>(tw, j % NS, w);
+          tm_store_row<R, RAD>(lb, col + tm_copy(tp, tid, p) * tp.width, w);
+        }
+      }
+    }
+    tm_fill_sched<R, Q, NT, SCHED, NS * RAD>(twp_sched);
+  }
+}
 
 template <typename R, int Q, int NT, int SCHED, int NS, bool INV, bool FIRST, bool LAST,
           class Hook, class Rows, class NextRows>
@@ -631,25 +923,25 @@ __device__ __forceinline__ void fft2(Cx<R>* F, const Cx<R>* twp, const volatile 
   Fft2Run<R, Q, NT, SCHED, NS0, STOP, INV, Pre, Post>::run(F, twp, z, pre, post, rows);
 }
 
-// Step boundary: the last pass of the in-step forward FFT (kHead, radix R,
+// Step boundary: the last pass of the in-step forward FFT (kMid, radix R,
 // NS = Q/R), the next dispersion phasor, and the first pass of the next
-// step's IFFT (kTail, radix R, NS = 1) in one load/compute/store round: the
+// step's IFFT (kMid, radix R, NS = 1) in one load/compute/store round: the
 // forward butterfly j produces samples j + r*Q/R, exactly the inputs of
 // inverse butterfly j (dbp.py:398, :395, :396).
-template <typename R, int Q, int NT>
+template <typename R, int Q, int NT, int SI, int SFW>
 __device__ __forceinline__ void fft2_boundary(Cx<R>* __restrict__ F,
                                               const Cx<R>* __restrict__ twHead,
                                               const Cx<R>* __restrict__ ph,
                                               const volatile int* zero) {
-  constexpr int RAD = sched_radix(Q, 1, kTail);
+  constexpr int RAD = sched_radix(Q, 1, SI);
   constexpr int NSF = Q / RAD;  // forward last pass
-  static_assert(sched_radix(Q, NSF, kHead) == RAD, "kHead must end with kTail's first radix");
+  static_assert(sched_radix(Q, NSF, SFW) == RAD, "the forward FFT must end with the IFFT's first radix");
   constexpr int LR = Q / RAD;
   constexpr int SLOTS = NT / 2;
   static_assert((Q / RAD) % SLOTS == 0, "butterflies must tile the half-block");
   constexpr int PER = (Q / RAD) / SLOTS;
   constexpr int SF = padded_len(Q);
-  PassRows<R, Q, NT, NSF, kHead> rows;
+  PassRows<R, Q, NT, NSF, SFW> rows;
   rows.fetch(twHead);
   Cx<R> v[PER][RAD];
   const int tid = threadIdx.x + *zero;
@@ -668,7 +960,7 @@ __device__ __forceinline__ void fft2_boundary(Cx<R>* __restrict__ F,
     // and hand it to the inverse butterfly as its input r
     Cx<R> u[RAD];
 #pragma unroll
-    for (int r = 0; r < RAD; ++r) u[r] = cmul(v[p][bitrev<RAD>(r)], ldg(ph + j + r * LR));
+    for (int r = 0; r < RAD; ++r) u[r] = cmul(v[p][bitrev<RAD>(r)], ldg_na(ph + j + r * LR));
     dft_reg<R, RAD, true>(u);
 #pragma unroll
     for (int r = 0; r < RAD; ++r) v[p][r] = u[r];
@@ -689,10 +981,10 @@ __device__ __forceinline__ void fft2_boundary(Cx<R>* __restrict__ F,
 // synchronise between load and store with a named barrier, and a full
 // barrier ends the pass so no warp runs ahead into a later pass whose named
 // barrier expects a different thread count.
-template <typename R, int Q, int L, int NT, int NS, bool INV, class Rows, class NextRows>
+template <typename R, int Q, int L, int NT, int NS, bool INV, int HS, class Rows, class NextRows>
 __device__ __forceinline__ void fft1_pass(Cx<R>* __restrict__ buf, const Cx<R>* __restrict__ twp,
                                           const volatile int* zero, Rows& rows, NextRows& next) {
-  constexpr int RAD = sched_radix(L, NS, kHalf);
+  constexpr int RAD = sched_radix(L, NS, HS);
   constexpr int LR = L / RAD;
   constexpr int NB = L / RAD;
   const int tid = threadIdx.x + *zero;
@@ -740,27 +1032,28 @@ __device__ __forceinline__ void fft1_pass(Cx<R>* __restrict__ buf, const Cx<R>* 
   }
 }
 
-template <typename R, int Q, int L, int NT, int NS, bool INV>
+template <typename R, int Q, int L, int NT, int NS, bool INV, int HS>
 struct Fft1Run {
-  using Rows = PassRows<R, L, NT, NS, kHalf>;
+  using Rows = PassRows<R, L, NT, NS, HS>;
   static __device__ __forceinline__ void run(Cx<R>* buf, const Cx<R>* twp, const volatile int* z,
                                              Rows& rows) {
-    constexpr int NS2 = NS * sched_radix(L, NS, kHalf);
-    PassRows<R, L, NT, NS2, kHalf> next;
-    fft1_pass<R, Q, L, NT, NS, INV>(buf, twp, z, rows, next);
-    Fft1Run<R, Q, L, NT, NS2, INV>::run(buf, twp, z, next);
+    constexpr int NS2 = NS * sched_radix(L, NS, HS);
+    PassRows<R, L, NT, NS2, HS> next;
+    fft1_pass<R, Q, L, NT, NS, INV, HS>(buf, twp, z, rows, next);
+    Fft1Run<R, Q, L, NT, NS2, INV, HS>::run(buf, twp, z, next);
   }
 };
-template <typename R, int Q, int L, int NT, bool INV>
-struct Fft1Run<R, Q, L, NT, L, INV> {
+template <typename R, int Q, int L, int NT, bool INV, int HS>
+struct Fft1Run<R, Q, L, NT, L, INV, HS> {
   static __device__ __forceinline__ void run(Cx<R>*, const Cx<R>*, const volatile int*,
-                                             PassRows<R, L, NT, L, kHalf>&) {}
+                                             PassRows<R, L, NT, L, HS>&) {}
 };
 
-template <typename R, int Q, int L, int NT, bool INV>
+// Half-length FFT of buf (HS: kHalf, or kHalf | kTM with TMEM twiddles).
+template <typename R, int Q, int L, int NT, bool INV, int HS = kHalf>
 __device__ __forceinline__ void fft1(Cx<R>* buf, const Cx<R>* twp, const volatile int* z) {
-  PassRows<R, L, NT, 1, kHalf> none;
-  Fft1Run<R, Q, L, NT, 1, INV>::run(buf, twp, z, none);
+  PassRows<R, L, NT, 1, HS> none;
+  Fft1Run<R, Q, L, NT, 1, INV, HS>::run(buf, twp, z, none);
 }
 
 // ------------------------------------------------------------------------
@@ -806,6 +1099,28 @@ __host__ __device__ constexpr int min_blocks() {
              ? (sizeof(R) == 4 ? CB_FLOAT_THREADS : 512) / threads_for<R, Q>()
              : 1;
 }
+
+// TMEM columns per CTA: the whole 512 shared by the CTAs the register
+// budget makes resident (the launch enforces that residency with its shared
+// memory request). Transforms read their twiddles from TMEM when all rows
+// fit (FP32 and FP64 for Q = 2048 and 4096).
+#ifndef CB_NO_TMEM
+template <typename R, int Q>
+__host__ __device__ constexpr int tm_cols() {
+  int c = 32;
+  while (c * 2 * min_blocks<R, Q>() <= 512) c *= 2;
+  return c * min_blocks<R, Q>() <= 512 ? c : 0;
+}
+template <typename R, int Q>
+__host__ __device__ constexpr bool tm_on() {
+  return tm_cols<R, Q>() >= 32 && tm_total((int)sizeof(R), Q, threads_for<R, Q>()) <= tm_cols<R, Q>();
+}
+#else
+template <typename R, int Q>
+__host__ __device__ constexpr int tm_cols() { return 0; }
+template <typename R, int Q>
+__host__ __device__ constexpr bool tm_on() { return false; }
+#endif
 
 // MIMO slice of CTA c: bins [mimo_lo(c), mimo_lo(c+1)) of the H+1 rfft bins.
 __host__ __device__ constexpr int mimo_lo(int c, int P, int H) { return (c * (H + 1)) / P; }
@@ -866,6 +1181,29 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
       mbar_init_fence();
     }
   }
+  constexpr bool TMON = tm_on<R, Q>();
+  // field transforms: inverse (IFFT, outer) and forward (in-step FFT)
+  // schedules; half-length transforms
+  constexpr int FI = TMON ? (kMid | kTM) : kTail;
+  constexpr int FF = TMON ? (kMid | kTM) : kHead;
+  constexpr int HS = kHalf | (TMON ? kTM : 0);
+  if constexpr (TMON) {
+    // allocate this CTA's TMEM columns (warp 0) and copy the twiddle rows in
+    if (threadIdx.x < 32) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                   ::"r"(smem_addr(&cb_tm_base)), "n"(tm_cols<R, Q>()));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    tm_fill_sched<R, Q, NT, FI, 1>(prm.twp + twp_base(Q, kMid));
+    tm_fill_sched<R, Q, NT, HS, 1>(prm.twp + twp_base(Q, kHalf));
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    // the barrier after the block load orders these stores before every
+    // tcgen05.ld of another warp (fence::after_thread_sync there)
+  }
   const int tid = threadIdx.x;
   const int rank = (P > 1) ? (int)(blockIdx.x % P) : 0;
   const int64_t cid = prm.cid0 + blockIdx.x / P;
@@ -878,8 +1216,8 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
 
   const Cx<R>* __restrict__ twQ = prm.twQ;
   const Cx<R>* __restrict__ twN = prm.twN;
-  const Cx<R>* __restrict__ twpT = prm.twp + twp_base(Q, kTail);  // field IFFT / outer
-  const Cx<R>* __restrict__ twpF = prm.twp + twp_base(Q, kHead);  // in-step field FFT
+  const Cx<R>* __restrict__ twpT = prm.twp + twp_base(Q, FI);  // field IFFT / outer
+  const Cx<R>* __restrict__ twpF = prm.twp + twp_base(Q, FF);  // in-step field FFT
   const Cx<R>* __restrict__ twpH = prm.twp + twp_base(Q, kHalf);  // half-length FFTs
 
   CB_MARK(0);
@@ -900,6 +1238,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
     }
   }
   __syncthreads();
+  if constexpr (TMON) asm volatile("tcgen05.fence::after_thread_sync;");
 
   const size_t ph_tab = (size_t)P * Q;
   CB_MARK(1);
@@ -910,9 +1249,9 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
   if constexpr (P == 1) {
     PhasorHook<R> ph0;
     ph0.ph = prm.phasor + (size_t)prm.ph_index[0] * ph_tab;
-    fft2<R, Q, NT, kTail, false, NoHook, PhasorHook<R>>(F, twpT, &s_zero, NoHook(), ph0);
+    fft2<R, Q, NT, FI, false, NoHook, PhasorHook<R>>(F, twpT, &s_zero, NoHook(), ph0);
   } else {
-    fft2<R, Q, NT, kTail, false>(F, twpT, &s_zero);
+    fft2<R, Q, NT, FI, false>(F, twpT, &s_zero);
     // ---- 3. cross-subband radix-P stage over DSMEM: CTA c produces bins
     //         Q*k1 + k2 for k2 in its slice and every k1, and writes each to
     //         the CTA that owns it in the fftshift'd subband layout. Row 0's
@@ -971,7 +1310,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
   IntensityHook<R> ih;
   ih.I = Ireal;
   if (prm.n_steps > 0)
-    fft2<R, Q, NT, kTail, true, NoHook, IntensityHook<R>>(F, twpT, &s_zero, NoHook(), ih);
+    fft2<R, Q, NT, FI, true, NoHook, IntensityHook<R>>(F, twpT, &s_zero, NoHook(), ih);
   CB_MARK(3);
   constexpr int KU = (H / 2 + 1 + NT - 1) / NT;  // untangle/twist bins per thread
   for (int st = 0; st < prm.n_steps; ++st) {
@@ -983,7 +1322,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
       const int k = tid + u * NT;
       twk[u] = (k <= H / 2) ? ldg(twQ + k) : mk((R)1, (R)0);
     }
-    fft1<R, Q, H, NT, false>(IS, twpH, &s_zero);
+    fft1<R, Q, H, NT, false, HS>(IS, twpH, &s_zero);
     CB_MARK(8 + 8 * st + 0);
 
     // r2c untangle: I_hat[k], k = 0..H (numpy rfft, dbp.py:194). For P > 1
@@ -1036,7 +1375,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
       for (int k = lo + tid; k < hi; k += NT) {
         Cx<R> sv[P];
 #pragma unroll
-        for (int l = 0; l < P; ++l) sv[l] = ldg(mimo + (size_t)l * (H + 1) + k);
+        for (int l = 0; l < P; ++l) sv[l] = ldg_na(mimo + (size_t)l * (H + 1) + k);
         mbar_wait(&s_bar[0], st & 1);
         Cx<R> iv[P];
 #pragma unroll
@@ -1089,7 +1428,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
     }
     __syncthreads();
     CB_MARK(8 + 8 * st + 4);
-    fft1<R, Q, H, NT, true>(TS, twpH, &s_zero);
+    fft1<R, Q, H, NT, true, HS>(TS, twpH, &s_zero);
     CB_MARK(8 + 8 * st + 5);
 
     // rotation exp(-i theta) fused into the first pass of the subband FFT
@@ -1101,17 +1440,17 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
     rot.scale = theta_scale[st];
     const Cx<R>* ph_next = ph_rank + (size_t)prm.ph_index[st + 1] * ph_tab;
     if (st + 1 < prm.n_steps) {
-      fft2<R, Q, NT, kHead, false, RotationHook<R>, NoHook, 1, Q / sched_radix(Q, 1, kTail)>(
+      fft2<R, Q, NT, FF, false, RotationHook<R>, NoHook, 1, Q / sched_radix(Q, 1, FI)>(
           F, twpF, &s_zero, rot);
       CB_MARK(8 + 8 * st + 6);
-      fft2_boundary<R, Q, NT>(F, twpF, ph_next, &s_zero);
+      fft2_boundary<R, Q, NT, FI, FF>(F, twpF, ph_next, &s_zero);
       CB_MARK(8 + 8 * st + 7);
-      fft2<R, Q, NT, kTail, true, NoHook, IntensityHook<R>, sched_radix(Q, 1, kTail)>(
+      fft2<R, Q, NT, FI, true, NoHook, IntensityHook<R>, sched_radix(Q, 1, FI)>(
           F, twpT, &s_zero, NoHook(), ih);
     } else {
       PhasorHook<R> ph1;
       ph1.ph = ph_next;
-      fft2<R, Q, NT, kHead, false, RotationHook<R>, PhasorHook<R>>(F, twpF, &s_zero, rot, ph1);
+      fft2<R, Q, NT, FF, false, RotationHook<R>, PhasorHook<R>>(F, twpF, &s_zero, rot, ph1);
     }
   }
 
@@ -1151,7 +1490,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
     for (int t = tid; t < Q; t += NT) F[SF + pad(t)] = S[pad(t)];
     __syncthreads();
   }
-  fft2<R, Q, NT, kTail, true>(F, twpT, &s_zero);
+  fft2<R, Q, NT, FI, true>(F, twpT, &s_zero);
 
   CB_MARK(5);
   CB_TIMELINE(1);
@@ -1167,6 +1506,13 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
         dst[prm.out_pstride + obase + t] = F[SF + pad(t2)];
       }
     }
+  }
+  if constexpr (TMON) {
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (threadIdx.x < 32)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(cb_tm_base),
+                   "n"(tm_cols<R, Q>()));
   }
 }
 

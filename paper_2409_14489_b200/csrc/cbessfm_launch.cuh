@@ -25,12 +25,31 @@ cudaError_t launch_one(const Params<R>& prm, int64_t nclusters, cudaStream_t str
                        KernelInfo* info) {
   auto kern = cbessfm_block_kernel<R, P, Q>;
   constexpr int NT = threads_for<R, Q>();
-  const size_t smem = smem_bytes<R, Q>(P);
+  size_t smem = smem_bytes<R, Q>(P);
   // function attributes are per device; set them once per device
   static unsigned long long configured = 0;
+  static size_t smem_tm = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   const unsigned long long bit = 1ull << (dev & 63);
+  if constexpr (tm_on<R, Q>()) {
+    // TMEM twiddles: every resident CTA holds 512 / min_blocks columns, so
+    // no more than min_blocks CTAs of TMEM-using kernels may share an SM.
+    // Claiming 1/min_blocks of the SM's shared memory (the fields use most
+    // of it anyway) guarantees that for any mix of such kernels, and the
+    // tcgen05.alloc in the kernel never waits.
+    if (!smem_tm) {
+      int per_sm = 0, reserved = 0;
+      cudaFuncAttributes fa = {};
+      cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+      cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+      cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+      if (e != cudaSuccess) return e;
+      const size_t need = (size_t)per_sm / min_blocks<R, Q>() - (size_t)reserved - fa.sharedSizeBytes;
+      smem_tm = need > smem ? need : smem;
+    }
+    smem = smem_tm;
+  }
   if (!(__atomic_load_n(&configured, __ATOMIC_ACQUIRE) & bit)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);

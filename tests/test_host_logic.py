@@ -130,6 +130,39 @@ def test_pad_identity_used_by_kernel_addressing():
             ns *= R
 
 
+def _kmid_radices(L):
+    # csrc/cbessfm_kernel.cuh sched_radix(kMid): radix 16 first and last,
+    # the leftover in between
+    out, ns = [], 1
+    while ns < L:
+        if ns == 1 or L // ns <= 16:
+            r = min(16, L // ns)
+        else:
+            r = min(16, L // ns // 16)
+        out.append((ns, r))
+        ns *= r
+    return out
+
+
+def test_kmid_schedule_fuses_and_keeps_pad_identity():
+    pad = lambda i: i + (i >> 4)
+    assert [r for _, r in _kmid_radices(2048)] == [16, 8, 16]
+    assert [r for _, r in _kmid_radices(4096)] == [16, 16, 16]
+    assert [r for _, r in _kmid_radices(8192)] == [16, 16, 2, 16]
+    for L in (256, 512, 1024, 2048, 4096, 8192):
+        sched = _kmid_radices(L)
+        assert int(np.prod([r for _, r in sched])) == L
+        # the forward FFT's last pass and the IFFT's first are radix 16, so
+        # the step boundary fuses them (fft2_boundary)
+        assert sched[0][1] == 16 and sched[-1] == (L // 16, 16)
+        for ns, R in sched:
+            j = np.arange(L // R)
+            d0 = (j // ns) * ns * R + j % ns
+            for r in range(R):
+                assert np.all(pad(d0 + r * ns) == pad(d0) + pad(r * ns))
+                assert np.all(pad(j + r * (L // R)) == pad(j) + pad(r * (L // R)))
+
+
 @pytest.mark.parametrize("batch,nblk,world", [(1, 143, 8), (64, 1137, 8),
                                               (3, 10, 8), (8, 5, 8), (2, 7, 2),
                                               (1, 1, 4), (5, 3, 3)])
