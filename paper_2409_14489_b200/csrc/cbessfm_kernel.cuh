@@ -279,6 +279,10 @@ __device__ __forceinline__ void dft_reg(Cx<R>* v) {
 #endif
 constexpr int kMaxRad = 16;
 constexpr int kTail = 0, kHead = 1, kHalf = 2, kMid = 3, kTM = 4;
+// kStash (field schedules, one-block-per-CTA kernel): butterflies a thread
+// computes before the pass barrier are parked in TMEM instead of registers,
+// all but the last (see tm_stash_*)
+constexpr int kStash = 8;
 
 __host__ __device__ constexpr int sched_radix(int L, int ns, int sched) {
   const int sc = sched & 3;
@@ -605,6 +609,15 @@ __device__ __forceinline__ void bar_named(int id, int nthreads) {
 // stored with the complex padding.
 __device__ __forceinline__ int fpos(int p) { return 2 * pad(p >> 1) + (p & 1); }
 
+// Thread index inside the NT-thread group that runs one subband's
+// transforms: the whole CTA in the one-subband-per-CTA kernel, one of P
+// groups in the one-block-per-CTA kernel (NT a power of two; groups start
+// at multiples of NT, so lane and half-warp bits are unchanged).
+template <int NT>
+__device__ __forceinline__ int ltid() {
+  return (int)threadIdx.x & (NT - 1);
+}
+
 // ------------------------------------------------------------------------
 // Field FFT thread mapping: the two polarisations of a butterfly run on the
 // two half-warps (lane bit 4 selects x or y), so a thread holds one
@@ -669,14 +682,25 @@ __device__ __forceinline__ void sincos_acc(R a, R* s, R* c);
 // step, but legal) take the libdevice path.
 template <>
 __device__ __forceinline__ void sincos_acc<float>(float a, float* s, float* c) {
+  float r;
+  int q;
   if (fabsf(a) > 8192.0f) {
-    sincosf(a, s, c);
-    return;
+    // large arguments (never reached by a per-step nonlinear phase, but
+    // legal): reduce in FP64 (exact to ~1e-16 |a| for |a| < 2^31), no
+    // libdevice Payne-Hanek path with its local-memory table
+    const double ad = (double)a;
+    const double jd = rint(ad * 0.63661977236758134308);
+    double rd = fma(jd, -1.5707963267948966192, ad);
+    rd = fma(jd, -6.123233995736766036e-17, rd);
+    r = (float)rd;
+    q = (int)((long long)jd & 3);
+  } else {
+    const float j = rintf(a * 0.636619772367581343f);
+    r = __fmaf_rn(j, -0x1.921fb6p+0f, a);
+    r = __fmaf_rn(j, 0x1.777a5cp-25f, r);
+    r = __fmaf_rn(j, 0x1.ee59dap-50f, r);
+    q = __float2int_rn(j);
   }
-  const float j = rintf(a * 0.636619772367581343f);
-  float r = __fmaf_rn(j, -0x1.921fb6p+0f, a);
-  r = __fmaf_rn(j, 0x1.777a5cp-25f, r);
-  r = __fmaf_rn(j, 0x1.ee59dap-50f, r);
   const float r2 = r * r;
   float ps = __fmaf_rn(r2, -1.9515295891e-4f, 8.3321608736e-3f);
   ps = __fmaf_rn(r2, ps, -1.6666654611e-1f);
@@ -685,7 +709,6 @@ __device__ __forceinline__ void sincos_acc<float>(float a, float* s, float* c) {
   pc = __fmaf_rn(r2, pc, 4.166664568298827e-2f);
   pc = __fmaf_rn(r2, pc, -0.5f);
   const float cs = __fmaf_rn(r2, pc, 1.0f);
-  const int q = __float2int_rn(j);
   const float ss = (q & 1) ? cs : sn;
   const float cc = (q & 1) ? sn : cs;
   *s = (q & 2) ? -ss : ss;
@@ -750,6 +773,49 @@ __host__ __device__ constexpr int bfly(int t) {
 // Twiddle rows of the butterflies a thread runs in one pass. FIELD: the
 // field FFT mapping (butterfly fbase(t) + p * NT/2 of polarisation fpol(t));
 // otherwise the half-length mapping (butterfly bfly(t + p * NT)).
+// Butterfly parking for passes that run several butterflies per thread:
+// Stockham passes are in place, so every butterfly's outputs must be held
+// until the pass barrier; slots 0..PER-2 wait in TMEM (columns after the
+// twiddle rows, one block per sharer of the lane: threadIdx.x / 128).
+template <typename R, int RAD>
+__host__ __device__ constexpr int stash_width() {
+  return tm_width(RAD * 2 * (int)sizeof(R) / 4);
+}
+template <typename R, int RAD>
+__device__ __forceinline__ void tm_stash_store(uint32_t lane_base, int col, const Cx<R>* v) {
+  constexpr int W = stash_width<R, RAD>();
+  constexpr int CW = 2 * sizeof(R) / 4;
+  uint32_t u[W];
+#pragma unroll
+  for (int r = 0; r < RAD; ++r) tm_pack<R>(v[r], u + r * CW);
+  if constexpr (W <= 32) {
+    tm_st<W>(lane_base + col, u);
+  } else {
+#pragma unroll
+    for (int c = 0; c < W; c += 32) tm_st<32>(lane_base + col + c, u + c);
+  }
+}
+template <typename R, int RAD>
+__device__ __forceinline__ void tm_stash_load(uint32_t lane_base, int col, Cx<R>* v) {
+  constexpr int W = stash_width<R, RAD>();
+  constexpr int CW = 2 * sizeof(R) / 4;
+  uint32_t u[W];
+  if constexpr (W <= 32) {
+    tm_ld<W>(lane_base + col, u);
+  } else {
+#pragma unroll
+    for (int c = 0; c < W; c += 32) tm_ld<32>(lane_base + col + c, u + c);
+  }
+#pragma unroll
+  for (int r = 0; r < RAD; ++r) v[r] = tm_unpack<R>(u + r * CW);
+}
+// first stash column of slot p for this thread (COL0: first free column)
+template <typename R, int RAD, int PER>
+__device__ __forceinline__ int stash_col(int col0, int p) {
+  return col0 + ((int)threadIdx.x >> 7) * (PER - 1) * stash_width<R, RAD>() +
+         p * stash_width<R, RAD>();
+}
+
 // TMEM base address of this CTA's twiddle columns (kernels whose
 // schedules carry kTM allocate it, see tm_setup)
 __shared__ uint32_t cb_tm_base;
@@ -764,30 +830,16 @@ struct PassRows {
   static constexpr int SLOTS = kField ? NT / 2 : NT;  // threads per butterfly set
   static constexpr int PER = kLast ? 1 : ((L / RAD) >= SLOTS ? (L / RAD) / SLOTS : 1);
   static constexpr bool kHas = !kLast && NS > 1;
-  Cx<R> w[PER][RAD];
+  // L2 rows are prefetched for every slot; TMEM rows are read per slot just
+  // before use (short latency), so one row of registers suffices
+  Cx<R> w[kTmem ? 1 : PER][RAD];
   // Issue the loads (no use yet): called one pass early so the L2 latency
   // overlaps the current pass's stores, its barrier and the next pass's
-  // shared-memory loads.
+  // shared-memory loads. Nothing to do for TMEM rows.
   __device__ __forceinline__ void fetch(const Cx<R>* twp) {
-    if constexpr (kHas && kTmem) {
-      constexpr TmPass tp = tm_pass((int)sizeof(R), Q, NT, SCHED, NS);
-      constexpr int col = tm_col((int)sizeof(R), Q, NT, SCHED, NS);
-      const uint32_t lb = tm_lane_base(cb_tm_base);
-      const int tid = threadIdx.x;
-      if constexpr (tp.dep_p) {
-#pragma unroll
-        for (int p = 0; p < PER; ++p)
-          tm_load_row<R, RAD>(lb, col + tm_copy(tp, tid, p) * tp.width, w[p]);
-      } else {
-        tm_load_row<R, RAD>(lb, col + tm_copy(tp, tid, 0) * tp.width, w[0]);
-#pragma unroll
-        for (int p = 1; p < PER; ++p)
-#pragma unroll
-          for (int r = 1; r < RAD; ++r) w[p][r] = w[0][r];
-      }
-    } else if constexpr (kHas) {
+    if constexpr (kHas && !kTmem) {
       const Cx<R>* tw = twp + twp_offset(L, NS, SCHED);
-      const int tid = threadIdx.x;
+      const int tid = ltid<NT>();
 #pragma unroll
       for (int p = 0; p < PER; ++p) {
         if constexpr (kField) {
@@ -799,6 +851,19 @@ struct PassRows {
           if ((L / RAD) >= NT || t < L / RAD) load_row<RAD, NS>(tw, j % NS, w[p]);
         }
       }
+    }
+  }
+  // Row of slot p (TMEM: loaded here, warp-converged).
+  __device__ __forceinline__ const Cx<R>* row(int p) {
+    if constexpr (kHas && kTmem) {
+      constexpr TmPass tp = tm_pass((int)sizeof(R), Q, NT, SCHED, NS);
+      constexpr int col = tm_col((int)sizeof(R), Q, NT, SCHED, NS);
+      if (!tp.dep_p && p > 0) return w[0];
+      tm_load_row<R, RAD>(tm_lane_base(cb_tm_base), col + tm_copy(tp, ltid<NT>(), p) * tp.width,
+                          w[0]);
+      return w[0];
+    } else {
+      return w[kTmem ? 0 : p];
     }
   }
 };
@@ -819,8 +884,11 @@ __device__ __forceinline__ void tm_fill_sched(const Cx<R>* twp_sched) {
       constexpr bool field = (SCHED & 3) != kHalf;
       const Cx<R>* tw = twp_sched + twp_offset(L, NS, SCHED);
       const uint32_t lb = tm_lane_base(cb_tm_base);
-      const int tid = threadIdx.x;
-      if (tp.copies > 1 || tid < 128) {
+      const int tid = ltid<NT>();
+      // the first group of NT threads writes (the groups of the
+      // one-block-per-CTA kernel share lanes and rows); lane-shared copies
+      // only from its first 128 threads
+      if ((int)threadIdx.x < NT && (tp.copies > 1 || tid < 128)) {
 #pragma unroll
         for (int p = 0; p < (tp.dep_p ? tp.per : 1); ++p) {
           int j;
@@ -850,8 +918,10 @@ __device__ __forceinline__ void fft2_pass(Cx<R>* __restrict__ F, const Cx<R>* __
   static_assert((Q / RAD) % SLOTS == 0, "butterflies must tile the half-block");
   constexpr int PER = (Q / RAD) / SLOTS;
   constexpr int SF = padded_len(Q);
+  constexpr bool STASH = (SCHED & kStash) != 0 && PER > 1;
+  constexpr int SCOL = tm_total((int)sizeof(R), Q, NT);
   Cx<R> v[PER][RAD];
-  const int tid = threadIdx.x + *zero;
+  const int tid = ltid<NT>() + *zero;
   Cx<R>* Fp = F + fpol<NT>(tid) * SF;
   const int jb = fbase<NT>(tid);
 #pragma unroll
@@ -862,15 +932,26 @@ __device__ __forceinline__ void fft2_pass(Cx<R>* __restrict__ F, const Cx<R>* __
     for (int r = 0; r < RAD; ++r) v[p][r] = b[pad(r * LR)];
     if constexpr (FIRST) hook.template pre<R, RAD, LR>(j, v[p]);
     if constexpr (NS > 1) {
+      const Cx<R>* w = rows.row(p);
 #pragma unroll
-      for (int r = 1; r < RAD; ++r)
-        v[p][r] = INV ? cmulc(v[p][r], rows.w[p][r]) : cmul(v[p][r], rows.w[p][r]);
+      for (int r = 1; r < RAD; ++r) v[p][r] = INV ? cmulc(v[p][r], w[r]) : cmul(v[p][r], w[r]);
     }
     dft_reg<R, RAD, INV>(v[p]);
+    if constexpr (STASH) {
+      if (p < PER - 1)
+        tm_stash_store<R, RAD>(tm_lane_base(cb_tm_base), stash_col<R, RAD, PER>(SCOL, p), v[p]);
+    }
   }
+  if constexpr (STASH) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   __syncthreads();
 #pragma unroll
-  for (int p = 0; p < PER; ++p) {
+  for (int pp = 0; pp < PER; ++pp) {
+    // the register-resident last slot first, then the parked ones
+    const int p = STASH ? (pp == 0 ? PER - 1 : pp - 1) : pp;
+    if constexpr (STASH) {
+      if (pp > 0)
+        tm_stash_load<R, RAD>(tm_lane_base(cb_tm_base), stash_col<R, RAD, PER>(SCOL, p), v[p]);
+    }
     const int j = jb + p * SLOTS;
     const int d0 = (j / NS) * NS * RAD + j % NS;
     if constexpr (LAST) hook.template post<R, RAD, NS>(d0, v[p]);
@@ -941,10 +1022,12 @@ __device__ __forceinline__ void fft2_boundary(Cx<R>* __restrict__ F,
   static_assert((Q / RAD) % SLOTS == 0, "butterflies must tile the half-block");
   constexpr int PER = (Q / RAD) / SLOTS;
   constexpr int SF = padded_len(Q);
+  constexpr bool STASH = (SFW & kStash) != 0 && PER > 1;
+  constexpr int SCOL = tm_total((int)sizeof(R), Q, NT);
   PassRows<R, Q, NT, NSF, SFW> rows;
   rows.fetch(twHead);
   Cx<R> v[PER][RAD];
-  const int tid = threadIdx.x + *zero;
+  const int tid = ltid<NT>() + *zero;
   Cx<R>* Fp = F + fpol<NT>(tid) * SF;
   const int jb = fbase<NT>(tid);
 #pragma unroll
@@ -953,8 +1036,11 @@ __device__ __forceinline__ void fft2_boundary(Cx<R>* __restrict__ F,
     const Cx<R>* b = Fp + pad(j);
 #pragma unroll
     for (int r = 0; r < RAD; ++r) v[p][r] = b[pad(r * LR)];
+    {
+      const Cx<R>* w = rows.row(p);
 #pragma unroll
-    for (int r = 1; r < RAD; ++r) v[p][r] = cmul(v[p][r], rows.w[p][r]);
+      for (int r = 1; r < RAD; ++r) v[p][r] = cmul(v[p][r], w[r]);
+    }
     dft_reg<R, RAD, false>(v[p]);
     // natural output r sits at j + r*LR in v[bitrev(r)]: apply the phasor
     // and hand it to the inverse butterfly as its input r
@@ -964,10 +1050,20 @@ __device__ __forceinline__ void fft2_boundary(Cx<R>* __restrict__ F,
     dft_reg<R, RAD, true>(u);
 #pragma unroll
     for (int r = 0; r < RAD; ++r) v[p][r] = u[r];
+    if constexpr (STASH) {
+      if (p < PER - 1)
+        tm_stash_store<R, RAD>(tm_lane_base(cb_tm_base), stash_col<R, RAD, PER>(SCOL, p), v[p]);
+    }
   }
+  if constexpr (STASH) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   __syncthreads();
 #pragma unroll
-  for (int p = 0; p < PER; ++p) {
+  for (int pp = 0; pp < PER; ++pp) {
+    const int p = STASH ? (pp == 0 ? PER - 1 : pp - 1) : pp;
+    if constexpr (STASH) {
+      if (pp > 0)
+        tm_stash_load<R, RAD>(tm_lane_base(cb_tm_base), stash_col<R, RAD, PER>(SCOL, p), v[p]);
+    }
     const int j = jb + p * SLOTS;
     Cx<R>* b = Fp + pad(j * RAD);  // inverse first pass: NS = 1, d0 = R*j
 #pragma unroll
@@ -987,7 +1083,7 @@ __device__ __forceinline__ void fft1_pass(Cx<R>* __restrict__ buf, const Cx<R>* 
   constexpr int RAD = sched_radix(L, NS, HS);
   constexpr int LR = L / RAD;
   constexpr int NB = L / RAD;
-  const int tid = threadIdx.x + *zero;
+  const int tid = ltid<NT>() + *zero;
   auto body_load = [&](int j, Cx<R>* v, const Cx<R>* w) {
     const Cx<R>* b = buf + pad(j);
 #pragma unroll
@@ -1008,7 +1104,7 @@ __device__ __forceinline__ void fft1_pass(Cx<R>* __restrict__ buf, const Cx<R>* 
     constexpr int PER = NB / NT;
     Cx<R> v[PER][RAD];
 #pragma unroll
-    for (int p = 0; p < PER; ++p) body_load(bfly<L, NS, RAD>(tid + p * NT), v[p], rows.w[p]);
+    for (int p = 0; p < PER; ++p) body_load(bfly<L, NS, RAD>(tid + p * NT), v[p], rows.row(p));
     __syncthreads();
 #pragma unroll
     for (int p = 0; p < PER; ++p) body_store(bfly<L, NS, RAD>(tid + p * NT), v[p]);
@@ -1023,7 +1119,8 @@ __device__ __forceinline__ void fft1_pass(Cx<R>* __restrict__ buf, const Cx<R>* 
     if (tid < ACT) {
       Cx<R> v[RAD];
       const bool on = (NB % 32 == 0) || tid < NB;
-      if (on) body_load(tid, v, rows.w[0]);
+      const Cx<R>* w = rows.row(0);  // warp-converged (TMEM)
+      if (on) body_load(tid, v, w);
       bar_named(1, ACT);
       if (on) body_store(tid, v);
     }
@@ -1104,6 +1201,13 @@ __host__ __device__ constexpr int min_blocks() {
 // budget makes resident (the launch enforces that residency with its shared
 // memory request). Transforms read their twiddles from TMEM when all rows
 // fit (FP32 and FP64 for Q = 2048 and 4096).
+__host__ __device__ constexpr bool defined_no_tmem() {
+#ifdef CB_NO_TMEM
+  return true;
+#else
+  return false;
+#endif
+}
 #ifndef CB_NO_TMEM
 template <typename R, int Q>
 __host__ __device__ constexpr int tm_cols() {
@@ -1513,6 +1617,321 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
     if (threadIdx.x < 32)
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(cb_tm_base),
                    "n"(tm_cols<R, Q>()));
+  }
+}
+
+
+// ------------------------------------------------------------------------
+// One-block-per-CTA variant.
+//
+// With P subbands of Q = 2048 samples the P-CTA cluster kernel above holds
+// 4 clusters' CTAs per SM, so one configs[1] waveform (143 blocks) needs two
+// rounds and the second runs a quarter full. Here one CTA holds a whole
+// overlap-save block: P groups of Q/16 threads, group s owning subband s
+// (both polarisation rows and its intensity buffer, P * 43.5 KB of shared
+// memory for P = 5), so one CTA fills an SM and 143 blocks run in one round
+// on 148 SMs. The cross-subband steps need no cluster: the outer radix-P
+// stages read all subbands from local shared memory (registers carry the
+// inputs across one barrier, so no staging row is needed), and the MIMO
+// reads every subband's intensity spectrum in place -- no DSMEM pushes, no
+// mbarrier waits. Each thread runs two radix-16 butterflies per pass
+// (96-register budget); the twiddle rows sit in TMEM as above (the P groups
+// share lanes and rows).
+
+template <typename R, int P, int Q>
+__host__ __device__ constexpr size_t fat_smem_bytes() {
+  return sizeof(Cx<R>) * (size_t)P * (2 * padded_len(Q) + padded_len(Q / 2 + 1));
+}
+template <typename R, int P, int Q>
+__host__ __device__ constexpr bool fat_ok() {
+#ifdef CB_NO_FAT
+  return false;
+#else
+  // float, Q = 2048 (radix-4 half-length passes keep every group thread
+  // busy), P subbands that fit one SM's shared memory
+  return sizeof(R) == 4 && Q == 2048 && P >= 2 && fat_smem_bytes<R, P, Q>() <= 232448 - 1024;
+#endif
+}
+template <int Q>
+__host__ __device__ constexpr int fat_group() {
+  return Q / 16;
+}
+__host__ __device__ constexpr int pow2_cols(int c) {
+  int a = 32;
+  while (a < c) a *= 2;
+  return a;
+}
+
+template <typename R, int P, int Q>
+__global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(const Params<R> prm) {
+  constexpr int NT = fat_group<Q>();  // threads per subband group
+  constexpr int NTC = P * NT;         // threads per CTA
+  constexpr int H = Q / 2;
+  constexpr int SF = padded_len(Q);
+  constexpr int SG = 2 * SF + padded_len(H + 1);  // shared entries per group
+  static_assert(NT % 128 == 0, "groups must start on a TMEM lane quarter");
+  static_assert((H / CB_HALF_RAD) >= NT, "half-length passes must keep every thread busy");
+  // TMEM: twiddle rows, then the butterfly parking of the P*NT/128 lane
+  // sharers (at most 3 radix-8 or 1 radix-16 butterfly each)
+  constexpr int STASH_W = 3 * stash_width<R, 8>() > stash_width<R, 16>() ? 3 * stash_width<R, 8>()
+                                                                           : stash_width<R, 16>();
+  constexpr int TM_NEED = tm_total((int)sizeof(R), Q, NT) + (NTC / 128) * STASH_W;
+  constexpr bool TMON = !defined_no_tmem() && TM_NEED <= 512;
+  constexpr int COLS = pow2_cols(TM_NEED);
+  constexpr int FI = TMON ? (kMid | kTM | kStash) : kTail;
+  constexpr int FF = TMON ? (kMid | kTM | kStash) : kHead;
+  constexpr int HS = kHalf | (TMON ? kTM : 0);
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Cx<R>* const base = reinterpret_cast<Cx<R>*>(smem_raw);
+  const int grp = (int)threadIdx.x / NT;  // subband of this thread's group
+  const int tid = ltid<NT>();
+  Cx<R>* F = base + grp * SG;
+  Cx<R>* IS = F + 2 * SF;
+  Cx<R>* TS = IS;
+  __shared__ int s_zero;
+  if (threadIdx.x == 0) s_zero = 0;
+  if constexpr (TMON) {
+    if (threadIdx.x < 32) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                   ::"r"(smem_addr(&cb_tm_base)), "n"(COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    tm_fill_sched<R, Q, NT, FI, 1>(prm.twp + twp_base(Q, kMid));
+    tm_fill_sched<R, Q, NT, HS, 1>(prm.twp + twp_base(Q, kHalf));
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+  }
+  const int64_t cid = prm.cid0 + blockIdx.x;
+  const int64_t wv = cid / prm.nb;
+  const int64_t b = prm.b0 + cid % prm.nb;
+  const int64_t n = prm.n;
+  const int64_t cset = prm.n_sets > 1 ? wv % prm.n_sets : 0;
+  const Cx<R>* __restrict__ mimo = prm.mimo + cset * (int64_t)P * (H + 1);
+  const R* __restrict__ theta_scale = prm.theta_scale + cset * prm.n_steps;
+  const Cx<R>* __restrict__ twQ = prm.twQ;
+  const Cx<R>* __restrict__ twN = prm.twN;
+  const Cx<R>* __restrict__ twpT = prm.twp + twp_base(Q, FI);
+  const Cx<R>* __restrict__ twpF = prm.twp + twp_base(Q, FF);
+  const Cx<R>* __restrict__ twpH = prm.twp + twp_base(Q, kHalf);
+
+  // ---- 1. group s loads the polyphase component u[s + P*t2] of the
+  //         circular window starting at (b*keep - half) mod n (dbp.py:473-475)
+  {
+    int64_t start = (b * prm.keep - prm.half) % n;
+    if (start < 0) start += n;
+    start -= prm.in_origin;
+    if (start < 0) start += n;
+    const Cx<R>* src = prm.in + wv * prm.in_bstride;
+    for (int t2 = tid; t2 < Q; t2 += NT) {
+      int64_t idx = start + grp + (int64_t)P * t2;
+      if (idx >= n) idx -= n;
+      F[pad(t2)] = src[idx];
+      F[SF + pad(t2)] = src[prm.in_pstride + idx];
+    }
+  }
+  __syncthreads();
+  if constexpr (TMON) asm volatile("tcgen05.fence::after_thread_sync;");
+
+  // ---- 2.-3. outer transform (dbp.py:387-389): FFT_Q per subband, then
+  //         the radix-P stage across subbands. Thread-strided over k2: the P
+  //         inputs Q*k1 + k2 are read into registers, a barrier, then the P
+  //         outputs (x 1/P x first phasor) go to their subband homes in place.
+  fft2<R, Q, NT, FI, false>(F, twpT, &s_zero);
+  constexpr int KPT = (Q + NTC - 1) / NTC;
+  const R invP = (R)1 / (R)P;
+  const Cx<R>* ph0 = prm.phasor + (size_t)prm.ph_index[0] * (size_t)P * Q;
+  for (int pol = 0; pol < 2; ++pol) {
+    Cx<R> bv[KPT][P];
+#pragma unroll
+    for (int u = 0; u < KPT; ++u) {
+      const int k2 = (int)threadIdx.x + u * NTC;
+      if (k2 < Q) {
+#pragma unroll
+        for (int r = 0; r < P; ++r) {
+          Cx<R> v = base[r * SG + pol * SF + pad(k2)];
+          if (r) v = cmul(v, ldg(twN + r * k2));
+          bv[u][r] = v;
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < KPT; ++u) {
+      const int k2 = (int)threadIdx.x + u * NTC;
+      if (k2 < Q) {
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) {
+          Cx<R> sm = bv[u][0];
+#pragma unroll
+          for (int r = 1; r < P; ++r) sm = sm + cmul(bv[u][r], ldg(twN + ((r * k1) % P) * Q));
+          int i, m;
+          bin_home<P, Q>(Q * k1 + k2, i, m);
+          base[i * SG + pol * SF + pad(m)] = cmul(scale(sm, invP), ldg(ph0 + (size_t)i * Q + m));
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- 4. nonlinear steps (dbp.py:394-398), as in the cluster kernel
+  const Cx<R>* ph_grp = prm.phasor + (size_t)grp * Q;
+  const size_t ph_tab = (size_t)P * Q;
+  R* Ireal = reinterpret_cast<R*>(IS);
+  const R* Treal = reinterpret_cast<const R*>(TS);
+  IntensityHook<R> ih;
+  ih.I = Ireal;
+  if (prm.n_steps > 0)
+    fft2<R, Q, NT, FI, true, NoHook, IntensityHook<R>>(F, twpT, &s_zero, NoHook(), ih);
+  constexpr int KU = (H / 2 + 1 + NT - 1) / NT;
+  for (int st = 0; st < prm.n_steps; ++st) {
+    Cx<R> twk[KU];
+#pragma unroll
+    for (int u = 0; u < KU; ++u) {
+      const int k = tid + u * NT;
+      twk[u] = (k <= H / 2) ? ldg(twQ + k) : mk((R)1, (R)0);
+    }
+    fft1<R, Q, H, NT, false, HS>(IS, twpH, &s_zero);
+    // r2c untangle in place: I_hat[k], k = 0..H (numpy rfft, dbp.py:194)
+#pragma unroll
+    for (int u = 0; u < KU; ++u) {
+      const int k = tid + u * NT;
+      if (k > H / 2) break;
+      if (k == 0) {
+        const Cx<R> z = IS[pad(0)];
+        IS[pad(0)] = mk(z.x + z.y, (R)0);
+        IS[pad(H)] = mk(z.x - z.y, (R)0);
+      } else {
+        const Cx<R> a = IS[pad(k)];
+        const Cx<R> bq = conj(IS[pad(H - k)]);
+        const Cx<R> e = scale(a + bq, (R)0.5);
+        const Cx<R> dd = a - bq;
+        const Cx<R> o = mk(dd.y * (R)0.5, -dd.x * (R)0.5);
+        const Cx<R> wo = cmul(o, twk[u]);
+        IS[pad(k)] = e + wo;
+        if (k != H - k) IS[pad(H - k)] = conj(e - wo);
+      }
+    }
+    __syncthreads();
+    // MIMO coupling (dbp.py:195) in place: bin k of every subband, one
+    // thread per bin
+    for (int k = (int)threadIdx.x; k <= H; k += NTC) {
+      Cx<R> sv[P], iv[P];
+#pragma unroll
+      for (int l = 0; l < P; ++l) sv[l] = ldg_na(mimo + (size_t)l * (H + 1) + k);
+#pragma unroll
+      for (int l = 0; l < P; ++l) iv[l] = base[l * SG + 2 * SF + pad(k)];
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        Cx<R> acc = mk((R)0, (R)0);
+#pragma unroll
+        for (int l = 0; l < P; ++l)
+          acc = acc + (l >= i ? cmul(sv[l - i], iv[l]) : cmul(conj(sv[i - l]), iv[l]));
+        base[i * SG + 2 * SF + pad(k)] = acc;
+      }
+    }
+    __syncthreads();
+    // c2r pre-twist in place (numpy irfft ignores Im of bins 0 and H)
+#pragma unroll
+    for (int u = 0; u < KU; ++u) {
+      const int k = tid + u * NT;
+      if (k > H / 2) break;
+      if (k == 0) {
+        const R x0 = TS[pad(0)].x, xh = TS[pad(H)].x;
+        TS[pad(0)] = mk(x0 + xh, x0 - xh);
+      } else {
+        const Cx<R> a = TS[pad(k)];
+        const Cx<R> c = conj(TS[pad(H - k)]);
+        const Cx<R> wk = twk[u];
+        const Cx<R> s2 = a + c;
+        const Cx<R> dd = cmulc(a - c, wk);
+        TS[pad(k)] = mk(s2.x - dd.y, s2.y + dd.x);
+        if (k != H - k) {
+          const Cx<R> a2 = conj(c);
+          const Cx<R> c2 = conj(a);
+          const Cx<R> s3 = a2 + c2;
+          const Cx<R> w2 = mk(-wk.x, wk.y);
+          const Cx<R> d2 = cmulc(a2 - c2, w2);
+          TS[pad(H - k)] = mk(s3.x - d2.y, s3.y + d2.x);
+        }
+      }
+    }
+    __syncthreads();
+    fft1<R, Q, H, NT, true, HS>(TS, twpH, &s_zero);
+    RotationHook<R> rot;
+    rot.th = Treal;
+    rot.scale = theta_scale[st];
+    const Cx<R>* ph_next = ph_grp + (size_t)prm.ph_index[st + 1] * ph_tab;
+    if (st + 1 < prm.n_steps) {
+      fft2<R, Q, NT, FF, false, RotationHook<R>, NoHook, 1, Q / sched_radix(Q, 1, FI)>(
+          F, twpF, &s_zero, rot);
+      fft2_boundary<R, Q, NT, FI, FF>(F, twpF, ph_next, &s_zero);
+      fft2<R, Q, NT, FI, true, NoHook, IntensityHook<R>, sched_radix(Q, 1, FI)>(
+          F, twpT, &s_zero, NoHook(), ih);
+    } else {
+      PhasorHook<R> ph1;
+      ph1.ph = ph_next;
+      fft2<R, Q, NT, FF, false, RotationHook<R>, PhasorHook<R>>(F, twpF, &s_zero, rot, ph1);
+    }
+  }
+
+  // ---- 5. merge + outer IFFT (dbp.py:400-401): inverse radix-P stage in
+  //         place (registers across one barrier), then FFT_Q^-1 per group
+  for (int pol = 0; pol < 2; ++pol) {
+    Cx<R> xv[KPT][P];
+#pragma unroll
+    for (int u = 0; u < KPT; ++u) {
+      const int k2 = (int)threadIdx.x + u * NTC;
+      if (k2 < Q) {
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) {
+          int i, m;
+          bin_home<P, Q>(Q * k1 + k2, i, m);
+          xv[u][k1] = base[i * SG + pol * SF + pad(m)];
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < KPT; ++u) {
+      const int k2 = (int)threadIdx.x + u * NTC;
+      if (k2 < Q) {
+#pragma unroll
+        for (int n1 = 0; n1 < P; ++n1) {
+          Cx<R> sm = xv[u][0];
+#pragma unroll
+          for (int k1 = 1; k1 < P; ++k1) sm = sm + cmulc(xv[u][k1], ldg(twN + ((n1 * k1) % P) * Q));
+          if (n1) sm = cmulc(sm, ldg(twN + n1 * k2));
+          base[n1 * SG + pol * SF + pad(k2)] = sm;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  fft2<R, Q, NT, FI, true>(F, twpT, &s_zero);
+
+  // ---- 6. keep proc[half : half + span] (dbp.py:476-477)
+  {
+    const int64_t span = min(prm.keep, n - b * prm.keep);
+    Cx<R>* dst = prm.out + wv * prm.out_bstride;
+    const int64_t obase = b * prm.keep - prm.half - prm.out_origin;
+    for (int t2 = tid; t2 < Q; t2 += NT) {
+      const int64_t t = grp + (int64_t)P * t2;
+      if (t >= prm.half && t < prm.half + span) {
+        dst[obase + t] = F[pad(t2)];
+        dst[prm.out_pstride + obase + t] = F[SF + pad(t2)];
+      }
+    }
+  }
+  if constexpr (TMON) {
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (threadIdx.x < 32)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(cb_tm_base),
+                   "n"(COLS));
   }
 }
 

@@ -20,9 +20,62 @@ constexpr int max_q() {
   return sizeof(R) == 4 ? 8192 : 4096;
 }
 
+// One-block-per-CTA kernel (cbessfm_fat_kernel): one CTA of P * Q/16
+// threads per overlap-save block, no cluster. Used where fat_ok() holds
+// unless CBESSFM_KERNEL=cluster.
+template <typename R, int P, int Q>
+cudaError_t launch_fat(const Params<R>& prm, int64_t nblocks, cudaStream_t stream,
+                       KernelInfo* info) {
+  auto kern = cbessfm_fat_kernel<R, P, Q>;
+  constexpr int NT = P * fat_group<Q>();
+  constexpr size_t smem = fat_smem_bytes<R, P, Q>();
+  static unsigned long long configured = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(__atomic_load_n(&configured, __ATOMIC_ACQUIRE) & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
+    __atomic_fetch_or(&configured, bit, __ATOMIC_RELEASE);
+  }
+  if (info) {
+    info->threads = NT;
+    info->cluster = 1;
+    info->smem = smem;
+    int per_sm = 0, sms = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
+    if (e != cudaSuccess) return e;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    info->max_active_clusters = per_sm * sms;
+    if (nblocks == 0) return cudaSuccess;
+  }
+  const int64_t max_blocks = 0x7fffffff;
+  Params<R> p = prm;
+  for (int64_t c0 = 0; c0 < nblocks; c0 += max_blocks) {
+    const int64_t nc = nblocks - c0 < max_blocks ? nblocks - c0 : max_blocks;
+    p.cid0 = prm.cid0 + c0;
+    kern<<<dim3((unsigned)nc), dim3(NT), smem, stream>>>(p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+inline bool use_cluster_kernel() {
+  const char* env = getenv("CBESSFM_KERNEL");
+  return env && env[0] == 'c';
+}
+
 template <typename R, int P, int Q>
 cudaError_t launch_one(const Params<R>& prm, int64_t nclusters, cudaStream_t stream,
                        KernelInfo* info) {
+  if constexpr (fat_ok<R, P, Q>()) {
+    if (!use_cluster_kernel()) return launch_fat<R, P, Q>(prm, nclusters, stream, info);
+  }
   auto kern = cbessfm_block_kernel<R, P, Q>;
   constexpr int NT = threads_for<R, Q>();
   size_t smem = smem_bytes<R, Q>(P);
@@ -45,7 +98,10 @@ cudaError_t launch_one(const Params<R>& prm, int64_t nclusters, cudaStream_t str
       cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
       cudaError_t e = cudaFuncGetAttributes(&fa, kern);
       if (e != cudaSuccess) return e;
-      const size_t need = (size_t)per_sm / min_blocks<R, Q>() - (size_t)reserved - fa.sharedSizeBytes;
+      // (1 KB below the exact share: the occupancy calculator treats an
+      // exactly full SM as one CTA short)
+      const size_t need =
+          (size_t)per_sm / min_blocks<R, Q>() - (size_t)reserved - fa.sharedSizeBytes - 1024;
       smem_tm = need > smem ? need : smem;
     }
     smem = smem_tm;
@@ -56,6 +112,11 @@ cudaError_t launch_one(const Params<R>& prm, int64_t nclusters, cudaStream_t str
     if (e != cudaSuccess) return e;
     if (P > 8) {
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    if constexpr (tm_on<R, Q>()) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
       if (e != cudaSuccess) return e;
     }
     __atomic_fetch_or(&configured, bit, __ATOMIC_RELEASE);
