@@ -287,6 +287,35 @@ def ncu_traffic(dtype: str):
     return None, None
 
 
+def kernel_block(eng, args):
+    """Which block kernel one step launches and its launch geometry: the
+    one-block-per-CTA kernel when its grid fits one round (csrc/
+    cbessfm_launch.cuh use_fat_kernel), else the P-CTA cluster kernel."""
+    import torch
+    real = "float" if args.dtype == "c64" else "double"
+    q = WL["block"] // 5
+    from paper_2409_14489_b200._native import num_blocks
+    nblocks = args.batch * num_blocks(WL["n"], WL["block"], WL["overlap"])
+    env = os.environ.get("CBESSFM_KERNEL", "")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    fat = (args.dtype == "c64" and q == 2048 and not env.startswith("c")
+           and (env.startswith("f") or nblocks <= sms))
+    saved = os.environ.get("CBESSFM_KERNEL")
+    os.environ["CBESSFM_KERNEL"] = "fat" if fat else "cluster"
+    try:
+        info = eng.plan.info()
+    finally:
+        if saved is None:
+            del os.environ["CBESSFM_KERNEL"]
+        else:
+            os.environ["CBESSFM_KERNEL"] = saved
+    name = ("cbessfm_fat_kernel<float,5,%d>" % q if fat
+            else "cbessfm_block_kernel<%s,5,%d>" % (real, q))
+    return {"name": name, "blocks_per_launch": nblocks,
+            "plan": {k: getattr(info, k) for k in ("threads_per_cta", "cluster_size",
+                                                    "smem_per_cta", "max_active_clusters", "q")}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -566,11 +595,7 @@ def main():
             "config": config_block(args, world), "impl": "ours",
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": args.steps, "clocks": clocks, "gather": gather,
-            "kernel": {"name": "cbessfm_block_kernel<%s,5,%d>" % (
-                           "float" if args.dtype == "c64" else "double", WL["block"] // 5),
-                       "plan": {k: getattr(eng.plan.info(), k) for k in
-                                ("threads_per_cta", "cluster_size", "smem_per_cta",
-                                 "max_active_clusters", "q")}}}
+            "kernel": kernel_block(eng, args)}
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

@@ -271,10 +271,14 @@ cudaError_t dispatch<double>(int P, const cbessfm::Params<double>& prm, int q, i
 }
 #undef CB_CASE
 
+// set while cbessfm_run_host issues its pipelined chunk launches
+thread_local int g_kernel_pref = 0;
+
 template <typename R>
 cbessfm::Params<R> make_params(const cbessfm_plan* p, const cbessfm_io* io) {
   using C = cbessfm::Cx<R>;
   cbessfm::Params<R> prm;
+  prm.kernel_pref = g_kernel_pref;
   prm.in = reinterpret_cast<const C*>(io->in);
   prm.out = reinterpret_cast<C*>(io->out);
   prm.in_bstride = io->in_batch_stride;
@@ -506,7 +510,9 @@ cbessfm_status cbessfm_run_host(const cbessfm_plan* cp, const cbessfm_host_io* i
     }
     return CBESSFM_OK;
   };
+  g_kernel_pref = 1;  // chunks of several steps in flight: cluster kernel
   const cbessfm_status status = enqueue();
+  g_kernel_pref = 0;
   // join every pipeline stream into the caller's stream (also after an
   // error), then release the staging buffers in stream order
   for (int i = 0; i < 2 + chunks; ++i) cudaStreamWaitEvent(st, event(p->host_streams[i]), 0);

@@ -93,6 +93,7 @@ __device__ __forceinline__ Cx<R> operator-(Cx<R> a, Cx<R> b) {
 }
 // float complex add/sub as one packed FADD2 (sm_100 f32x2): same IEEE
 // results as the two scalar adds, half the issue slots
+#ifndef CB_NO_FADD2
 __device__ __forceinline__ Cx<float> operator+(Cx<float> a, Cx<float> b) {
   const float2 r = __fadd2_rn(make_float2(a.x, a.y), make_float2(b.x, b.y));
   return mk(r.x, r.y);
@@ -101,6 +102,7 @@ __device__ __forceinline__ Cx<float> operator-(Cx<float> a, Cx<float> b) {
   const float2 r = __fadd2_rn(make_float2(a.x, a.y), make_float2(-b.x, -b.y));
   return mk(r.x, r.y);
 }
+#endif
 template <typename R>
 __device__ __forceinline__ Cx<R> cmul(Cx<R> a, Cx<R> b) {
   return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -1176,6 +1178,8 @@ struct Params {
   const Cx<R>* twp;        // per-pass rows, layout twp_base()
   int n_steps;
   int64_t cid0;            // first cluster index of this launch chunk
+  int kernel_pref;         // 0: choose by grid size, 1: cluster kernel (several
+                           // launches in flight, cbessfm_run_host)
   long long* dbg;          // phase clocks of CTA 0 (CB_PHASE_PROFILE builds only)
 };
 

@@ -65,16 +65,29 @@ cudaError_t launch_fat(const Params<R>& prm, int64_t nblocks, cudaStream_t strea
   return cudaSuccess;
 }
 
-inline bool use_cluster_kernel() {
+// Kernel choice for a launch of `nblocks` overlap-save blocks where both
+// kernels apply: the one-block-per-CTA kernel when the blocks fit one
+// round on the GPU (one CTA per SM: no second, under-filled round as with
+// 4-CTA clusters), the cluster kernel beyond (higher sustained rate, measured
+// crossover at two rounds). CBESSFM_KERNEL=fat|cluster overrides.
+inline bool use_fat_kernel(int64_t nblocks, int pref) {
   const char* env = getenv("CBESSFM_KERNEL");
-  return env && env[0] == 'c';
+  if (env && env[0] == 'c') return false;
+  if (env && env[0] == 'f') return true;
+  // the pipelined host path keeps two steps' chunks in flight, where the
+  // cluster kernel's four CTAs per SM beat one CTA per SM
+  if (pref == 1) return false;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return nblocks <= (int64_t)sms;
 }
 
 template <typename R, int P, int Q>
 cudaError_t launch_one(const Params<R>& prm, int64_t nclusters, cudaStream_t stream,
                        KernelInfo* info) {
   if constexpr (fat_ok<R, P, Q>()) {
-    if (!use_cluster_kernel()) return launch_fat<R, P, Q>(prm, nclusters, stream, info);
+    if (use_fat_kernel(nclusters, prm.kernel_pref)) return launch_fat<R, P, Q>(prm, nclusters, stream, info);
   }
   auto kern = cbessfm_block_kernel<R, P, Q>;
   constexpr int NT = threads_for<R, Q>();
