@@ -285,6 +285,10 @@ constexpr int kTail = 0, kHead = 1, kHalf = 2, kMid = 3, kTM = 4;
 // computes before the pass barrier are parked in TMEM instead of registers,
 // all but the last (see tm_stash_*)
 constexpr int kStash = 8;
+// kGroupBar (one-block-per-CTA kernel): the passes of a subband group
+// synchronise on the group's own named barrier, so the P groups drift out
+// of phase and one group's shared-memory phase overlaps another's math
+constexpr int kGroupBar = 16;
 
 __host__ __device__ constexpr int sched_radix(int L, int ns, int sched) {
   const int sc = sched & 3;
@@ -611,6 +615,17 @@ __device__ __forceinline__ void bar_named(int id, int nthreads) {
 // stored with the complex padding.
 __device__ __forceinline__ int fpos(int p) { return 2 * pad(p >> 1) + (p & 1); }
 
+// Barrier ending a pass phase: the whole CTA, or (kGroupBar) the NT-thread
+// group of the calling thread (named barriers 1..P; 0 is __syncthreads).
+template <int SCHED, int NT>
+__device__ __forceinline__ void pass_sync() {
+  if constexpr ((SCHED & kGroupBar) != 0) {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)threadIdx.x / NT), "n"(NT) : "memory");
+  } else {
+    __syncthreads();
+  }
+}
+
 // Thread index inside the NT-thread group that runs one subband's
 // transforms: the whole CTA in the one-subband-per-CTA kernel, one of P
 // groups in the one-block-per-CTA kernel (NT a power of two; groups start
@@ -811,11 +826,20 @@ __device__ __forceinline__ void tm_stash_load(uint32_t lane_base, int col, Cx<R>
 #pragma unroll
   for (int r = 0; r < RAD; ++r) v[r] = tm_unpack<R>(u + r * CW);
 }
+// Columns each lane sharer (threadIdx.x / 128) owns for parking: one
+// layout for every pass (with kGroupBar the groups, which share lanes, run
+// different passes at the same time), sized for the widest pass -- three
+// radix-8 or one radix-16 butterfly.
+template <typename R>
+__host__ __device__ constexpr int stash_stride() {
+  return 3 * stash_width<R, 8>() > stash_width<R, 16>() ? 3 * stash_width<R, 8>()
+                                                        : stash_width<R, 16>();
+}
 // first stash column of slot p for this thread (COL0: first free column)
 template <typename R, int RAD, int PER>
 __device__ __forceinline__ int stash_col(int col0, int p) {
-  return col0 + ((int)threadIdx.x >> 7) * (PER - 1) * stash_width<R, RAD>() +
-         p * stash_width<R, RAD>();
+  static_assert((PER - 1) * stash_width<R, RAD>() <= stash_stride<R>(), "stash overflow");
+  return col0 + ((int)threadIdx.x >> 7) * stash_stride<R>() + p * stash_width<R, RAD>();
 }
 
 // TMEM base address of this CTA's twiddle columns (kernels whose
@@ -945,7 +969,7 @@ __device__ __forceinline__ void fft2_pass(Cx<R>* __restrict__ F, const Cx<R>* __
     }
   }
   if constexpr (STASH) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-  __syncthreads();
+  pass_sync<SCHED, NT>();
 #pragma unroll
   for (int pp = 0; pp < PER; ++pp) {
     // the register-resident last slot first, then the parked ones
@@ -962,7 +986,7 @@ __device__ __forceinline__ void fft2_pass(Cx<R>* __restrict__ F, const Cx<R>* __
     for (int r = 0; r < RAD; ++r) b[pad(r * NS)] = v[p][bitrev<RAD>(r)];
   }
   next.fetch(twp_next);
-  __syncthreads();
+  pass_sync<SCHED, NT>();
 }
 
 // Runs the passes NS, NS*R, ... of a length-Q field FFT with schedule
@@ -1058,7 +1082,7 @@ __device__ __forceinline__ void fft2_boundary(Cx<R>* __restrict__ F,
     }
   }
   if constexpr (STASH) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-  __syncthreads();
+  pass_sync<SFW, NT>();
 #pragma unroll
   for (int pp = 0; pp < PER; ++pp) {
     const int p = STASH ? (pp == 0 ? PER - 1 : pp - 1) : pp;
@@ -1071,7 +1095,7 @@ __device__ __forceinline__ void fft2_boundary(Cx<R>* __restrict__ F,
 #pragma unroll
     for (int r = 0; r < RAD; ++r) b[pad(r)] = v[p][bitrev<RAD>(r)];
   }
-  __syncthreads();
+  pass_sync<SFW, NT>();
 }
 
 // Single-array pass for the half-length real-transform FFTs. Passes with
@@ -1107,11 +1131,11 @@ __device__ __forceinline__ void fft1_pass(Cx<R>* __restrict__ buf, const Cx<R>* 
     Cx<R> v[PER][RAD];
 #pragma unroll
     for (int p = 0; p < PER; ++p) body_load(bfly<L, NS, RAD>(tid + p * NT), v[p], rows.row(p));
-    __syncthreads();
+    pass_sync<HS, NT>();
 #pragma unroll
     for (int p = 0; p < PER; ++p) body_store(bfly<L, NS, RAD>(tid + p * NT), v[p]);
     next.fetch(twp);
-    __syncthreads();
+    pass_sync<HS, NT>();
   } else {
     // fewer butterflies than threads: the leading whole warps run the pass
     // and synchronise between load and store with a named barrier; the full
@@ -1127,7 +1151,7 @@ __device__ __forceinline__ void fft1_pass(Cx<R>* __restrict__ buf, const Cx<R>* 
       if (on) body_store(tid, v);
     }
     next.fetch(twp);
-    __syncthreads();
+    pass_sync<HS, NT>();
   }
 }
 
@@ -1677,14 +1701,18 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
   static_assert((H / CB_HALF_RAD) >= NT, "half-length passes must keep every thread busy");
   // TMEM: twiddle rows, then the butterfly parking of the P*NT/128 lane
   // sharers (at most 3 radix-8 or 1 radix-16 butterfly each)
-  constexpr int STASH_W = 3 * stash_width<R, 8>() > stash_width<R, 16>() ? 3 * stash_width<R, 8>()
-                                                                           : stash_width<R, 16>();
-  constexpr int TM_NEED = tm_total((int)sizeof(R), Q, NT) + (NTC / 128) * STASH_W;
+  constexpr int TM_NEED = tm_total((int)sizeof(R), Q, NT) + (NTC / 128) * stash_stride<R>();
   constexpr bool TMON = !defined_no_tmem() && TM_NEED <= 512;
   constexpr int COLS = pow2_cols(TM_NEED);
-  constexpr int FI = TMON ? (kMid | kTM | kStash) : kTail;
-  constexpr int FF = TMON ? (kMid | kTM | kStash) : kHead;
-  constexpr int HS = kHalf | (TMON ? kTM : 0);
+#ifndef CB_GB_FIELD
+#define CB_GB_FIELD kGroupBar
+#endif
+#ifndef CB_GB_HALF
+#define CB_GB_HALF kGroupBar
+#endif
+  constexpr int FI = (TMON ? (kMid | kTM | kStash) : kTail) | CB_GB_FIELD;
+  constexpr int FF = (TMON ? (kMid | kTM | kStash) : kHead) | CB_GB_FIELD;
+  constexpr int HS = kHalf | (TMON ? kTM : 0) | CB_GB_HALF;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Cx<R>* const base = reinterpret_cast<Cx<R>*>(smem_raw);
@@ -1710,6 +1738,8 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
     asm volatile("tcgen05.fence::before_thread_sync;");
   }
   const int64_t cid = prm.cid0 + blockIdx.x;
+  (void)cid;
+  CB_MARK(0);
   const int64_t wv = cid / prm.nb;
   const int64_t b = prm.b0 + cid % prm.nb;
   const int64_t n = prm.n;
@@ -1722,31 +1752,40 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
   const Cx<R>* __restrict__ twpF = prm.twp + twp_base(Q, FF);
   const Cx<R>* __restrict__ twpH = prm.twp + twp_base(Q, kHalf);
 
-  // ---- 1. group s loads the polyphase component u[s + P*t2] of the
-  //         circular window starting at (b*keep - half) mod n (dbp.py:473-475)
+  // ---- 1. load the circular window starting at (b*keep - half) mod n
+  //         (dbp.py:473-475) with consecutive threads on consecutive
+  //         samples (coalesced); sample t goes to polyphase row t mod P,
+  //         position t / P
   {
     int64_t start = (b * prm.keep - prm.half) % n;
     if (start < 0) start += n;
     start -= prm.in_origin;
     if (start < 0) start += n;
     const Cx<R>* src = prm.in + wv * prm.in_bstride;
-    for (int t2 = tid; t2 < Q; t2 += NT) {
-      int64_t idx = start + grp + (int64_t)P * t2;
+    for (int t = (int)threadIdx.x; t < P * Q; t += NTC) {
+      int64_t idx = start + t;
       if (idx >= n) idx -= n;
-      F[pad(t2)] = src[idx];
-      F[SF + pad(t2)] = src[prm.in_pstride + idx];
+      const int r = t % P, t2 = t / P;
+      Cx<R>* Fr = base + r * SG;
+      Fr[pad(t2)] = src[idx];
+      Fr[SF + pad(t2)] = src[prm.in_pstride + idx];
     }
   }
   __syncthreads();
   if constexpr (TMON) asm volatile("tcgen05.fence::after_thread_sync;");
+  CB_MARK(1);
 
   // ---- 2.-3. outer transform (dbp.py:387-389): FFT_Q per subband, then
   //         the radix-P stage across subbands. Thread-strided over k2: the P
   //         inputs Q*k1 + k2 are read into registers, a barrier, then the P
   //         outputs (x 1/P x first phasor) go to their subband homes in place.
   fft2<R, Q, NT, FI, false>(F, twpT, &s_zero);
+  __syncthreads();  // the passes synchronise per group only
   constexpr int KPT = (Q + NTC - 1) / NTC;
   const R invP = (R)1 / (R)P;
+  Cx<R> wP[P];  // W_P^m = twN[m Q]
+#pragma unroll
+  for (int m = 0; m < P; ++m) wP[m] = ldg(twN + m * Q);
   const Cx<R>* ph0 = prm.phasor + (size_t)prm.ph_index[0] * (size_t)P * Q;
   for (int pol = 0; pol < 2; ++pol) {
     Cx<R> bv[KPT][P];
@@ -1771,7 +1810,7 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
         for (int k1 = 0; k1 < P; ++k1) {
           Cx<R> sm = bv[u][0];
 #pragma unroll
-          for (int r = 1; r < P; ++r) sm = sm + cmul(bv[u][r], ldg(twN + ((r * k1) % P) * Q));
+          for (int r = 1; r < P; ++r) sm = sm + cmul(bv[u][r], wP[(r * k1) % P]);
           int i, m;
           bin_home<P, Q>(Q * k1 + k2, i, m);
           base[i * SG + pol * SF + pad(m)] = cmul(scale(sm, invP), ldg(ph0 + (size_t)i * Q + m));
@@ -1781,6 +1820,7 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
     __syncthreads();
   }
 
+  CB_MARK(2);
   // ---- 4. nonlinear steps (dbp.py:394-398), as in the cluster kernel
   const Cx<R>* ph_grp = prm.phasor + (size_t)grp * Q;
   const size_t ph_tab = (size_t)P * Q;
@@ -1790,6 +1830,7 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
   ih.I = Ireal;
   if (prm.n_steps > 0)
     fft2<R, Q, NT, FI, true, NoHook, IntensityHook<R>>(F, twpT, &s_zero, NoHook(), ih);
+  CB_MARK(3);
   constexpr int KU = (H / 2 + 1 + NT - 1) / NT;
   for (int st = 0; st < prm.n_steps; ++st) {
     Cx<R> twk[KU];
@@ -1799,6 +1840,7 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
       twk[u] = (k <= H / 2) ? ldg(twQ + k) : mk((R)1, (R)0);
     }
     fft1<R, Q, H, NT, false, HS>(IS, twpH, &s_zero);
+    CB_MARK(8 + 8 * st + 0);
     // r2c untangle in place: I_hat[k], k = 0..H (numpy rfft, dbp.py:194)
 #pragma unroll
     for (int u = 0; u < KU; ++u) {
@@ -1820,6 +1862,7 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
       }
     }
     __syncthreads();
+    CB_MARK(8 + 8 * st + 1);
     // MIMO coupling (dbp.py:195) in place: bin k of every subband, one
     // thread per bin
     for (int k = (int)threadIdx.x; k <= H; k += NTC) {
@@ -1838,6 +1881,8 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
       }
     }
     __syncthreads();
+    CB_MARK(8 + 8 * st + 2);
+    CB_MARK(8 + 8 * st + 3);
     // c2r pre-twist in place (numpy irfft ignores Im of bins 0 and H)
 #pragma unroll
     for (int u = 0; u < KU; ++u) {
@@ -1864,7 +1909,9 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
       }
     }
     __syncthreads();
+    CB_MARK(8 + 8 * st + 4);
     fft1<R, Q, H, NT, true, HS>(TS, twpH, &s_zero);
+    CB_MARK(8 + 8 * st + 5);
     RotationHook<R> rot;
     rot.th = Treal;
     rot.scale = theta_scale[st];
@@ -1872,7 +1919,9 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
     if (st + 1 < prm.n_steps) {
       fft2<R, Q, NT, FF, false, RotationHook<R>, NoHook, 1, Q / sched_radix(Q, 1, FI)>(
           F, twpF, &s_zero, rot);
+      CB_MARK(8 + 8 * st + 6);
       fft2_boundary<R, Q, NT, FI, FF>(F, twpF, ph_next, &s_zero);
+      CB_MARK(8 + 8 * st + 7);
       fft2<R, Q, NT, FI, true, NoHook, IntensityHook<R>, sched_radix(Q, 1, FI)>(
           F, twpT, &s_zero, NoHook(), ih);
     } else {
@@ -1882,8 +1931,13 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
     }
   }
 
+  __syncthreads();
+  CB_MARK(4);
   // ---- 5. merge + outer IFFT (dbp.py:400-401): inverse radix-P stage in
   //         place (registers across one barrier), then FFT_Q^-1 per group
+  Cx<R> wQ[P];  // W_P^m again (not kept live through the step loop)
+#pragma unroll
+  for (int m = 0; m < P; ++m) wQ[m] = ldg(twN + m * Q + *(&s_zero));
   for (int pol = 0; pol < 2; ++pol) {
     Cx<R> xv[KPT][P];
 #pragma unroll
@@ -1907,7 +1961,7 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
         for (int n1 = 0; n1 < P; ++n1) {
           Cx<R> sm = xv[u][0];
 #pragma unroll
-          for (int k1 = 1; k1 < P; ++k1) sm = sm + cmulc(xv[u][k1], ldg(twN + ((n1 * k1) % P) * Q));
+          for (int k1 = 1; k1 < P; ++k1) sm = sm + cmulc(xv[u][k1], wQ[(n1 * k1) % P]);
           if (n1) sm = cmulc(sm, ldg(twN + n1 * k2));
           base[n1 * SG + pol * SF + pad(k2)] = sm;
         }
@@ -1916,18 +1970,19 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
     __syncthreads();
   }
   fft2<R, Q, NT, FI, true>(F, twpT, &s_zero);
+  __syncthreads();
+  CB_MARK(5);
 
-  // ---- 6. keep proc[half : half + span] (dbp.py:476-477)
+  // ---- 6. keep proc[half : half + span] (dbp.py:476-477), coalesced
   {
     const int64_t span = min(prm.keep, n - b * prm.keep);
     Cx<R>* dst = prm.out + wv * prm.out_bstride;
     const int64_t obase = b * prm.keep - prm.half - prm.out_origin;
-    for (int t2 = tid; t2 < Q; t2 += NT) {
-      const int64_t t = grp + (int64_t)P * t2;
-      if (t >= prm.half && t < prm.half + span) {
-        dst[obase + t] = F[pad(t2)];
-        dst[prm.out_pstride + obase + t] = F[SF + pad(t2)];
-      }
+    for (int64_t t = prm.half + threadIdx.x; t < prm.half + span; t += NTC) {
+      const int r = (int)(t % P), t2 = (int)(t / P);
+      const Cx<R>* Fr = base + r * SG;
+      dst[obase + t] = Fr[pad(t2)];
+      dst[prm.out_pstride + obase + t] = Fr[SF + pad(t2)];
     }
   }
   if constexpr (TMON) {
