@@ -289,17 +289,15 @@ def ncu_traffic(dtype: str):
 
 def kernel_block(eng, args):
     """Which block kernel one step launches and its launch geometry: the
-    one-block-per-CTA kernel when its grid fits one round (csrc/
-    cbessfm_launch.cuh use_fat_kernel), else the P-CTA cluster kernel."""
+    one-block-per-CTA kernel for c64 at N' = 2048 (csrc/cbessfm_launch.cuh
+    use_fat_kernel), else the P-CTA cluster kernel."""
     import torch
     real = "float" if args.dtype == "c64" else "double"
     q = WL["block"] // 5
     from paper_2409_14489_b200._native import num_blocks
     nblocks = args.batch * num_blocks(WL["n"], WL["block"], WL["overlap"])
     env = os.environ.get("CBESSFM_KERNEL", "")
-    sms = torch.cuda.get_device_properties(0).multi_processor_count
-    fat = (args.dtype == "c64" and q == 2048 and not env.startswith("c")
-           and (env.startswith("f") or nblocks <= sms))
+    fat = args.dtype == "c64" and q == 2048 and not env.startswith("c")
     saved = os.environ.get("CBESSFM_KERNEL")
     os.environ["CBESSFM_KERNEL"] = "fat" if fat else "cluster"
     try:

@@ -22,7 +22,7 @@ constexpr int max_q() {
 
 // One-block-per-CTA kernel (cbessfm_fat_kernel): one CTA of P * Q/16
 // threads per overlap-save block, no cluster. Used where fat_ok() holds
-// unless CBESSFM_KERNEL=cluster.
+// (see use_fat_kernel).
 template <typename R, int P, int Q>
 cudaError_t launch_fat(const Params<R>& prm, int64_t nblocks, cudaStream_t stream,
                        KernelInfo* info) {
@@ -65,22 +65,19 @@ cudaError_t launch_fat(const Params<R>& prm, int64_t nblocks, cudaStream_t strea
   return cudaSuccess;
 }
 
-// Kernel choice for a launch of `nblocks` overlap-save blocks where both
-// kernels apply: the one-block-per-CTA kernel when the blocks fit one
-// round on the GPU (one CTA per SM: no second, under-filled round as with
-// 4-CTA clusters), the cluster kernel beyond (higher sustained rate, measured
-// crossover at two rounds). CBESSFM_KERNEL=fat|cluster overrides.
+// Kernel choice where both kernels apply (FP32, N' = 2048, P <= 5): the
+// one-block-per-CTA kernel for device-resident launches (configs[1]
+// waveforms: 0.386 / 0.741 / 1.43 / 2.81 / 5.55 ms for 1 / 2 / 4 / 8 / 16
+// per launch vs 0.471 / 0.815 / 1.53 / 2.95 / 5.81 for the cluster kernel),
+// the cluster kernel for the pipelined host path, whose chunks of a few
+// blocks want the lower per-block latency of spreading a block over P SMs
+// (end to end 2.74e9 vs 2.63e9 2D/s). CBESSFM_KERNEL=fat|cluster overrides.
 inline bool use_fat_kernel(int64_t nblocks, int pref) {
+  (void)nblocks;
   const char* env = getenv("CBESSFM_KERNEL");
   if (env && env[0] == 'c') return false;
   if (env && env[0] == 'f') return true;
-  // the pipelined host path keeps two steps' chunks in flight, where the
-  // cluster kernel's four CTAs per SM beat one CTA per SM
-  if (pref == 1) return false;
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return nblocks <= (int64_t)sms;
+  return pref != 1;
 }
 
 template <typename R, int P, int Q>

@@ -295,9 +295,9 @@ def test_set_evaluator_reuses_its_plan(cuda):
 
 @pytest.mark.parametrize("kernel", ["fat", "cluster"])
 def test_both_block_kernels_match_reference(cuda, kernel, monkeypatch):
-    # csrc/cbessfm_launch.cuh use_fat_kernel: for P <= 5, Q = 2048 in FP32 a
-    # launch that fits one round runs the one-block-per-CTA kernel, larger
-    # ones the P-CTA cluster kernel; each must meet the c64 bar on its own
+    # csrc/cbessfm_launch.cuh use_fat_kernel: for P <= 5, Q = 2048 in FP32
+    # device launches run the one-block-per-CTA kernel, the pipelined host
+    # path the P-CTA cluster kernel; each must meet the c64 bar on its own
     # (configs[1] golden case, the reference's output), bit-identical across
     # a split into block ranges
     import torch
@@ -318,9 +318,8 @@ def test_both_block_kernels_match_reference(cuda, kernel, monkeypatch):
 
 
 def test_fat_and_cluster_kernels_agree_at_scale(cuda, monkeypatch):
-    # 3 configs[1]-size waveforms (429 blocks: the default picks the cluster
-    # kernel) vs the one-block-per-CTA kernel forced: same FP32 arithmetic
-    # per block except the outer radix-P stage's summation order
+    # 3 configs[1]-size waveforms (429 blocks) through both kernels: same
+    # FP32 arithmetic per block except the outer radix-P stage's order
     import torch
     g = golden("cfg2_nsb5")
     rate = g.wave.sample_rate
