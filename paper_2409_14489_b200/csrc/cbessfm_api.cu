@@ -94,6 +94,19 @@ struct cbessfm_plan {
   // host-buffer pipeline (cbessfm_run_host): streams created on first use
   std::mutex host_mu;
   std::vector<cudaStream_t> host_streams;  // [0] copy in, [1] copy out, [2..] compute
+  // device staging of cbessfm_run_host: a ring of slots reused across calls
+  // (each waits for its previous user's D2H), so calls with several steps
+  // in flight neither allocate per call nor pick up the stream-ordered
+  // allocator's cross-stream reuse dependencies
+  struct HostSlot {
+    void* din = nullptr;
+    void* dout = nullptr;
+    size_t bytes = 0;
+    cudaEvent_t done = nullptr;
+  };
+  static constexpr int kHostSlots = 4;
+  HostSlot host_slots[kHostSlots];
+  int host_next = 0;
 };
 
 namespace {
@@ -232,6 +245,12 @@ cbessfm_status upload_all(cbessfm_plan* p, const cbessfm_desc* d) {
 
 void free_plan(cbessfm_plan* p) {
   if (!p) return;
+  for (auto& sl : p->host_slots) {
+    if (sl.done) cudaEventSynchronize(sl.done);
+    cudaFree(sl.din);
+    cudaFree(sl.dout);
+    if (sl.done) cudaEventDestroy(sl.done);
+  }
   for (cudaStream_t st : p->host_streams) cudaStreamDestroy(st);
   cudaFree(p->phasor);
   cudaFree(p->ph_index);
@@ -455,12 +474,29 @@ cbessfm_status cbessfm_run_host(const cbessfm_plan* cp, const cbessfm_host_io* i
     p->host_streams.push_back(s2);
   }
   cudaStream_t s_in = p->host_streams[0], s_out = p->host_streams[1];
-  void *din = nullptr, *dout = nullptr;
-  if ((e = cudaMallocAsync(&din, rows * rowb, st)) != cudaSuccess) return cuda_fail(e, "alloc in");
-  if ((e = cudaMallocAsync(&dout, rows * rowb, st)) != cudaSuccess) {
-    cudaFreeAsync(din, st);
-    return cuda_fail(e, "alloc out");
+  cbessfm_plan::HostSlot& slot = p->host_slots[p->host_next];
+  p->host_next = (p->host_next + 1) % cbessfm_plan::kHostSlots;
+  if (!slot.done) {
+    if ((e = cudaEventCreateWithFlags(&slot.done, cudaEventDisableTiming)) != cudaSuccess)
+      return cuda_fail(e, "event create");
+  } else {
+    cudaStreamWaitEvent(st, slot.done, 0);  // its previous call's D2H has finished
   }
+  if (slot.bytes < rows * rowb) {
+    cudaFreeAsync(slot.din, st);
+    cudaFreeAsync(slot.dout, st);
+    slot.din = slot.dout = nullptr;
+    slot.bytes = 0;
+    if ((e = cudaMallocAsync(&slot.din, rows * rowb, st)) != cudaSuccess)
+      return cuda_fail(e, "alloc in");
+    if ((e = cudaMallocAsync(&slot.dout, rows * rowb, st)) != cudaSuccess) {
+      cudaFreeAsync(slot.din, st);
+      slot.din = nullptr;
+      return cuda_fail(e, "alloc out");
+    }
+    slot.bytes = rows * rowb;
+  }
+  void *din = slot.din, *dout = slot.dout;
   std::vector<cudaEvent_t> evs;
   auto event = [&](cudaStream_t s2) {
     cudaEvent_t ev;
@@ -514,10 +550,9 @@ cbessfm_status cbessfm_run_host(const cbessfm_plan* cp, const cbessfm_host_io* i
   const cbessfm_status status = enqueue();
   g_kernel_pref = 0;
   // join every pipeline stream into the caller's stream (also after an
-  // error), then release the staging buffers in stream order
+  // error); the staging slot is reusable once that point is reached
   for (int i = 0; i < 2 + chunks; ++i) cudaStreamWaitEvent(st, event(p->host_streams[i]), 0);
-  cudaFreeAsync(din, st);
-  cudaFreeAsync(dout, st);
+  cudaEventRecord(slot.done, st);  // the slot is free once this call completes
   for (cudaEvent_t ev : evs) cudaEventDestroy(ev);  // released once complete
   if (status != CBESSFM_OK) return status;
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "cbessfm_run_host");
