@@ -76,6 +76,7 @@ std::vector<double> pass_tables(int Q, const std::vector<double>& tq, int real_b
   fill(Q, kHead);
   fill(Q, kMid);
   fill(Q / 2, kHalf);
+  fill(Q / 2, kHalf | kWide);  // one-block-per-CTA kernel
   return out;
 }
 

@@ -273,7 +273,9 @@ __device__ __forceinline__ void dft_reg(Cx<R>* v) {
 //            narrow middle pass runs several butterflies per thread and
 //            spills, so small Q keep kTail/kHead.
 //   kHalf -- radix-4 passes for the half-length real-transform FFTs, which
-//            keeps all Q/8 threads busy on Q/2 points
+//            keeps all Q/8 threads busy on Q/2 points; with kWide, radix-8
+//            passes (1024: 8 8 8 2, one pass fewer): the one-block-per-CTA
+//            kernel's Q/16-thread groups, and the cluster kernel from Q = 2048
 // kTM may be or'ed into kMid or kHalf: that transform reads its twiddle
 // rows from tensor memory (see "Twiddle rows in tensor memory" below).
 #ifndef CB_HALF_RAD
@@ -289,10 +291,15 @@ constexpr int kStash = 8;
 // synchronise on the group's own named barrier, so the P groups drift out
 // of phase and one group's shared-memory phase overlaps another's math
 constexpr int kGroupBar = 16;
+// kWide (kHalf only): radix-8 half-length passes, rows in their own section
+constexpr int kWide = 32;
 
 __host__ __device__ constexpr int sched_radix(int L, int ns, int sched) {
   const int sc = sched & 3;
-  if (sc == kHalf) return L / ns >= CB_HALF_RAD ? CB_HALF_RAD : L / ns;
+  if (sc == kHalf) {
+    const int hr = (sched & kWide) ? 8 : CB_HALF_RAD;
+    return L / ns >= hr ? hr : L / ns;
+  }
   if (sc == kHead && ns == 1) {
     int head = L;
     while (head > kMaxRad) head /= kMaxRad;
@@ -313,15 +320,18 @@ __host__ __device__ constexpr int twp_offset(int L, int NS, int sched) {
 __host__ __device__ constexpr int twp_size(int L, int sched) { return twp_offset(L, L, sched); }
 // per-pass twiddle rows in Params::twp:
 //   [kTail rows of Q][kHead rows of Q][kMid rows of Q][kHalf rows of Q/2]
+//   [kHalf|kWide rows of Q/2]
 __host__ __device__ constexpr int twp_base(int Q, int sched) {
   const int sc = sched & 3;
+  const int half = twp_size(Q, kTail) + twp_size(Q, kHead) + twp_size(Q, kMid);
   return sc == kTail ? 0
        : sc == kHead ? twp_size(Q, kTail)
        : sc == kMid  ? twp_size(Q, kTail) + twp_size(Q, kHead)
-                     : twp_size(Q, kTail) + twp_size(Q, kHead) + twp_size(Q, kMid);
+       : (sched & kWide) ? half + twp_size(Q / 2, kHalf)
+                         : half;
 }
 __host__ __device__ constexpr int twp_total(int Q) {
-  return twp_base(Q, kHalf) + twp_size(Q / 2, kHalf);
+  return twp_base(Q, kHalf | kWide) + twp_size(Q / 2, kHalf | kWide);
 }
 
 // Twiddle storage of one pass (NS rows k, radix RAD, entries r = 1..RAD-1)
@@ -473,13 +483,14 @@ __host__ __device__ constexpr TmPass tm_pass(int rbytes, int Q, int NT, int sche
   return TmPass{rad, per, dep_g, dep_p, copies, tm_width(tm_words(rbytes, rad))};
 }
 // first TMEM column of pass (sched, NS): kMid passes, then kHalf passes
+// (radix-8 ones when sched carries kWide)
 __host__ __device__ constexpr int tm_col(int rbytes, int Q, int NT, int sched, int NS) {
   int c = 0;
   for (int pass = 0; pass < 2; ++pass) {
-    const int sc = pass == 0 ? kMid : kHalf;
+    const int sc = pass == 0 ? kMid : (kHalf | (sched & kWide));
     const int L = pass == 0 ? Q : Q / 2;
     for (int ns = 1; ns < L; ns *= sched_radix(L, ns, sc)) {
-      if (sc == (sched & 3) && ns == NS) return c;
+      if ((sc & 3) == (sched & 3) && ns == NS) return c;
       if (ns > 1) {
         const TmPass t = tm_pass(rbytes, Q, NT, sc, ns);
         c += t.copies * t.width;
@@ -488,8 +499,12 @@ __host__ __device__ constexpr int tm_col(int rbytes, int Q, int NT, int sched, i
   }
   return c;
 }
+// columns of the rows (either half-length variant; the butterfly parking
+// starts after them)
 __host__ __device__ constexpr int tm_total(int rbytes, int Q, int NT) {
-  return tm_col(rbytes, Q, NT, kHalf, Q / 2);
+  const int a = tm_col(rbytes, Q, NT, kHalf, Q / 2);
+  const int b = tm_col(rbytes, Q, NT, kHalf | kWide, Q / 2);
+  return a > b ? a : b;
 }
 
 // Copy index of the row thread `tid` uses in slot p of a pass.
@@ -1318,7 +1333,10 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
   // schedules; half-length transforms
   constexpr int FI = TMON ? (kMid | kTM) : kTail;
   constexpr int FF = TMON ? (kMid | kTM) : kHead;
-  constexpr int HS = kHalf | (TMON ? kTM : 0);
+  // radix-8 half-length passes from Q = 2048 (measured: c64 -1.3 %, c128
+  // -2.5 % per step at Q = 2048 vs radix 4, though a pass then keeps only
+  // half the CTA's threads busy)
+  constexpr int HS = kHalf | (TMON ? kTM : 0) | (Q >= 2048 ? kWide : 0);
   if constexpr (TMON) {
     // allocate this CTA's TMEM columns (warp 0) and copy the twiddle rows in
     if (threadIdx.x < 32) {
@@ -1330,7 +1348,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     tm_fill_sched<R, Q, NT, FI, 1>(prm.twp + twp_base(Q, kMid));
-    tm_fill_sched<R, Q, NT, HS, 1>(prm.twp + twp_base(Q, kHalf));
+    tm_fill_sched<R, Q, NT, HS, 1>(prm.twp + twp_base(Q, HS));
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;");
     // the barrier after the block load orders these stores before every
@@ -1350,7 +1368,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
   const Cx<R>* __restrict__ twN = prm.twN;
   const Cx<R>* __restrict__ twpT = prm.twp + twp_base(Q, FI);  // field IFFT / outer
   const Cx<R>* __restrict__ twpF = prm.twp + twp_base(Q, FF);  // in-step field FFT
-  const Cx<R>* __restrict__ twpH = prm.twp + twp_base(Q, kHalf);  // half-length FFTs
+  const Cx<R>* __restrict__ twpH = prm.twp + twp_base(Q, HS);  // half-length FFTs
 
   CB_MARK(0);
   CB_TIMELINE(0);
@@ -1698,7 +1716,7 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
   constexpr int SF = padded_len(Q);
   constexpr int SG = 2 * SF + padded_len(H + 1);  // shared entries per group
   static_assert(NT % 128 == 0, "groups must start on a TMEM lane quarter");
-  static_assert((H / CB_HALF_RAD) >= NT, "half-length passes must keep every thread busy");
+  static_assert((H / 8) >= NT, "half-length passes must keep every thread busy");
   // TMEM: twiddle rows, then the butterfly parking of the P*NT/128 lane
   // sharers (at most 3 radix-8 or 1 radix-16 butterfly each)
   constexpr int TM_NEED = tm_total((int)sizeof(R), Q, NT) + (NTC / 128) * stash_stride<R>();
@@ -1712,7 +1730,7 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
 #endif
   constexpr int FI = (TMON ? (kMid | kTM | kStash) : kTail) | CB_GB_FIELD;
   constexpr int FF = (TMON ? (kMid | kTM | kStash) : kHead) | CB_GB_FIELD;
-  constexpr int HS = kHalf | (TMON ? kTM : 0) | CB_GB_HALF;
+  constexpr int HS = kHalf | kWide | (TMON ? kTM : 0) | CB_GB_HALF;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Cx<R>* const base = reinterpret_cast<Cx<R>*>(smem_raw);
@@ -1733,7 +1751,7 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     tm_fill_sched<R, Q, NT, FI, 1>(prm.twp + twp_base(Q, kMid));
-    tm_fill_sched<R, Q, NT, HS, 1>(prm.twp + twp_base(Q, kHalf));
+    tm_fill_sched<R, Q, NT, HS, 1>(prm.twp + twp_base(Q, HS));
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;");
   }
@@ -1750,7 +1768,7 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
   const Cx<R>* __restrict__ twN = prm.twN;
   const Cx<R>* __restrict__ twpT = prm.twp + twp_base(Q, FI);
   const Cx<R>* __restrict__ twpF = prm.twp + twp_base(Q, FF);
-  const Cx<R>* __restrict__ twpH = prm.twp + twp_base(Q, kHalf);
+  const Cx<R>* __restrict__ twpH = prm.twp + twp_base(Q, HS);
 
   // ---- 1. load the circular window starting at (b*keep - half) mod n
   //         (dbp.py:473-475) with consecutive threads on consecutive
@@ -1831,6 +1849,96 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
   if (prm.n_steps > 0)
     fft2<R, Q, NT, FI, true, NoHook, IntensityHook<R>>(F, twpT, &s_zero, NoHook(), ih);
   CB_MARK(3);
+#ifndef CB_SPLIT_MIMO
+  // One CTA phase per step between the half-length FFTs: thread k (k <= H/2)
+  // owns the bin pair (k, H-k) of every subband -- r2c untangle, MIMO of both
+  // bins, c2r pre-twist -- all in registers (the three are pair-local), so
+  // there is one shared-memory round trip and two CTA barriers instead of
+  // three of each. Same operations, same order as the three-phase form.
+  constexpr int KP = (H / 2 + 1 + NTC - 1) / NTC;  // bin pairs per thread
+  for (int st = 0; st < prm.n_steps; ++st) {
+    Cx<R> wks[KP];
+#pragma unroll
+    for (int u = 0; u < KP; ++u) {
+      const int kp = (int)threadIdx.x + u * NTC;
+      wks[u] = kp <= H / 2 ? ldg(twQ + kp) : mk((R)1, (R)0);
+    }
+    fft1<R, Q, H, NT, false, HS>(IS, twpH, &s_zero);
+    CB_MARK(8 + 8 * st + 0);
+    __syncthreads();  // every subband's spectrum is read below
+    CB_MARK(8 + 8 * st + 1);
+#pragma unroll
+    for (int u = 0; u < KP; ++u) {
+      const int kp = (int)threadIdx.x + u * NTC;  // bin pair (kp, H - kp)
+      if (kp > H / 2) break;
+      const int kq = H - kp;
+      const Cx<R> wk = wks[u];
+      Cx<R> ia[P], ib[P];  // I_hat[kp], I_hat[kq] of every subband
+#pragma unroll
+      for (int l = 0; l < P; ++l) {
+        const Cx<R>* Il = base + l * SG + 2 * SF;
+        // r2c untangle (numpy rfft, dbp.py:194)
+        if (kp == 0) {
+          const Cx<R> z = Il[pad(0)];
+          ia[l] = mk(z.x + z.y, (R)0);
+          ib[l] = mk(z.x - z.y, (R)0);
+        } else {
+          const Cx<R> a = Il[pad(kp)];
+          const Cx<R> bq = conj(Il[pad(kq)]);
+          const Cx<R> e = scale(a + bq, (R)0.5);
+          const Cx<R> dd = a - bq;
+          const Cx<R> o = mk(dd.y * (R)0.5, -dd.x * (R)0.5);
+          const Cx<R> wo = cmul(o, wk);
+          ia[l] = e + wo;
+          ib[l] = kp == kq ? ia[l] : conj(e - wo);  // bin H/2 pairs with itself
+        }
+      }
+      // MIMO coupling (dbp.py:195) of both bins
+      Cx<R> ta[P], tb[P];
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int k = half ? kq : kp;
+        const Cx<R>* iv = half ? ib : ia;
+        Cx<R> sv[P];
+#pragma unroll
+        for (int l = 0; l < P; ++l) sv[l] = ldg_na(mimo + (size_t)l * (H + 1) + k);
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          Cx<R> acc = mk((R)0, (R)0);
+#pragma unroll
+          for (int l = 0; l < P; ++l)
+            acc = acc + (l >= i ? cmul(sv[l - i], iv[l]) : cmul(conj(sv[i - l]), iv[l]));
+          (half ? tb : ta)[i] = acc;
+        }
+      }
+      // c2r pre-twist (numpy irfft ignores Im of bins 0 and H)
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        Cx<R>* Ti = base + i * SG + 2 * SF;
+        if (kp == 0) {
+          Ti[pad(0)] = mk(ta[i].x + tb[i].x, ta[i].x - tb[i].x);
+        } else {
+          const Cx<R> a = ta[i];
+          const Cx<R> c = conj(tb[i]);
+          const Cx<R> s2 = a + c;
+          const Cx<R> dd = cmulc(a - c, wk);
+          Ti[pad(kp)] = mk(s2.x - dd.y, s2.y + dd.x);
+          if (kp != kq) {
+            const Cx<R> a2 = conj(c);
+            const Cx<R> c2 = conj(a);
+            const Cx<R> s3 = a2 + c2;
+            const Cx<R> w2 = mk(-wk.x, wk.y);
+            const Cx<R> d2 = cmulc(a2 - c2, w2);
+            Ti[pad(kq)] = mk(s3.x - d2.y, s3.y + d2.x);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    CB_MARK(8 + 8 * st + 2);
+    CB_MARK(8 + 8 * st + 3);
+    CB_MARK(8 + 8 * st + 4);
+#else
   constexpr int KU = (H / 2 + 1 + NT - 1) / NT;
   for (int st = 0; st < prm.n_steps; ++st) {
     Cx<R> twk[KU];
@@ -1910,6 +2018,7 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
     }
     __syncthreads();
     CB_MARK(8 + 8 * st + 4);
+#endif
     fft1<R, Q, H, NT, true, HS>(TS, twpH, &s_zero);
     CB_MARK(8 + 8 * st + 5);
     RotationHook<R> rot;
