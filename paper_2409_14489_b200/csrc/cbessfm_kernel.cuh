@@ -281,6 +281,9 @@ __device__ __forceinline__ void dft_reg(Cx<R>* v) {
 #ifndef CB_HALF_RAD
 #define CB_HALF_RAD 4
 #endif
+#ifndef CB_WIDE16
+#define CB_WIDE16 1
+#endif
 constexpr int kMaxRad = 16;
 constexpr int kTail = 0, kHead = 1, kHalf = 2, kMid = 3, kTM = 4;
 // kStash (field schedules, one-block-per-CTA kernel): butterflies a thread
@@ -297,6 +300,9 @@ constexpr int kWide = 32;
 __host__ __device__ constexpr int sched_radix(int L, int ns, int sched) {
   const int sc = sched & 3;
   if (sc == kHalf) {
+    // kWide at L = 1024: one radix-16 pass first (no twiddles), then
+    // radix 8 (1024: 16 8 8) -- three shared-memory round trips, not four
+    if (CB_WIDE16 && (sched & kWide) && ns == 1 && L == 1024) return 16;
     const int hr = (sched & kWide) ? 8 : CB_HALF_RAD;
     return L / ns >= hr ? hr : L / ns;
   }
@@ -1162,7 +1168,8 @@ __device__ __forceinline__ void fft1_pass(Cx<R>* __restrict__ buf, const Cx<R>* 
       const bool on = (NB % 32 == 0) || tid < NB;
       const Cx<R>* w = rows.row(0);  // warp-converged (TMEM)
       if (on) body_load(tid, v, w);
-      bar_named(1, ACT);
+      // (kGroupBar: one id per group, after the groups' pass ids 1..P)
+      bar_named((HS & kGroupBar) ? 1 + (int)(blockDim.x / NT) + (int)threadIdx.x / NT : 1, ACT);
       if (on) body_store(tid, v);
     }
     next.fetch(twp);
