@@ -36,6 +36,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace cbessfm {
 
 namespace cg = cooperative_groups;
@@ -296,6 +298,17 @@ constexpr int kStash = 8;
 constexpr int kGroupBar = 16;
 // kWide (kHalf only): radix-8 half-length passes, rows in their own section
 constexpr int kWide = 32;
+// kCarry (field schedules of the one-block-per-CTA kernel, with kStash): the
+// last pass of every IFFT that feeds the nonlinear step (radix 16, NS = Q/16,
+// intensity hook) keeps its outputs in TMEM instead of writing F, and the
+// first pass of the forward FFT after the rotation (radix 16, NS = 1) reads
+// them back: butterfly j produces exactly the samples j + r*Q/16 that
+// butterfly j of the next pass consumes, so the field's shared-memory round
+// trip between the two, and both passes' load/store barriers, disappear
+#ifndef CB_CARRY
+#define CB_CARRY 1
+#endif
+constexpr int kCarry = 64;
 
 __host__ __device__ constexpr int sched_radix(int L, int ns, int sched) {
   const int sc = sched & 3;
@@ -851,16 +864,18 @@ __device__ __forceinline__ void tm_stash_load(uint32_t lane_base, int col, Cx<R>
 // layout for every pass (with kGroupBar the groups, which share lanes, run
 // different passes at the same time), sized for the widest pass -- three
 // radix-8 or one radix-16 butterfly.
+// (kCarry: at least two radix-16 butterflies, the carried pass outputs)
 template <typename R>
-__host__ __device__ constexpr int stash_stride() {
-  return 3 * stash_width<R, 8>() > stash_width<R, 16>() ? 3 * stash_width<R, 8>()
-                                                        : stash_width<R, 16>();
+__host__ __device__ constexpr int stash_stride(bool carry = false) {
+  const int s = 3 * stash_width<R, 8>() > stash_width<R, 16>() ? 3 * stash_width<R, 8>()
+                                                               : stash_width<R, 16>();
+  return carry && 2 * stash_width<R, 16>() > s ? 2 * stash_width<R, 16>() : s;
 }
 // first stash column of slot p for this thread (COL0: first free column)
-template <typename R, int RAD, int PER>
+template <typename R, int RAD, int PER, bool CARRY = false>
 __device__ __forceinline__ int stash_col(int col0, int p) {
-  static_assert((PER - 1) * stash_width<R, RAD>() <= stash_stride<R>(), "stash overflow");
-  return col0 + ((int)threadIdx.x >> 7) * stash_stride<R>() + p * stash_width<R, RAD>();
+  static_assert((PER - 1) * stash_width<R, RAD>() <= stash_stride<R>(CARRY), "stash overflow");
+  return col0 + ((int)threadIdx.x >> 7) * stash_stride<R>(CARRY) + p * stash_width<R, RAD>();
 }
 
 // TMEM base address of this CTA's twiddle columns (kernels whose
@@ -966,11 +981,56 @@ __device__ __forceinline__ void fft2_pass(Cx<R>* __restrict__ F, const Cx<R>* __
   constexpr int PER = (Q / RAD) / SLOTS;
   constexpr int SF = padded_len(Q);
   constexpr bool STASH = (SCHED & kStash) != 0 && PER > 1;
+  constexpr bool CARRYS = (SCHED & kCarry) != 0;
   constexpr int SCOL = tm_total((int)sizeof(R), Q, NT);
-  Cx<R> v[PER][RAD];
   const int tid = ltid<NT>() + *zero;
   Cx<R>* Fp = F + fpol<NT>(tid) * SF;
   const int jb = fbase<NT>(tid);
+  // kCarry: the intensity IFFT's last pass parks its outputs (natural order,
+  // sample j + r*LR in slot r) in TMEM, the rotation FFT's first pass takes
+  // them from there; neither touches F in the other direction, so neither
+  // needs its load/store barrier
+  constexpr bool CARRY_OUT = CARRYS && LAST && INV && std::is_same<Hook, IntensityHook<R>>::value;
+  constexpr bool CARRY_IN = CARRYS && FIRST && !INV && std::is_same<Hook, RotationHook<R>>::value;
+  if constexpr (CARRY_OUT || CARRY_IN) {
+    static_assert(RAD == sched_radix(Q, 1, SCHED) && (CARRY_IN ? NS == 1 : NS == LR),
+                  "carried passes: radix-R butterflies on samples j + r*Q/R");
+    static_assert(PER * stash_width<R, RAD>() <= stash_stride<R>(true), "carry overflow");
+    const uint32_t lb = tm_lane_base(cb_tm_base);
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+      const int j = jb + p * SLOTS;
+      const int col = SCOL + ((int)threadIdx.x >> 7) * stash_stride<R>(true) +
+                      p * stash_width<R, RAD>();
+      Cx<R> v[RAD];
+      if constexpr (CARRY_IN) {
+        tm_stash_load<R, RAD>(lb, col, v);
+        hook.template pre<R, RAD, LR>(j, v);
+        dft_reg<R, RAD, INV>(v);
+        Cx<R>* b = Fp + pad(j * RAD);  // NS = 1: d0 = R*j
+#pragma unroll
+        for (int r = 0; r < RAD; ++r) b[pad(r)] = v[bitrev<RAD>(r)];
+      } else {
+        const Cx<R>* b = Fp + pad(j);
+#pragma unroll
+        for (int r = 0; r < RAD; ++r) v[r] = b[pad(r * LR)];
+        const Cx<R>* w = rows.row(p);
+#pragma unroll
+        for (int r = 1; r < RAD; ++r) v[r] = cmulc(v[r], w[r]);
+        dft_reg<R, RAD, INV>(v);
+        hook.template post<R, RAD, NS>(j, v);  // d0 = j (j < NS)
+        Cx<R> u[RAD];
+#pragma unroll
+        for (int r = 0; r < RAD; ++r) u[r] = v[bitrev<RAD>(r)];
+        tm_stash_store<R, RAD>(lb, col, u);
+      }
+    }
+    if constexpr (CARRY_OUT) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    next.fetch(twp_next);
+    pass_sync<SCHED, NT>();
+    return;
+  }
+  Cx<R> v[PER][RAD];
 #pragma unroll
   for (int p = 0; p < PER; ++p) {
     const int j = jb + p * SLOTS;
@@ -986,7 +1046,7 @@ __device__ __forceinline__ void fft2_pass(Cx<R>* __restrict__ F, const Cx<R>* __
     dft_reg<R, RAD, INV>(v[p]);
     if constexpr (STASH) {
       if (p < PER - 1)
-        tm_stash_store<R, RAD>(tm_lane_base(cb_tm_base), stash_col<R, RAD, PER>(SCOL, p), v[p]);
+        tm_stash_store<R, RAD>(tm_lane_base(cb_tm_base), stash_col<R, RAD, PER, CARRYS>(SCOL, p), v[p]);
     }
   }
   if constexpr (STASH) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -997,7 +1057,7 @@ __device__ __forceinline__ void fft2_pass(Cx<R>* __restrict__ F, const Cx<R>* __
     const int p = STASH ? (pp == 0 ? PER - 1 : pp - 1) : pp;
     if constexpr (STASH) {
       if (pp > 0)
-        tm_stash_load<R, RAD>(tm_lane_base(cb_tm_base), stash_col<R, RAD, PER>(SCOL, p), v[p]);
+        tm_stash_load<R, RAD>(tm_lane_base(cb_tm_base), stash_col<R, RAD, PER, CARRYS>(SCOL, p), v[p]);
     }
     const int j = jb + p * SLOTS;
     const int d0 = (j / NS) * NS * RAD + j % NS;
@@ -1070,6 +1130,7 @@ __device__ __forceinline__ void fft2_boundary(Cx<R>* __restrict__ F,
   constexpr int PER = (Q / RAD) / SLOTS;
   constexpr int SF = padded_len(Q);
   constexpr bool STASH = (SFW & kStash) != 0 && PER > 1;
+  constexpr bool CARRYS = (SFW & kCarry) != 0;
   constexpr int SCOL = tm_total((int)sizeof(R), Q, NT);
   PassRows<R, Q, NT, NSF, SFW> rows;
   rows.fetch(twHead);
@@ -1099,7 +1160,7 @@ __device__ __forceinline__ void fft2_boundary(Cx<R>* __restrict__ F,
     for (int r = 0; r < RAD; ++r) v[p][r] = u[r];
     if constexpr (STASH) {
       if (p < PER - 1)
-        tm_stash_store<R, RAD>(tm_lane_base(cb_tm_base), stash_col<R, RAD, PER>(SCOL, p), v[p]);
+        tm_stash_store<R, RAD>(tm_lane_base(cb_tm_base), stash_col<R, RAD, PER, CARRYS>(SCOL, p), v[p]);
     }
   }
   if constexpr (STASH) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -1109,7 +1170,7 @@ __device__ __forceinline__ void fft2_boundary(Cx<R>* __restrict__ F,
     const int p = STASH ? (pp == 0 ? PER - 1 : pp - 1) : pp;
     if constexpr (STASH) {
       if (pp > 0)
-        tm_stash_load<R, RAD>(tm_lane_base(cb_tm_base), stash_col<R, RAD, PER>(SCOL, p), v[p]);
+        tm_stash_load<R, RAD>(tm_lane_base(cb_tm_base), stash_col<R, RAD, PER, CARRYS>(SCOL, p), v[p]);
     }
     const int j = jb + p * SLOTS;
     Cx<R>* b = Fp + pad(j * RAD);  // inverse first pass: NS = 1, d0 = R*j
@@ -1726,7 +1787,8 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
   static_assert((H / 8) >= NT, "half-length passes must keep every thread busy");
   // TMEM: twiddle rows, then the butterfly parking of the P*NT/128 lane
   // sharers (at most 3 radix-8 or 1 radix-16 butterfly each)
-  constexpr int TM_NEED = tm_total((int)sizeof(R), Q, NT) + (NTC / 128) * stash_stride<R>();
+  constexpr bool CARRY = CB_CARRY && sizeof(R) == 4;
+  constexpr int TM_NEED = tm_total((int)sizeof(R), Q, NT) + (NTC / 128) * stash_stride<R>(CARRY);
   constexpr bool TMON = !defined_no_tmem() && TM_NEED <= 512;
   constexpr int COLS = pow2_cols(TM_NEED);
 #ifndef CB_GB_FIELD
@@ -1735,8 +1797,9 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
 #ifndef CB_GB_HALF
 #define CB_GB_HALF kGroupBar
 #endif
-  constexpr int FI = (TMON ? (kMid | kTM | kStash) : kTail) | CB_GB_FIELD;
-  constexpr int FF = (TMON ? (kMid | kTM | kStash) : kHead) | CB_GB_FIELD;
+  constexpr int FC = CARRY ? kCarry : 0;
+  constexpr int FI = (TMON ? (kMid | kTM | kStash | FC) : kTail) | CB_GB_FIELD;
+  constexpr int FF = (TMON ? (kMid | kTM | kStash | FC) : kHead) | CB_GB_FIELD;
   constexpr int HS = kHalf | kWide | (TMON ? kTM : 0) | CB_GB_HALF;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
