@@ -478,12 +478,14 @@ def main():
                "path": "per rank: pinned halo'd input slice H2D, cbessfm_run on its block "
                        "range, kept samples D2H"}
     elif not (args.no_e2e or args.profile or big):
-        # a streaming receiver: two steps in flight on two streams with
-        # double-buffered host outputs, so step k+1's H2D overlaps step k's
-        # kernel tail and D2H; every step still copies its whole input in
-        # and its whole result out
-        inflight = int(os.environ.get("BENCH_E2E_INFLIGHT", "2"))
-        chunks = int(os.environ.get("BENCH_E2E_CHUNKS", "8"))
+        # a streaming receiver: three steps in flight on three streams with
+        # triple-buffered host outputs, so step k+1's H2D overlaps step k's
+        # kernel and D2H; every step still copies its whole input in and its
+        # whole result out. With steps overlapping each other, 3 chunks per
+        # step beat 8 (fewer, larger copies; tools/e2e_sweep.sh: ~2.95-3.08e9
+        # vs ~2.74-2.77e9 2D/s)
+        inflight = int(os.environ.get("BENCH_E2E_INFLIGHT", "3"))
+        chunks = int(os.environ.get("BENCH_E2E_CHUNKS", "3"))
         hx = x.cpu().pin_memory()
         houts = [torch.empty_like(hx).pin_memory() for _ in range(inflight)]
         sides = [torch.cuda.Stream(dev) for _ in range(inflight)]
@@ -517,7 +519,8 @@ def main():
                "h2d_bytes_per_step": int(hx.numel() * hx.element_size()),
                "d2h_bytes_per_step": int(houts[0].numel() * houts[0].element_size()),
                "path": "C ABI cbessfm_run_host (via DbpEngine.run_host): pinned host buffers, "
-                       "chunked H2D / fused kernel / D2H overlap, two steps in flight"}
+                       f"chunked H2D / fused kernel / D2H overlap ({chunks} chunks), "
+                       f"{inflight} steps in flight"}
 
     # the only collective of the path: final gather of the kept samples to
     # every rank (all_gather over NCCL), timed separately from `value`

@@ -305,6 +305,9 @@ constexpr int kWide = 32;
 // them back: butterfly j produces exactly the samples j + r*Q/16 that
 // butterfly j of the next pass consumes, so the field's shared-memory round
 // trip between the two, and both passes' load/store barriers, disappear
+#ifndef CB_ROT_MUFU
+#define CB_ROT_MUFU 0
+#endif
 #ifndef CB_CARRY
 #define CB_CARRY 1
 #endif
@@ -745,6 +748,14 @@ __device__ __forceinline__ void sincos_acc<float>(float a, float* s, float* c) {
     rd = fma(jd, -6.123233995736766036e-17, rd);
     r = (float)rd;
     q = (int)((long long)jd & 3);
+  } else if (CB_ROT_MUFU) {
+    // experiment: reduction to [-pi, pi] and the SFU sin/cos (abs error
+    // ~2^-21 on that range) instead of the FMA-pipe polynomials
+    const float j = rintf(a * 0.159154943091895336f);
+    r = __fmaf_rn(j, -6.28318548202514648f, a);
+    r = __fmaf_rn(j, 1.74845553146951162e-7f, r);
+    __sincosf(r, s, c);
+    return;
   } else {
     const float j = rintf(a * 0.636619772367581343f);
     r = __fmaf_rn(j, -0x1.921fb6p+0f, a);
