@@ -1870,6 +1870,16 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
       Fr[SF + pad(t2)] = src[prm.in_pstride + idx];
     }
   }
+  // per-step scalars (theta scale, phasor table index) staged in shared
+  // memory: read in the step loop right before the rotation FFT and the
+  // boundary pass, where an L2 round trip would stall every warp
+  constexpr int kStepCache = 256;
+  __shared__ R s_tsc[kStepCache];
+  __shared__ int s_phi[kStepCache + 1];
+  for (int i = (int)threadIdx.x; i <= prm.n_steps && i <= kStepCache; i += NTC) {
+    if (i < prm.n_steps && i < kStepCache) s_tsc[i] = theta_scale[i];
+    s_phi[i] = prm.ph_index[i];
+  }
   __syncthreads();
   if constexpr (TMON) asm volatile("tcgen05.fence::after_thread_sync;");
   CB_MARK(1);
@@ -2104,8 +2114,9 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
     CB_MARK(8 + 8 * st + 5);
     RotationHook<R> rot;
     rot.th = Treal;
-    rot.scale = theta_scale[st];
-    const Cx<R>* ph_next = ph_grp + (size_t)prm.ph_index[st + 1] * ph_tab;
+    rot.scale = st < kStepCache ? s_tsc[st] : theta_scale[st];
+    const Cx<R>* ph_next =
+        ph_grp + (size_t)(st < kStepCache ? s_phi[st + 1] : prm.ph_index[st + 1]) * ph_tab;
     if (st + 1 < prm.n_steps) {
       fft2<R, Q, NT, FF, false, RotationHook<R>, NoHook, 1, Q / sched_radix(Q, 1, FI)>(
           F, twpF, &s_zero, rot);
