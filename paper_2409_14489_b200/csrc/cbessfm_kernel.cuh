@@ -1543,6 +1543,11 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
   CB_MARK(3);
   constexpr int KU = (H / 2 + 1 + NT - 1) / NT;  // untangle/twist bins per thread
   for (int st = 0; st < prm.n_steps; ++st) {
+    // per-step scalars issued at the top of the step: their L2 latency
+    // overlaps the intensity transforms instead of stalling the rotation
+    // FFT and the boundary pass
+    const R tsc_st = theta_scale[st];
+    const int phi_next = prm.ph_index[st + 1];  // n_steps + 1 entries
     // W_Q^k of this thread's untangle/twist bins, issued before the FFT so
     // the L2 latency hides behind it (the same k serve both)
     Cx<R> twk[KU];
@@ -1666,8 +1671,8 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
     // applies the final phasor (dbp.py:399)
     RotationHook<R> rot;
     rot.th = Treal;
-    rot.scale = theta_scale[st];
-    const Cx<R>* ph_next = ph_rank + (size_t)prm.ph_index[st + 1] * ph_tab;
+    rot.scale = tsc_st;
+    const Cx<R>* ph_next = ph_rank + (size_t)phi_next * ph_tab;
     if (st + 1 < prm.n_steps) {
       fft2<R, Q, NT, FF, false, RotationHook<R>, NoHook, 1, Q / sched_radix(Q, 1, FI)>(
           F, twpF, &s_zero, rot);
