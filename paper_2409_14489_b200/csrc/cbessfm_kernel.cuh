@@ -1240,8 +1240,9 @@ __device__ __forceinline__ void fft1_pass(Cx<R>* __restrict__ buf, const Cx<R>* 
       const bool on = (NB % 32 == 0) || tid < NB;
       const Cx<R>* w = rows.row(0);  // warp-converged (TMEM)
       if (on) body_load(tid, v, w);
-      // (kGroupBar: one id per group, after the groups' pass ids 1..P)
-      bar_named((HS & kGroupBar) ? 1 + (int)(blockDim.x / NT) + (int)threadIdx.x / NT : 1, ACT);
+      // (several groups per CTA: one id per group, after the groups' pass
+      // ids 1..P, whether the pass ends on a group or a CTA barrier)
+      bar_named((int)blockDim.x > NT ? 1 + (int)(blockDim.x / NT) + (int)threadIdx.x / NT : 1, ACT);
       if (on) body_store(tid, v);
     }
     next.fetch(twp);
