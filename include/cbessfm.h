@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define CBESSFM_VERSION 2
+#define CBESSFM_VERSION 3
 
 typedef enum {
   CBESSFM_OK = 0,
@@ -118,6 +118,8 @@ typedef struct {
   int64_t smem_per_cta;
   int32_t max_active_clusters;
   int32_t q;               /* per-subband FFT size N' = N / N_sb          */
+  char kernel[64];         /* the block kernel a device-resident launch   */
+                           /* runs, e.g. "cbessfm_block_kernel<double,5,2048>" (ABI 3) */
 } cbessfm_plan_info;
 
 /* Version of this ABI (CBESSFM_VERSION). */
@@ -155,10 +157,11 @@ cbessfm_status cbessfm_nlpr(int32_t dtype, int32_t n_subbands, int32_t n_prime, 
 
 /* Replace the coefficient-set tables of a plan (same geometry, same n_sets):
  * mimo [n_sets][P][Q/2+1] and theta_scale [n_sets][n_steps], HOST, laid
- * out as in cbessfm_desc. Ordered on `stream` and synchronous; an
+ * out as in cbessfm_desc. n_sets must equal the plan's (CBESSFM_ERR_INVALID
+ * otherwise: the host arrays are read for exactly that many sets). Ordered on `stream` and synchronous; an
  * optimiser re-evaluating candidate taps reuses one plan this way instead
  * of rebuilding it (the dispersion tables and twiddles do not change). */
-cbessfm_status cbessfm_plan_update_sets(cbessfm_plan* plan, const double* mimo,
+cbessfm_status cbessfm_plan_update_sets(cbessfm_plan* plan, int32_t n_sets, const double* mimo,
                                         const double* theta_scale, void* stream);
 
 /* Free the plan's device tables. */

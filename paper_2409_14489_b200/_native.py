@@ -51,7 +51,12 @@ class HostIo(C.Structure):
 class PlanInfo(C.Structure):
     _fields_ = [("threads_per_cta", C.c_int32), ("cluster_size", C.c_int32),
                 ("smem_per_cta", C.c_int64),
-                ("max_active_clusters", C.c_int32), ("q", C.c_int32)]
+                ("max_active_clusters", C.c_int32), ("q", C.c_int32),
+                ("kernel", C.c_char * 64)]
+
+    @property
+    def kernel_name(self) -> str:
+        return self.kernel.decode()
 
 
 class SsfmDesc(C.Structure):
@@ -93,7 +98,7 @@ SIGNATURES = {
     "cbessfm_run_host": (C.c_int, [C.c_void_p, C.POINTER(HostIo), C.c_void_p]),
     "cbessfm_nlpr": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                C.POINTER(C.c_double), C.c_double, C.c_void_p]),
-    "cbessfm_plan_update_sets": (C.c_int, [C.c_void_p, C.POINTER(C.c_double),
+    "cbessfm_plan_update_sets": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_double),
                                            C.POINTER(C.c_double), C.c_void_p]),
     "cbessfm_plan_destroy": (C.c_int, [C.c_void_p]),
     "cbessfm_last_error": (C.c_char_p, []),
@@ -125,7 +130,7 @@ _lib = None
 _lock = threading.Lock()
 
 
-ABI_VERSION = 2   # CBESSFM_VERSION in include/cbessfm.h
+ABI_VERSION = 3   # CBESSFM_VERSION in include/cbessfm.h
 
 
 def load() -> C.CDLL:
@@ -222,7 +227,10 @@ class NativePlan:
         """Overwrite the coefficient-set tables (cbessfm_plan_update_sets)."""
         mi = np.ascontiguousarray(mimo, np.complex128)
         th = np.ascontiguousarray(theta_scale, np.float64)
-        check(self._lib.cbessfm_plan_update_sets(self.handle, _dptr(mi.view(np.float64)),
+        if mi.ndim != 3 or th.ndim != 2 or mi.shape[0] != th.shape[0]:
+            raise ValueError("mimo must be [n_sets, P, Q/2+1] and theta_scale [n_sets, n_steps]")
+        check(self._lib.cbessfm_plan_update_sets(self.handle, mi.shape[0],
+                                                 _dptr(mi.view(np.float64)),
                                                  _dptr(th), C.c_void_p(stream)),
               "cbessfm_plan_update_sets")
 

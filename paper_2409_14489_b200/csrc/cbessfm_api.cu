@@ -291,6 +291,22 @@ cudaError_t dispatch<double>(int P, const cbessfm::Params<double>& prm, int q, i
 }
 #undef CB_CASE
 
+// Every entry point that touches a plan runs on the plan's device and
+// restores the caller's current device on return (a process may drive
+// several GPUs from one thread).
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 // set while cbessfm_run_host issues its pipelined chunk launches
 thread_local int g_kernel_pref = 0;
 
@@ -386,17 +402,10 @@ cbessfm_status cbessfm_plan_create(const cbessfm_desc* d, cbessfm_plan** out) {
   p->n_phasors = d->n_phasors;
   p->n_sets = d->n_sets > 1 ? d->n_sets : 1;
   p->device = d->device;
-  cudaError_t e = cudaSetDevice(d->device);
-  if (e != cudaSuccess) {
+  DeviceGuard dg(d->device);
+  if (dg.err != cudaSuccess) {
     delete p;
-    return cuda_fail(e, "cudaSetDevice");
-  }
-  // cbessfm_run_host allocates its staging buffers stream-ordered: keep
-  // freed blocks in the device's default pool instead of returning them
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, d->device) == cudaSuccess) {
-    uint64_t keep_all = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep_all);
+    return cuda_fail(dg.err, "cudaSetDevice");
   }
   const cbessfm_status st =
       p->dtype == CBESSFM_C64 ? upload_all<float>(p, d) : upload_all<double>(p, d);
@@ -411,6 +420,8 @@ cbessfm_status cbessfm_plan_create(const cbessfm_desc* d, cbessfm_plan** out) {
 cbessfm_status cbessfm_plan_info_get(const cbessfm_plan* p, cbessfm_plan_info* info) {
   g_err.clear();
   if (!p || !info) return fail(CBESSFM_ERR_INVALID, "null plan or info");
+  DeviceGuard dg(p->device);
+  if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
   cbessfm::KernelInfo ki{};
   cudaError_t e;
   if (p->dtype == CBESSFM_C64) {
@@ -426,6 +437,7 @@ cbessfm_status cbessfm_plan_info_get(const cbessfm_plan* p, cbessfm_plan_info* i
   info->smem_per_cta = (int64_t)ki.smem;
   info->max_active_clusters = ki.max_active_clusters;
   info->q = p->Q;
+  snprintf(info->kernel, sizeof info->kernel, "%s", ki.name);
   return CBESSFM_OK;
 }
 
@@ -442,6 +454,8 @@ cbessfm_status cbessfm_run(const cbessfm_plan* p, const cbessfm_io* io, void* st
     return fail(CBESSFM_ERR_INVALID, "origins out of range");
   const int64_t nclusters = io->batch * (io->block_end - io->block_begin);
   if (nclusters == 0) return CBESSFM_OK;
+  DeviceGuard dg(p->device);
+  if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e;
   if (p->dtype == CBESSFM_C64)
@@ -467,6 +481,8 @@ cbessfm_status cbessfm_run_host(const cbessfm_plan* cp, const cbessfm_host_io* i
   const size_t rowb = (size_t)n * esz, rows = (size_t)batch * 2;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   std::lock_guard<std::mutex> lock(p->host_mu);
+  DeviceGuard dg(p->device);
+  if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
   cudaError_t e;
   while ((int)p->host_streams.size() < 2 + chunks) {
     cudaStream_t s2;
@@ -484,14 +500,17 @@ cbessfm_status cbessfm_run_host(const cbessfm_plan* cp, const cbessfm_host_io* i
     cudaStreamWaitEvent(st, slot.done, 0);  // its previous call's D2H has finished
   }
   if (slot.bytes < rows * rowb) {
-    cudaFreeAsync(slot.din, st);
-    cudaFreeAsync(slot.dout, st);
+    // grow the slot (rare: first call or a longer waveform). Plain
+    // cudaMalloc/cudaFree: the slot outlives the call, and the device's
+    // default stream-ordered pool is left alone
+    if (slot.done) cudaEventSynchronize(slot.done);
+    cudaFree(slot.din);
+    cudaFree(slot.dout);
     slot.din = slot.dout = nullptr;
     slot.bytes = 0;
-    if ((e = cudaMallocAsync(&slot.din, rows * rowb, st)) != cudaSuccess)
-      return cuda_fail(e, "alloc in");
-    if ((e = cudaMallocAsync(&slot.dout, rows * rowb, st)) != cudaSuccess) {
-      cudaFreeAsync(slot.din, st);
+    if ((e = cudaMalloc(&slot.din, rows * rowb)) != cudaSuccess) return cuda_fail(e, "alloc in");
+    if ((e = cudaMalloc(&slot.dout, rows * rowb)) != cudaSuccess) {
+      cudaFree(slot.din);
       slot.din = nullptr;
       return cuda_fail(e, "alloc out");
     }
@@ -560,12 +579,19 @@ cbessfm_status cbessfm_run_host(const cbessfm_plan* cp, const cbessfm_host_io* i
   return CBESSFM_OK;
 }
 
-cbessfm_status cbessfm_plan_update_sets(cbessfm_plan* p, const double* mimo,
+cbessfm_status cbessfm_plan_update_sets(cbessfm_plan* p, int32_t n_sets, const double* mimo,
                                         const double* theta_scale, void* stream) {
   g_err.clear();
   if (!p || !mimo || (p->n_steps > 0 && !theta_scale))
     return fail(CBESSFM_ERR_INVALID, "null plan or tables");
   if (p->n_steps == 0) return fail(CBESSFM_ERR_INVALID, "plan has no nonlinear steps");
+  if (n_sets != p->n_sets) {
+    char buf[128];
+    snprintf(buf, sizeof buf, "plan holds %d coefficient sets, %d given", p->n_sets, (int)n_sets);
+    return fail(CBESSFM_ERR_INVALID, buf);
+  }
+  DeviceGuard dg(p->device);
+  if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const cudaError_t e = p->dtype == CBESSFM_C64 ? rewrite_sets<float>(p, mimo, theta_scale, st)
                                                 : rewrite_sets<double>(p, mimo, theta_scale, st);
@@ -574,6 +600,8 @@ cbessfm_status cbessfm_plan_update_sets(cbessfm_plan* p, const double* mimo,
 
 cbessfm_status cbessfm_plan_destroy(cbessfm_plan* p) {
   g_err.clear();
+  if (!p) return CBESSFM_OK;
+  DeviceGuard dg(p->device);
   free_plan(p);
   return CBESSFM_OK;
 }
@@ -583,6 +611,7 @@ const char* cbessfm_last_error(void) { return g_err.c_str(); }
 int32_t cbessfm_debug_phase_times(const cbessfm_plan* p, int64_t* out, int32_t n) {
   if (!p || !out || !p->dbg) return 0;
   if (n > kDbgSlots) n = kDbgSlots;
+  DeviceGuard dg(p->device);
   return cudaMemcpy(out, p->dbg, sizeof(long long) * n, cudaMemcpyDeviceToHost) == cudaSuccess
              ? n
              : -1;

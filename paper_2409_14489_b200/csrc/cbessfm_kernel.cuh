@@ -776,10 +776,46 @@ __device__ __forceinline__ void sincos_acc<float>(float a, float* s, float* c) {
   *s = (q & 2) ? -ss : ss;
   *c = ((q + 1) & 2) ? -cc : cc;
 }
+// FP64: two-term FMA Cody-Waite reduction to [-pi/4, pi/4] (a - j*pi/2 is
+// formed with one rounding; the tail constant carries pi/2 to ~2^-106) and
+// the fdlibm kernel polynomials (degree 13 / 14, about 1 ulp): ~20 FP64
+// instructions, no branchy libdevice path. Arguments beyond 2^20 (never
+// reached by a per-step nonlinear phase, but legal) take libdevice sincos.
+#ifndef CB_LIBDEVICE_SINCOS
+template <>
+__device__ __forceinline__ void sincos_acc<double>(double a, double* s, double* c) {
+  if (fabs(a) > 1048576.0) {
+    sincos(a, s, c);
+    return;
+  }
+  const double j = rint(a * 0.63661977236758134308);
+  double r = fma(j, -1.57079632679489655800e+00, a);
+  r = fma(j, -6.12323399573676603587e-17, r);
+  const int q = (int)j;
+  const double r2 = r * r;
+  double ps = fma(r2, 1.58969099521155010221e-10, -2.50507602534068634195e-08);
+  ps = fma(r2, ps, 2.75573137070700676789e-06);
+  ps = fma(r2, ps, -1.98412698298579493134e-04);
+  ps = fma(r2, ps, 8.33333333332248946124e-03);
+  ps = fma(r2, ps, -1.66666666666666324348e-01);
+  const double sn = fma(r * r2, ps, r);
+  double pc = fma(r2, -1.13596475577881948265e-11, 2.08757232129817482790e-09);
+  pc = fma(r2, pc, -2.75573143513906633035e-07);
+  pc = fma(r2, pc, 2.48015872894767294178e-05);
+  pc = fma(r2, pc, -1.38888888888741095749e-03);
+  pc = fma(r2, pc, 4.16666666666666019037e-02);
+  const double cs = fma(r2 * r2, pc, fma(r2, -0.5, 1.0));
+  const double ss = (q & 1) ? cs : sn;
+  const double cc = (q & 1) ? sn : cs;
+  *s = (q & 2) ? -ss : ss;
+  *c = ((q + 1) & 2) ? -cc : cc;
+}
+#else
 template <>
 __device__ __forceinline__ void sincos_acc<double>(double a, double* s, double* c) {
   sincos(a, s, c);
 }
+#endif
 
 // Rotate by exp(-i theta), theta = scale * th[p] (dbp.py:196, :208); th is
 // the float view of the packed irfft output. The two half-warps hold the

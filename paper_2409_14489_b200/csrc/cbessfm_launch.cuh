@@ -2,6 +2,7 @@
 // cudaLaunchKernelEx, dynamic shared memory opt-in, non-portable clusters).
 #pragma once
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "cbessfm_kernel.cuh"
@@ -13,7 +14,13 @@ struct KernelInfo {
   int cluster;
   size_t smem;
   int max_active_clusters;
+  char name[64];  // the kernel a launch of this shape runs
 };
+
+template <typename R>
+constexpr const char* real_name() {
+  return sizeof(R) == 4 ? "float" : "double";
+}
 
 template <typename R>
 constexpr int max_q() {
@@ -46,6 +53,7 @@ cudaError_t launch_fat(const Params<R>& prm, int64_t nblocks, cudaStream_t strea
     info->threads = NT;
     info->cluster = 1;
     info->smem = smem;
+    snprintf(info->name, sizeof info->name, "cbessfm_fat_kernel<%s,%d,%d>", real_name<R>(), P, Q);
     int per_sm = 0, sms = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
     if (e != cudaSuccess) return e;
@@ -149,6 +157,7 @@ cudaError_t launch_one(const Params<R>& prm, int64_t nclusters, cudaStream_t str
     info->threads = NT;
     info->cluster = P;
     info->smem = smem;
+    snprintf(info->name, sizeof info->name, "cbessfm_block_kernel<%s,%d,%d>", real_name<R>(), P, Q);
     cfg.gridDim = dim3(P, 1, 1);
     int nc = 0;
     if (P > 1) {

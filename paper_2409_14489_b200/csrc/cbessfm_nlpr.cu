@@ -142,14 +142,30 @@ cudaError_t run_q(const void* in, void* out, const double* T, int P, double thet
   std::vector<R> hq(2 * (size_t)Q), ht(2 * (size_t)P * P * (H + 1));
   for (size_t m = 0; m < hq.size(); ++m) hq[m] = (R)tq[m];
   for (size_t m = 0; m < ht.size(); ++m) ht[m] = (R)T[m];
-  void *dtq = nullptr, *dtp = nullptr, *dT = nullptr;
+  // stream-ordered scratch, released on every exit path (also when a later
+  // allocation or upload fails)
+  struct Frees {
+    cudaStream_t st;
+    void* p[3] = {nullptr, nullptr, nullptr};
+    ~Frees() {
+      for (void* q : p)
+        if (q) cudaFreeAsync(q, st);
+    }
+  } fr{st};
+  void *&dtq = fr.p[0], *&dtp = fr.p[1], *&dT = fr.p[2];
   cudaError_t e;
   if ((e = cudaMallocAsync(&dtq, hq.size() * sizeof(R), st)) != cudaSuccess) return e;
   if ((e = cudaMallocAsync(&dtp, hp.size() * sizeof(R) + 16, st)) != cudaSuccess) return e;
   if ((e = cudaMallocAsync(&dT, ht.size() * sizeof(R), st)) != cudaSuccess) return e;
-  cudaMemcpyAsync(dtq, hq.data(), hq.size() * sizeof(R), cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(dtp, hp.data(), hp.size() * sizeof(R), cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(dT, ht.data(), ht.size() * sizeof(R), cudaMemcpyHostToDevice, st);
+  if ((e = cudaMemcpyAsync(dtq, hq.data(), hq.size() * sizeof(R), cudaMemcpyHostToDevice, st)) !=
+          cudaSuccess ||
+      (e = cudaMemcpyAsync(dtp, hp.data(), hp.size() * sizeof(R), cudaMemcpyHostToDevice, st)) !=
+          cudaSuccess ||
+      (e = cudaMemcpyAsync(dT, ht.data(), ht.size() * sizeof(R), cudaMemcpyHostToDevice, st)) !=
+          cudaSuccess) {
+    cudaStreamSynchronize(st);  // the host staging vectors may still be read
+    return e;
+  }
   auto kern = nlpr_kernel<R, Q>;
   const size_t smem = sizeof(Cx<R>) * 2 * (size_t)padded_len(H + 1);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -170,10 +186,8 @@ cudaError_t run_q(const void* in, void* out, const double* T, int P, double thet
                          reinterpret_cast<Cx<R>*>(out), reinterpret_cast<const Cx<R>*>(dT),
                          reinterpret_cast<const Cx<R>*>(dtq), reinterpret_cast<const Cx<R>*>(dtp),
                          (R)(theta_scale / Q), P);
-  cudaFreeAsync(dtq, st);
-  cudaFreeAsync(dtp, st);
-  cudaFreeAsync(dT, st);
   // the host staging vectors are read by the async copies: wait for them
+  // (the scratch is freed stream-ordered when `fr` goes out of scope)
   const cudaError_t s2 = cudaStreamSynchronize(st);
   return e != cudaSuccess ? e : s2;
 }

@@ -209,6 +209,8 @@ def launch(plan: _native.NativePlan, x, out, *, n: int | None = None,
     n = x.shape[2] if n is None else n
     sched = BlockSchedule(n, plan.block_size, plan.overlap)
     b0, b1 = (0, sched.n_blocks) if block_range is None else block_range
+    if x.device.index != plan.device or out.device.index != plan.device:
+        raise ValueError(f"tensors on {x.device}/{out.device}, plan on cuda:{plan.device}")
     if stream is None:
         stream = torch.cuda.current_stream(x.device)
     plan.run(in_ptr=x.data_ptr(), in_batch_stride=x.stride(0),
@@ -381,10 +383,12 @@ class SetEvaluator:
     def __call__(self, x, coeff_sets, out=None, stream=None):
         torch = _torch()
         coeff_sets = list(coeff_sets)
+        # the same checks on every call, the first included: a plan built
+        # from fewer (or more) sets than n_sets would reuse (or over-read) sets
+        mimo, theta = self._tables(coeff_sets)
         if self.plan is None:
             self.plan = _sets_plan(self.cfg, self.rate, coeff_sets, self.dtype, self.device)
         else:
-            mimo, theta = self._tables(coeff_sets)
             with torch.cuda.device(self.device):
                 st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
                 self.plan.update_sets(mimo, theta, st)
@@ -482,6 +486,8 @@ class DbpEngine:
             out = torch.empty(x.shape, dtype=x.dtype, pin_memory=x.is_pinned())
         if out.shape != x.shape or not out.is_contiguous() or out.is_cuda:
             raise ValueError("out must be a contiguous host tensor shaped like x")
+        # the C ABI selects the plan's device itself; the default stream is
+        # this engine's device's current stream, not the caller's device's
         stream = stream or torch.cuda.current_stream(self.device)
         self.plan.run_host(in_ptr=x.data_ptr(), out_ptr=out.data_ptr(), n=n,
                            batch=x.shape[0], chunks=chunks, stream=stream.cuda_stream)

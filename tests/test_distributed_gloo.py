@@ -23,6 +23,8 @@ def _free_port():
 
 def _oracle_compute(cfg, rate, coeffs):
     def run(x_slice, work, n):
+        import torch
+        x_slice = x_slice.numpy()
         outs = []
         for wf in x_slice:
             full = np.zeros((2, n), dtype=complex)
@@ -31,7 +33,7 @@ def _oracle_compute(cfg, rate, coeffs):
             b0, b1 = work.shard.blocks
             res = orc.run_cb_blocks(full, cfg, rate, coeffs, b0, b1)
             outs.append(res[:, work.out_begin:work.out_end])
-        return np.stack(outs)
+        return torch.from_numpy(np.stack(outs))
     return run
 
 
@@ -47,6 +49,7 @@ def _worker(rank, world, port, name, batch, q):
         out = run_distributed(x, g.cfg.block_size, g.cfg.overlap,
                               _oracle_compute(g.cfg, g.wave.sample_rate, g.coeffs))
         if rank == 0:
+            out = out.numpy()
             ref = np.stack([orc.run_cb_blocks(xb, g.cfg, g.wave.sample_rate, g.coeffs)
                             for xb in x])
             q.put(("ok", bool(np.array_equal(out, ref)),

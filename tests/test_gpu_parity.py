@@ -38,6 +38,29 @@ def test_golden_parity(cuda, name, dtype):
     assert err < TOL[dtype], f"{name} {dtype}: rel L2 {err:.3e}"
 
 
+def test_c64_precision_headroom(cuda):
+    # guard for FP32 "fast path" kernel changes (round-1 MUFU sincos went to
+    # 1.5e-5 on the 50-step case): every golden case stays at <= half the
+    # 1e-5 bar in c64, so a precision regression fails here before parity
+    worst = max((rel_rms(_run(golden(name), "c64"), golden(name).out), name)
+                for name in CASES)
+    assert worst[0] <= 5e-6, f"c64 worst case {worst[1]}: rel L2 {worst[0]:.3e}"
+
+
+def test_set_evaluator_rejects_wrong_set_count_first_call(cuda):
+    # the first call validates like every later one: a plan
+    # built from fewer sets than n_sets would silently reuse sets
+    import torch
+    g = golden("cfg1_nsb3_st2")
+    x = torch.from_numpy(np.vstack([g.wave.x, g.wave.y])).to(cuda)
+    ev = pb.SetEvaluator(g.cfg, g.wave.sample_rate, 3, dtype="c128")
+    with pytest.raises(ValueError):
+        ev(x, [g.coeffs, g.coeffs])
+    assert ev.plan is None
+    with pytest.raises(ValueError):
+        ev.__class__(g.cfg, g.wave.sample_rate, 2, dtype="c128")(x, [g.coeffs] * 3)
+
+
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
 def test_single_band_equals_essfm(cuda, dtype):
     # pkg/tests/test_dbp.py:60-64, against the reference ESSFM output
@@ -167,20 +190,23 @@ def test_counter_hook_matches_reference_cost(cuda):
 
 def test_gpu_compute_time_shards_reassemble(cuda):
     # the product's per-rank compute of distributed.run_distributed, run for
-    # both ranks of a world of 2 in one process (no collective needed here)
-    from paper_2409_14489_b200.distributed import gpu_compute, shard_work
-    from paper_2409_14489_b200.planner import gather_slice
+    # both ranks of a world of 2 in one process (no collective needed here):
+    # slices cut on the device, pieces stay device tensors in the plan dtype
+    import torch
+    from paper_2409_14489_b200.distributed import circular_slice, gpu_compute, shard_work
     g = golden("cfg2_nsb5")
-    x = np.vstack([g.wave.x, g.wave.y])[None]
+    x = torch.from_numpy(np.vstack([g.wave.x, g.wave.y])[None]).cuda()
     n = x.shape[-1]
-    eng = pb.DbpEngine(g.cfg, g.coeffs, g.wave.sample_rate, dtype="c128")
-    run = gpu_compute(eng)
-    out = np.zeros_like(x)
-    for rank in range(2):
-        w = shard_work(n, g.cfg.block_size, g.cfg.overlap, 1, 2, rank)
-        xs = gather_slice(x, w.in_origin, w.in_length)
-        out[:, :, w.out_begin:w.out_end] = run(xs, w, n)
-    assert rel_rms(out[0], g.out) < 1e-12
+    for dtype, tol in (("c128", 1e-12), ("c64", 1e-5)):
+        eng = pb.DbpEngine(g.cfg, g.coeffs, g.wave.sample_rate, dtype=dtype)
+        run = gpu_compute(eng)
+        out = torch.zeros_like(x, dtype=eng.torch_dtype)
+        for rank in range(2):
+            w = shard_work(n, g.cfg.block_size, g.cfg.overlap, 1, 2, rank)
+            piece = run(circular_slice(x, w.in_origin, w.in_length), w, n)
+            assert piece.is_cuda and piece.dtype == eng.torch_dtype
+            out[:, :, w.out_begin:w.out_end] = piece
+        assert rel_rms(out[0].to(torch.complex128).cpu().numpy(), g.out) < tol
 
 
 @pytest.mark.parametrize("chunks", [1, 3, 8])
