@@ -18,7 +18,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 BUILD = PKG.parent / "build" / "cbessfm"
 LIB = PKG / "libcbessfm.so"
-HEADERS = [CSRC / "cbessfm_kernel.cuh", CSRC / "cbessfm_launch.cuh",
+HEADERS = [CSRC / "cbessfm_kernel.cuh", CSRC / "cbessfm_launch.cuh", CSRC / "cbessfm_ip.cuh",
            PKG.parent / "include" / "cbessfm.h",
            PKG.parent / "include" / "cbessfm_peaks.h",
            PKG.parent / "include" / "cbessfm_ssfm.h",

@@ -85,6 +85,7 @@ std::vector<double> pass_tables(int Q, const std::vector<double>& tq, int real_b
 struct cbessfm_plan {
   int dtype, P, Q, N, overlap, n_steps, n_phasors, n_sets, device;
   void* phasor = nullptr;  // [n_phasors][P][Q]
+  void* phasor_rev = nullptr;  // the same rows in cbessfm_ip_kernel's bin order (c128, Q = 2048)
   int* ph_index = nullptr; // [n_steps + 1]
   void* mimo = nullptr;    // [P][Q/2+1]
   void* theta = nullptr;   // [n_sets][n_steps]
@@ -212,6 +213,20 @@ cbessfm_status upload_all(cbessfm_plan* p, const cbessfm_desc* d) {
   cudaError_t e;
   if ((e = upload_complex<R>(d->phasors, (size_t)p->n_phasors * PQ, &p->phasor, true)) != cudaSuccess)
     return cuda_fail(e, "upload phasors");
+  if (sizeof(R) == 8 && p->Q == cbessfm::kIpQ && p->P >= 2) {
+    // permuted copy for the in-place-pass kernel: row (tab, subband), entry
+    // ip_rev_index(s, m0, m1) = natural bin s + 16 m0 + 128 m1
+    std::vector<double> rev(2 * (size_t)p->n_phasors * PQ);
+    for (size_t row = 0; row < (size_t)p->n_phasors * p->P; ++row)
+      for (int k = 0; k < p->Q; ++k) {
+        const size_t dst = row * p->Q + cbessfm::ip_rev_index(k & 15, (k >> 4) & 7, k >> 7);
+        rev[2 * dst] = d->phasors[2 * (row * p->Q + k)];
+        rev[2 * dst + 1] = d->phasors[2 * (row * p->Q + k) + 1];
+      }
+    if ((e = upload_complex<R>(rev.data(), (size_t)p->n_phasors * PQ, &p->phasor_rev, true)) !=
+        cudaSuccess)
+      return cuda_fail(e, "upload permuted phasors");
+  }
   if ((e = cudaMalloc((void**)&p->ph_index, sizeof(int) * (p->n_steps + 1))) != cudaSuccess)
     return cuda_fail(e, "alloc phasor index");
   if ((e = cudaMemcpy(p->ph_index, d->phasor_index, sizeof(int) * (p->n_steps + 1),
@@ -254,6 +269,7 @@ void free_plan(cbessfm_plan* p) {
   }
   for (cudaStream_t st : p->host_streams) cudaStreamDestroy(st);
   cudaFree(p->phasor);
+  cudaFree(p->phasor_rev);
   cudaFree(p->ph_index);
   cudaFree(p->mimo);
   cudaFree(p->theta);
@@ -329,6 +345,7 @@ cbessfm::Params<R> make_params(const cbessfm_plan* p, const cbessfm_io* io) {
   prm.keep = p->N - p->overlap;
   prm.half = p->overlap / 2;
   prm.phasor = reinterpret_cast<const C*>(p->phasor);
+  prm.phasor_rev = reinterpret_cast<const C*>(p->phasor_rev);
   prm.ph_index = p->ph_index;
   prm.mimo = reinterpret_cast<const C*>(p->mimo);
   prm.theta_scale = reinterpret_cast<const R*>(p->theta);
@@ -429,6 +446,7 @@ cbessfm_status cbessfm_plan_info_get(const cbessfm_plan* p, cbessfm_plan_info* i
     e = dispatch<float>(p->P, prm, p->Q, 0, nullptr, &ki);
   } else {
     cbessfm::Params<double> prm{};
+    prm.phasor_rev = reinterpret_cast<const cbessfm::Cx<double>*>(p->phasor_rev);
     e = dispatch<double>(p->P, prm, p->Q, 0, nullptr, &ki);
   }
   if (e != cudaSuccess) return cuda_fail(e, "kernel occupancy query");

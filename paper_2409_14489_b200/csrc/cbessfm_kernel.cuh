@@ -33,6 +33,7 @@
 #pragma once
 
 #include <cooperative_groups.h>
+#include <cstdio>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -41,6 +42,42 @@
 namespace cbessfm {
 
 namespace cg = cooperative_groups;
+
+// Checked builds (-DCB_CHECKED, `build.py --variant checked`), the stand-in
+// for compute-sanitizer, which this GPU pool does not allow:
+//  * CB_POISON_SMEM fills a kernel's dynamic shared memory with a NaN
+//    pattern (NaN as one f64 and as two f32) before first use, so a read of
+//    a slot no pass wrote -- or read before its writer's barrier, the race
+//    racecheck looks for -- reaches the output as NaN or as a bit difference
+//    against the unchecked build (tests/test_gpu_checked.py);
+//  * CB_CHECK traps on an out-of-range global, shared or cluster index.
+#ifdef CB_CHECKED
+#define CB_CHECK(cond)                                                               \
+  do {                                                                               \
+    if (!(cond)) {                                                                   \
+      printf("CB_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, \
+             #cond, (int)blockIdx.x, (int)threadIdx.x);                              \
+      __trap();                                                                      \
+    }                                                                                \
+  } while (0)
+__device__ __forceinline__ void cb_poison_smem(void* base) {
+  uint32_t bytes;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(bytes));
+  const uint32_t nt = blockDim.x * blockDim.y * blockDim.z;
+  const uint32_t tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  unsigned long long* p = reinterpret_cast<unsigned long long*>(base);
+  for (uint32_t i = tid; i < bytes / 8; i += nt) p[i] = 0x7ff8dead7ff8deadull;
+  __syncthreads();
+}
+#define CB_POISON_SMEM(base) cb_poison_smem(base)
+#else
+#define CB_CHECK(cond) \
+  do {                 \
+  } while (0)
+#define CB_POISON_SMEM(base) \
+  do {                       \
+  } while (0)
+#endif
 
 // Phase timestamps of CTA 0 (debug builds with -DCB_PHASE_PROFILE only;
 // read back with cbessfm_debug_phase_times).
@@ -642,6 +679,17 @@ __device__ __forceinline__ void push(uint32_t raddr, Cx<double> v, uint32_t rbar
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
                ::"r"(raddr), "d"(v.x), "d"(v.y), "r"(rbar)
                : "memory");
+}
+
+// 16-byte global -> shared copy that bypasses the registers (LDGSTS, L2 only):
+// a thread issues all of its window samples back to back and waits once
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(smem_dst)),
+               "l"(gmem_src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 __device__ __forceinline__ void bar_named(int id, int nthreads) {
@@ -1324,6 +1372,8 @@ struct Params {
   int64_t keep;     // block_size - overlap
   int64_t half;     // overlap / 2
   const Cx<R>* phasor;     // [n_tab][P][Q], carries 1/Q
+  const Cx<R>* phasor_rev; // the same rows permuted to cbessfm_ip_kernel's bin order
+                           // (ip_rev_index), or null where that kernel does not apply
   const int* ph_index;     // [n_steps + 1]
   const Cx<R>* mimo;       // [n_sets][P][Q/2+1], S_h with the 3/2 XPM weight folded
   const R* theta_scale;    // [n_sets][n_steps], carries 1/Q
@@ -1415,6 +1465,7 @@ __device__ __forceinline__ void bin_home(int g, int& i, int& m) {
   if (s >= N) s -= N;
   i = s / Q;
   m = (s % Q + Q / 2) % Q;
+  CB_CHECK(g >= 0 && g < N && i >= 0 && i < P && m >= 0 && m < Q);
 }
 
 template <typename R, int P, int Q>
@@ -1425,6 +1476,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
   constexpr int SF = padded_len(Q);      // stride between x and y in F
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  CB_POISON_SMEM(smem_raw);
   Cx<R>* F = reinterpret_cast<Cx<R>*>(smem_raw);
   Cx<R>* IS = F + 2 * SF;
   // TS (theta_hat, then theta) reuses IS: a remote CTA writes bin k of it
@@ -1499,6 +1551,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
     for (int t2 = tid; t2 < Q; t2 += NT) {
       int64_t idx = start + rank + (int64_t)P * t2;
       if (idx >= n) idx -= n;
+      CB_CHECK(idx >= 0 && idx < n);
       F[pad(t2)] = src[idx];
       F[SF + pad(t2)] = src[prm.in_pstride + idx];
     }
@@ -1773,6 +1826,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
     for (int t2 = tid; t2 < Q; t2 += NT) {
       const int64_t t = rank + (int64_t)P * t2;
       if (t >= prm.half && t < prm.half + span) {
+        CB_CHECK(obase + t >= 0 && (prm.out_origin != 0 || obase + t < n));
         dst[obase + t] = F[pad(t2)];
         dst[prm.out_pstride + obase + t] = F[SF + pad(t2)];
       }
@@ -1856,6 +1910,7 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
   constexpr int HS = kHalf | kWide | (TMON ? kTM : 0) | CB_GB_HALF;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  CB_POISON_SMEM(smem_raw);
   Cx<R>* const base = reinterpret_cast<Cx<R>*>(smem_raw);
   const int grp = (int)threadIdx.x / NT;  // subband of this thread's group
   const int tid = ltid<NT>();
@@ -1906,6 +1961,7 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
     for (int t = (int)threadIdx.x; t < P * Q; t += NTC) {
       int64_t idx = start + t;
       if (idx >= n) idx -= n;
+      CB_CHECK(idx >= 0 && idx < n);
       const int r = t % P, t2 = t / P;
       Cx<R>* Fr = base + r * SG;
       Fr[pad(t2)] = src[idx];
@@ -2224,6 +2280,7 @@ __global__ void __launch_bounds__(P * fat_group<Q>(), 1) cbessfm_fat_kernel(cons
     for (int64_t t = prm.half + threadIdx.x; t < prm.half + span; t += NTC) {
       const int r = (int)(t % P), t2 = (int)(t / P);
       const Cx<R>* Fr = base + r * SG;
+      CB_CHECK(obase + t >= 0 && (prm.out_origin != 0 || obase + t < n));
       dst[obase + t] = Fr[pad(t2)];
       dst[prm.out_pstride + obase + t] = Fr[SF + pad(t2)];
     }

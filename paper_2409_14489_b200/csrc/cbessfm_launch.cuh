@@ -6,6 +6,7 @@
 #include <cstdlib>
 
 #include "cbessfm_kernel.cuh"
+#include "cbessfm_ip.cuh"
 
 namespace cbessfm {
 
@@ -88,13 +89,14 @@ inline bool use_fat_kernel(int64_t nblocks, int pref) {
   return pref != 1;
 }
 
-template <typename R, int P, int Q>
-cudaError_t launch_one(const Params<R>& prm, int64_t nclusters, cudaStream_t stream,
-                       KernelInfo* info) {
-  if constexpr (fat_ok<R, P, Q>()) {
-    if (use_fat_kernel(nclusters, prm.kernel_pref)) return launch_fat<R, P, Q>(prm, nclusters, stream, info);
-  }
-  auto kern = cbessfm_block_kernel<R, P, Q>;
+// Launch of a P-CTA-cluster block kernel (one cluster per overlap-save
+// block): dynamic shared memory opt-in and sizing, non-portable clusters,
+// occupancy query for `info`. KERN is cbessfm_block_kernel<R, P, Q> or
+// cbessfm_ip_kernel<R, P> (same Params, threads, shared memory and TMEM).
+template <typename R, int P, int Q, void (*KERN)(const Params<R>)>
+cudaError_t launch_cluster(const char* kname, const Params<R>& prm, int64_t nclusters,
+                           cudaStream_t stream, KernelInfo* info) {
+  auto kern = KERN;
   constexpr int NT = threads_for<R, Q>();
   size_t smem = smem_bytes<R, Q>(P);
   // function attributes are per device; set them once per device
@@ -157,7 +159,7 @@ cudaError_t launch_one(const Params<R>& prm, int64_t nclusters, cudaStream_t str
     info->threads = NT;
     info->cluster = P;
     info->smem = smem;
-    snprintf(info->name, sizeof info->name, "cbessfm_block_kernel<%s,%d,%d>", real_name<R>(), P, Q);
+    snprintf(info->name, sizeof info->name, "%s<%s,%d,%d>", kname, real_name<R>(), P, Q);
     cfg.gridDim = dim3(P, 1, 1);
     int nc = 0;
     if (P > 1) {
@@ -185,6 +187,36 @@ cudaError_t launch_one(const Params<R>& prm, int64_t nclusters, cudaStream_t str
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+
+// In-place-pass kernel (cbessfm_ip.cuh, complex128, N' = 2048, P >= 2):
+// selected with CBESSFM_KERNEL=ip. Same results as the cluster kernel
+// (parity-tested) but not faster: configs[4] 379.6 vs 373.5 ms per step,
+// configs[1] x8 6.01 vs 5.99 ms ("In-place passes"),
+// so the Stockham cluster kernel stays the default.
+template <typename R, int P, int Q>
+constexpr bool ip_ok() {
+  return sizeof(R) == 8 && Q == kIpQ && P >= 2;
+}
+inline bool use_ip_kernel() {
+  const char* env = getenv("CBESSFM_KERNEL");
+  return env && env[0] == 'i';
+}
+
+template <typename R, int P, int Q>
+cudaError_t launch_one(const Params<R>& prm, int64_t nclusters, cudaStream_t stream,
+                       KernelInfo* info) {
+  if constexpr (fat_ok<R, P, Q>()) {
+    if (use_fat_kernel(nclusters, prm.kernel_pref)) return launch_fat<R, P, Q>(prm, nclusters, stream, info);
+  }
+  if constexpr (ip_ok<R, P, Q>()) {
+    if (use_ip_kernel() && prm.phasor_rev)
+      return launch_cluster<R, P, Q, cbessfm_ip_kernel<R, P>>("cbessfm_ip_kernel", prm, nclusters,
+                                                              stream, info);
+  }
+  return launch_cluster<R, P, Q, cbessfm_block_kernel<R, P, Q>>("cbessfm_block_kernel", prm,
+                                                                nclusters, stream, info);
 }
 
 template <typename R, int P>

@@ -28,6 +28,7 @@ __global__ void __launch_bounds__(Q / 8) nlpr_kernel(const Cx<R>* in, Cx<R>* out
   constexpr int NT = Q / 8;
   constexpr int H = Q / 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  CB_POISON_SMEM(smem_raw);
   Cx<R>* IS = reinterpret_cast<Cx<R>*>(smem_raw);   // packed intensity -> I_hat
   Cx<R>* TS = IS + padded_len(H + 1);                // theta_hat -> theta
   __shared__ int s_zero;

@@ -33,6 +33,7 @@ template <typename R, int LG>
 __global__ void __launch_bounds__(kThreads, 1024 / kThreads)
     col_kernel(const __grid_constant__ ssfm::Params<R> p, int inv_in, int fwd_out, int pre_div) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  CB_POISON_SMEM(smem_raw);
   col_phase<R, Split<LG>::N1>(p, reinterpret_cast<Cx<R>*>(smem_raw), inv_in != 0, kNone, (R)0,
                               nullptr, pre_div != 0, fwd_out != 0);
 }
@@ -41,6 +42,7 @@ template <typename R, int LG>
 __global__ void __launch_bounds__(kThreads, 1024 / kThreads)
     row_kernel(const __grid_constant__ ssfm::Params<R> p, int fwd, int inv) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  CB_POISON_SMEM(smem_raw);
   row_phase<R, Split<LG>::N2>(p, reinterpret_cast<Cx<R>*>(smem_raw), (const Cx<R>*)nullptr,
                               (const Cx<R>*)nullptr, fwd != 0, inv != 0);
 }

@@ -38,6 +38,7 @@ template <typename R, int LG>
 __global__ void __launch_bounds__(kThreads, 1024 / kThreads) ssfm_kernel(const __grid_constant__ Params<R> p) {
   constexpr int N1 = Split<LG>::N1, N2 = Split<LG>::N2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  CB_POISON_SMEM(smem_raw);
   Cx<R>* buf = reinterpret_cast<Cx<R>*>(smem_raw);
   cg::grid_group grid = cg::this_grid();
   {  // both per-length twiddle tables, staged once for every phase of the run

@@ -357,3 +357,40 @@ def test_fat_and_cluster_kernels_agree_at_scale(cuda, monkeypatch):
         monkeypatch.setenv("CBESSFM_KERNEL", kernel)
         outs[kernel] = pb.run_dbp_tensor(x, g.cfg, g.coeffs, rate).cpu().numpy()
     assert rel_rms(outs["fat"], outs["cluster"]) < 2e-6
+
+
+@pytest.mark.parametrize("n_sb", [3, 5, 9])
+def test_in_place_pass_kernel_matches_oracle(cuda, n_sb, monkeypatch):
+    # CBESSFM_KERNEL=ip: the complex128 kernel with in-place, digit-reversed
+    # field passes (csrc/cbessfm_ip.cuh; N' = 2048, P >= 2, P = 9 is a
+    # non-portable cluster). configs[1] golden case against the reference's
+    # output, and configs[2] sweep points at N' = 2048 against the oracle;
+    # the plan reports which kernel ran
+    import math
+    from conftest import GOLDEN, load_coeffs
+    monkeypatch.setenv("CBESSFM_KERNEL", "ip")
+    if n_sb == 5:
+        g = golden("cfg2_nsb5")
+        assert rel_rms(_run(g, "c128"), g.out) < TOL["c128"]
+        cfg, rate, c = g.cfg, g.wave.sample_rate, g.coeffs
+    else:
+        n_st = 3
+        d = np.load(GOLDEN / "sweep_coeffs.npz")
+        c = load_coeffs(d, f"s{n_st}_b{n_sb}_r5_")
+        ov = -(-math.ceil(2679 / n_st) // (2 * n_sb)) * (2 * n_sb)
+        link = pb.LinkConfig(num_spans=15, span_length_km=80.0, alpha_db_per_km=0.2,
+                             dispersion_d_ps_nm_km=17.0, gamma_w_km=1.3)
+        cfg = pb.DbpConfig(link=link, variant="CB_ESSFM", n_steps=n_st, n_subbands=n_sb,
+                           splitting_ratio=0.5, block_size=n_sb * 2048, overlap=ov,
+                           oversampling=2.0)
+        rate = 128e9
+        field = gaussian_wdm(1 << 17, rate, n_channels=1, spacing=0.0, dbm_per_channel=2.0,
+                             seed=3)
+        w = pb.DualPolWaveform(field[0], field[1], rate)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", RuntimeWarning)
+            out = pb.run_dbp(w, cfg, c, dtype="c128")
+        ref = orc.run_cb_blocks(field, cfg, rate, c)
+        assert rel_rms(np.vstack([out.x, out.y]), ref) < TOL["c128"]
+    plan = pb.get_plan(cfg, rate, c, "c128")
+    assert plan.info().kernel_name.startswith("cbessfm_ip_kernel")

@@ -6,7 +6,7 @@ for rep in 1 2; do
   for lib in "$@"; do
     for b in $batches; do
       if [ -n "$lib" ]; then export CBESSFM_LIB=$PWD/paper_2409_14489_b200/$lib; else unset CBESSFM_LIB; fi
-      ms=$(python bench.py --no-cpu-baseline --no-e2e --batch $b ${BENCH_ARGS} 2>/dev/null | tail -1 | python -c "import json,sys; print(round(json.load(sys.stdin)['ms_per_step'],4))")
+      ms=$(python bench.py --no-cpu-baseline --no-e2e --no-extras --batch $b ${BENCH_ARGS} 2>/dev/null | tail -1 | python -c "import json,sys; print(round(json.load(sys.stdin)['ms_per_step'],4))")
       echo "rep$rep ${lib:-default} batch=$b ms=$ms"
     done
   done

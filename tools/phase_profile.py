@@ -11,19 +11,26 @@ from paper_2409_14489_b200 import _native
 from paper_2409_14489_b200.synth import gaussian_wdm
 
 dtype = sys.argv[1] if len(sys.argv) > 1 else "c64"
+bench.WL = bench.WORKLOADS["cfg2"]          # one configs[1] waveform (143 blocks)
 cfg, coeffs = bench.workload_cfg()
 eng = pb.DbpEngine(cfg, coeffs, bench.RATE, dtype=dtype)
 ct = torch.complex64 if dtype == "c64" else torch.complex128
 x = torch.from_numpy(gaussian_wdm(bench.WL["n"], bench.RATE, seed=0)[None]).cuda().to(ct)
 out = torch.empty_like(x)
+# batch 16: CTA 0 runs in the first wave of a fully loaded GPU
+xb = x.expand(16, 2, x.shape[-1]).contiguous()
+outb = torch.empty_like(xb)
 lib = _native.load()
 names = {0: "start", 1: "loaded", 2: "outer fwd (FFT+exchange)", 3: "first IFFT",
          4: "steps", 5: "outer inv (exchange+IFFT)"}
 step = ["fft1 fwd", "untangle+push", "mimo", "wait theta", "twist", "fft1 inv",
         "fft2 fwd (to boundary)", "boundary pass", "ifft2 rest"]
-for label, rng in (("1 block", (0, 1)), ("143 blocks", None)):
+for label, rng in (("1 block", (0, 1)), ("143 blocks", None), ("16 x 143 blocks", "b")):
     for _ in range(3):
-        eng.run_device(x, out, block_range=rng)
+        if rng == "b":
+            eng.run_device(xb, outb)
+        else:
+            eng.run_device(x, out, block_range=rng)
     torch.cuda.synchronize()
     buf = (C.c_int64 * 256)()
     lib.cbessfm_debug_phase_times(eng.plan.handle, buf, 256)

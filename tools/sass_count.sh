@@ -17,7 +17,7 @@ txt = open(sys.argv[1]).read()
 real, P, Q = sys.argv[2:5]
 for m in re.finditer(r"Function : (\S+)\n(.*?)(?=\n\s+Function : |\Z)", txt, re.S):
     name, body = m.group(1), m.group(2)
-    if f"Li{P}ELi{Q}EE" not in name:
+    if f"Li{P}ELi{Q}EE" not in name and not ("ip_kernel" in name and f"Li{P}EE" in name):
         continue
     ops = collections.Counter()
     for line in body.splitlines():
@@ -29,5 +29,5 @@ for m in re.finditer(r"Function : (\S+)\n(.*?)(?=\n\s+Function : |\Z)", txt, re.
     print(name[:60], "total", tot, "fp", sum(fp.values()), dict(sorted(fp.items())))
     print("  top:", ops.most_common(14))
 PY
-grep -A2 "Li${P}ELi${Q}EE" $D/ptxas.log | grep -E "registers|spill" | head -6
+grep -A2 -E "Li${P}ELi${Q}EE|ip_kernelI.Li${P}EE" $D/ptxas.log | grep -E "registers|spill" | head -6
 rm -rf $D
