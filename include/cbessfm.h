@@ -112,6 +112,24 @@ typedef struct {
   int32_t chunks;          /* pipeline depth (<= 0: default 8)            */
 } cbessfm_host_io;
 
+/* The reference's own waveform layout (DualPolWaveform, signals.py:32-86):
+ * x and y as separate HOST arrays of complex128, in any (pageable) memory,
+ * results into separate HOST complex128 arrays. For a c64 plan the cast to
+ * complex64 and back happens in the host copies. The copies run on a pool
+ * of host threads owned by the plan and are pipelined with the chunked
+ * H2D / kernel / D2H of cbessfm_run_host (page-locked staging kept by the
+ * plan). Synchronous: returns once out_x / out_y hold the result, like
+ * run_dbp (dbp.py:437-478). ABI 3. */
+typedef struct {
+  const double* in_x;      /* [n] complex128 (interleaved re, im)         */
+  const double* in_y;
+  double* out_x;           /* [n] complex128                              */
+  double* out_y;
+  int64_t n;               /* samples per polarisation                    */
+  int32_t chunks;          /* pipeline depth (<= 0: default 8)            */
+  int32_t host_threads;    /* copy threads (<= 0: min(8, hardware))       */
+} cbessfm_dualpol_io;
+
 typedef struct {
   int32_t threads_per_cta;
   int32_t cluster_size;
@@ -146,6 +164,12 @@ cbessfm_status cbessfm_run(const cbessfm_plan* plan, const cbessfm_io* io, void*
 /* Enqueue H2D, the fused kernel and D2H on `stream` for host buffers;
  * returns once enqueued (synchronise `stream` before reading `out`). */
 cbessfm_status cbessfm_run_host(const cbessfm_plan* plan, const cbessfm_host_io* io, void* stream);
+
+/* One waveform in the reference's layout (cbessfm_dualpol_io), host in,
+ * host out, synchronous; `stream` orders the device work. The entry the
+ * drop-in run_dbp calls. */
+cbessfm_status cbessfm_run_dualpol(const cbessfm_plan* plan, const cbessfm_dualpol_io* io,
+                                   void* stream);
 
 /* The public nlpr_step helper (dbp.py:211-230) on the GPU: coupled-band
  * nonlinear phase rotation of P time-domain subband waveforms of n_prime

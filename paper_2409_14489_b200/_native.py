@@ -48,6 +48,12 @@ class HostIo(C.Structure):
                 ("batch", C.c_int64), ("chunks", C.c_int32)]
 
 
+class DualPolIo(C.Structure):
+    _fields_ = [("in_x", C.c_void_p), ("in_y", C.c_void_p), ("out_x", C.c_void_p),
+                ("out_y", C.c_void_p), ("n", C.c_int64), ("chunks", C.c_int32),
+                ("host_threads", C.c_int32)]
+
+
 class PlanInfo(C.Structure):
     _fields_ = [("threads_per_cta", C.c_int32), ("cluster_size", C.c_int32),
                 ("smem_per_cta", C.c_int64),
@@ -96,6 +102,7 @@ SIGNATURES = {
     "cbessfm_plan_info_get": (C.c_int, [C.c_void_p, C.POINTER(PlanInfo)]),
     "cbessfm_run": (C.c_int, [C.c_void_p, C.POINTER(Io), C.c_void_p]),
     "cbessfm_run_host": (C.c_int, [C.c_void_p, C.POINTER(HostIo), C.c_void_p]),
+    "cbessfm_run_dualpol": (C.c_int, [C.c_void_p, C.POINTER(DualPolIo), C.c_void_p]),
     "cbessfm_nlpr": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                C.POINTER(C.c_double), C.c_double, C.c_void_p]),
     "cbessfm_plan_update_sets": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_double),
@@ -222,6 +229,21 @@ class NativePlan:
         io = HostIo(in_ptr, out_ptr, n, batch, chunks)
         check(self._lib.cbessfm_run_host(self.handle, C.byref(io), C.c_void_p(stream)),
               "cbessfm_run_host")
+
+    def run_dualpol(self, x: np.ndarray, y: np.ndarray, out_x: np.ndarray, out_y: np.ndarray,
+                    *, chunks: int = 8, host_threads: int = 0, stream: int = 0) -> None:
+        """One waveform in the reference's layout: separate complex128 host
+        arrays in and out (cbessfm_run_dualpol); synchronous."""
+        for a in (x, y, out_x, out_y):
+            if a.dtype != np.complex128 or not a.flags.c_contiguous or a.ndim != 1:
+                raise ValueError("run_dualpol takes 1-D contiguous complex128 arrays")
+        n = x.size
+        if y.size != n or out_x.size != n or out_y.size != n:
+            raise ValueError("x, y and the outputs must have the same length")
+        io = DualPolIo(x.ctypes.data, y.ctypes.data, out_x.ctypes.data, out_y.ctypes.data, n,
+                       chunks, host_threads)
+        check(self._lib.cbessfm_run_dualpol(self.handle, C.byref(io), C.c_void_p(stream)),
+              "cbessfm_run_dualpol")
 
     def update_sets(self, mimo: np.ndarray, theta_scale: np.ndarray, stream: int = 0) -> None:
         """Overwrite the coefficient-set tables (cbessfm_plan_update_sets)."""

@@ -5,7 +5,13 @@
 #include <cstdio>
 #include <cstring>
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <functional>
 #include <mutex>
+#include <thread>
+#include <tuple>
 #include <new>
 #include <string>
 #include <vector>
@@ -109,6 +115,55 @@ struct cbessfm_plan {
   static constexpr int kHostSlots = 4;
   HostSlot host_slots[kHostSlots];
   int host_next = 0;
+  // cbessfm_run_dualpol: page-locked staging (in, out: [2][n] of the plan's
+  // dtype) and the host copy threads, created on first use
+  std::vector<cudaEvent_t> host_events;  // run_dualpol's D2H events, destroyed after sync
+  void* pin_in = nullptr;
+  void* pin_out = nullptr;
+  size_t pin_bytes = 0;
+  struct Pool* pool = nullptr;
+};
+
+// Host worker threads for cbessfm_run_dualpol's staging copies (FIFO task
+// queue; a call submits its chunk copies in pipeline order and waits on
+// per-task completion flags).
+struct Pool {
+  std::vector<std::thread> workers;
+  std::deque<std::function<void()>> q;
+  std::mutex mu;
+  std::condition_variable cv;
+  bool stop = false;
+  explicit Pool(int n) {
+    for (int i = 0; i < n; ++i)
+      workers.emplace_back([this] {
+        for (;;) {
+          std::function<void()> task;
+          {
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [this] { return stop || !q.empty(); });
+            if (stop && q.empty()) return;
+            task = std::move(q.front());
+            q.pop_front();
+          }
+          task();
+        }
+      });
+  }
+  void submit(std::function<void()> f) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      q.push_back(std::move(f));
+    }
+    cv.notify_one();
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      stop = true;
+    }
+    cv.notify_all();
+    for (auto& t : workers) t.join();
+  }
 };
 
 namespace {
@@ -268,6 +323,9 @@ void free_plan(cbessfm_plan* p) {
     if (sl.done) cudaEventDestroy(sl.done);
   }
   for (cudaStream_t st : p->host_streams) cudaStreamDestroy(st);
+  delete p->pool;
+  if (p->pin_in) cudaFreeHost(p->pin_in);
+  if (p->pin_out) cudaFreeHost(p->pin_out);
   cudaFree(p->phasor);
   cudaFree(p->phasor_rev);
   cudaFree(p->ph_index);
@@ -484,23 +542,25 @@ cbessfm_status cbessfm_run(const cbessfm_plan* p, const cbessfm_io* io, void* st
   return CBESSFM_OK;
 }
 
-cbessfm_status cbessfm_run_host(const cbessfm_plan* cp, const cbessfm_host_io* io, void* stream) {
-  g_err.clear();
-  if (!cp || !io) return fail(CBESSFM_ERR_INVALID, "null plan or io");
-  if (!io->in || !io->out) return fail(CBESSFM_ERR_INVALID, "null input or output buffer");
-  if (io->n < cp->N) return fail(CBESSFM_ERR_INVALID, "block_size exceeds the sequence length");
-  if (io->batch <= 0) return fail(CBESSFM_ERR_INVALID, "batch must be positive");
-  cbessfm_plan* p = const_cast<cbessfm_plan*>(cp);  // only the stream pool is touched
-  const int64_t n = io->n, batch = io->batch;
+}  // extern "C"
+
+namespace {
+
+// The pipelined host-buffer schedule shared by cbessfm_run_host and
+// cbessfm_run_dualpol: `in` / `out` page-locked [batch][2][n] of the plan's
+// dtype. before_h2d(a, b) runs on the calling thread before samples [a, b)
+// of every row are copied in (run_dualpol waits there for its staging
+// copies); after_d2h(o0, o1, ev) after the D2H of kept samples [o0, o1) has
+// been enqueued, ev completing with it. Caller holds p->host_mu.
+cbessfm_status host_pipeline(cbessfm_plan* p, const void* in, void* out, int64_t n,
+                             int64_t batch, int chunks_req, cudaStream_t st,
+                             const std::function<void(int64_t, int64_t)>& before_h2d,
+                             const std::function<void(int64_t, int64_t, cudaEvent_t)>& after_d2h) {
   const int64_t keep = p->N - p->overlap, half = p->overlap / 2;
   const int64_t nb = cbessfm_num_blocks(n, p->N, p->overlap);
-  const int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(io->chunks > 0 ? io->chunks : 8, nb));
+  const int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(chunks_req > 0 ? chunks_req : 8, nb));
   const size_t esz = p->dtype == CBESSFM_C64 ? 8 : 16;
   const size_t rowb = (size_t)n * esz, rows = (size_t)batch * 2;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  std::lock_guard<std::mutex> lock(p->host_mu);
-  DeviceGuard dg(p->device);
-  if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
   cudaError_t e;
   while ((int)p->host_streams.size() < 2 + chunks) {
     cudaStream_t s2;
@@ -547,16 +607,20 @@ cbessfm_status cbessfm_run_host(const cbessfm_plan* cp, const cbessfm_host_io* i
   for (int i = 0; i < 2 + chunks; ++i) cudaStreamWaitEvent(p->host_streams[i], ev0, 0);
   // column ranges [a, b) of every (waveform, polarisation) row in one call
   auto h2d = [&](int64_t a, int64_t b) {
-    return cudaMemcpy2DAsync((char*)din + a * esz, rowb, (const char*)io->in + a * esz, rowb,
+    if (before_h2d) before_h2d(a, b);
+    return cudaMemcpy2DAsync((char*)din + a * esz, rowb, (const char*)in + a * esz, rowb,
                              (size_t)(b - a) * esz, rows, cudaMemcpyHostToDevice, s_in);
   };
   auto d2h = [&](int64_t a, int64_t b) {
-    return cudaMemcpy2DAsync((char*)io->out + a * esz, rowb, (const char*)dout + a * esz, rowb,
-                             (size_t)(b - a) * esz, rows, cudaMemcpyDeviceToHost, s_out);
+    const cudaError_t r = cudaMemcpy2DAsync((char*)out + a * esz, rowb, (const char*)dout + a * esz,
+                                            rowb, (size_t)(b - a) * esz, rows,
+                                            cudaMemcpyDeviceToHost, s_out);
+    if (r == cudaSuccess && after_d2h) after_d2h(a, b, event(s_out));
+    return r;
   };
-  // same schedule as DbpEngine.run_host: wrap piece first, then `chunks`
-  // sample ranges; blocks whose windows end inside the copied prefix run
-  // as soon as it lands, the last chunk takes the remaining blocks
+  // wrap piece first, then `chunks` sample ranges; blocks whose windows end
+  // inside the copied prefix run as soon as it lands, the last chunk takes
+  // the remaining blocks
   auto enqueue = [&]() -> cbessfm_status {
     const int64_t wrap = half > 0 ? n - half : n;
     if (half > 0 && (e = h2d(wrap, n)) != cudaSuccess) return cuda_fail(e, "h2d");
@@ -591,9 +655,158 @@ cbessfm_status cbessfm_run_host(const cbessfm_plan* cp, const cbessfm_host_io* i
   // error); the staging slot is reusable once that point is reached
   for (int i = 0; i < 2 + chunks; ++i) cudaStreamWaitEvent(st, event(p->host_streams[i]), 0);
   cudaEventRecord(slot.done, st);  // the slot is free once this call completes
-  for (cudaEvent_t ev : evs) cudaEventDestroy(ev);  // released once complete
+  if (!after_d2h)
+    for (cudaEvent_t ev : evs) cudaEventDestroy(ev);  // released once complete
+  else
+    for (cudaEvent_t ev : evs) p->host_events.push_back(ev);  // the caller syncs first
   if (status != CBESSFM_OK) return status;
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "cbessfm_run_host");
+  return CBESSFM_OK;
+}
+
+// c128 -> plan dtype copy of samples [a, b) of one polarisation row
+void stage_in(const cbessfm_plan* p, const double* src, void* row, int64_t a, int64_t b) {
+  if (p->dtype == CBESSFM_C128) {
+    memcpy((double*)row + 2 * a, src + 2 * a, (size_t)(b - a) * 16);
+  } else {
+    float* d = (float*)row;
+    for (int64_t i = 2 * a; i < 2 * b; ++i) d[i] = (float)src[i];
+  }
+}
+void stage_out(const cbessfm_plan* p, const void* row, double* dst, int64_t a, int64_t b) {
+  if (p->dtype == CBESSFM_C128) {
+    memcpy(dst + 2 * a, (const double*)row + 2 * a, (size_t)(b - a) * 16);
+  } else {
+    const float* s = (const float*)row;
+    for (int64_t i = 2 * a; i < 2 * b; ++i) dst[i] = (double)s[i];
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+cbessfm_status cbessfm_run_host(const cbessfm_plan* cp, const cbessfm_host_io* io, void* stream) {
+  g_err.clear();
+  if (!cp || !io) return fail(CBESSFM_ERR_INVALID, "null plan or io");
+  if (!io->in || !io->out) return fail(CBESSFM_ERR_INVALID, "null input or output buffer");
+  if (io->n < cp->N) return fail(CBESSFM_ERR_INVALID, "block_size exceeds the sequence length");
+  if (io->batch <= 0) return fail(CBESSFM_ERR_INVALID, "batch must be positive");
+  cbessfm_plan* p = const_cast<cbessfm_plan*>(cp);  // only the stream pool is touched
+  std::lock_guard<std::mutex> lock(p->host_mu);
+  DeviceGuard dg(p->device);
+  if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+  return host_pipeline(p, io->in, io->out, io->n, io->batch, io->chunks,
+                       reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr);
+}
+
+cbessfm_status cbessfm_run_dualpol(const cbessfm_plan* cp, const cbessfm_dualpol_io* io,
+                                   void* stream) {
+  g_err.clear();
+  if (!cp || !io) return fail(CBESSFM_ERR_INVALID, "null plan or io");
+  if (!io->in_x || !io->in_y || !io->out_x || !io->out_y)
+    return fail(CBESSFM_ERR_INVALID, "null input or output buffer");
+  if (io->n < cp->N) return fail(CBESSFM_ERR_INVALID, "block_size exceeds the sequence length");
+  cbessfm_plan* p = const_cast<cbessfm_plan*>(cp);
+  std::lock_guard<std::mutex> lock(p->host_mu);
+  DeviceGuard dg(p->device);
+  if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+  const int64_t n = io->n;
+  const size_t esz = p->dtype == CBESSFM_C64 ? 8 : 16;
+  const size_t bytes = 2 * (size_t)n * esz;
+  cudaError_t e;
+  if (p->pin_bytes < bytes) {
+    if (p->pin_in) cudaFreeHost(p->pin_in);
+    if (p->pin_out) cudaFreeHost(p->pin_out);
+    p->pin_in = p->pin_out = nullptr;
+    p->pin_bytes = 0;
+    if ((e = cudaHostAlloc(&p->pin_in, bytes, cudaHostAllocPortable)) != cudaSuccess)
+      return cuda_fail(e, "pinned staging");
+    if ((e = cudaHostAlloc(&p->pin_out, bytes, cudaHostAllocPortable)) != cudaSuccess)
+      return cuda_fail(e, "pinned staging");
+    p->pin_bytes = bytes;
+  }
+  if (!p->pool) {
+    const int hw = (int)std::thread::hardware_concurrency();
+    int nt = io->host_threads > 0 ? io->host_threads : std::min(8, std::max(1, hw));
+    p->pool = new Pool(nt);
+  }
+  char* rin = (char*)p->pin_in;
+  char* rout = (char*)p->pin_out;
+  const size_t rowb = (size_t)n * esz;
+  // staging copies in pieces, the wrap piece (the tail block 0 reads) first,
+  // then ascending; before each H2D the pipeline waits for its pieces
+  const int64_t half = p->overlap / 2;
+  const int64_t piece = std::max<int64_t>(4096, (n + 63) / 64);
+  std::vector<std::pair<int64_t, int64_t>> ranges;
+  const int64_t wrap = half > 0 ? n - half : n;
+  if (half > 0) ranges.push_back({wrap, n});
+  for (int64_t a = 0; a < wrap; a += piece) ranges.push_back({a, std::min(wrap, a + piece)});
+  std::vector<std::atomic<int>> done(ranges.size());
+  for (auto& d : done) d.store(0);
+  std::mutex wmu;
+  std::condition_variable wcv;
+  for (size_t t = 0; t < ranges.size(); ++t) {
+    p->pool->submit([&, t] {
+      stage_in(p, io->in_x, rin, ranges[t].first, ranges[t].second);
+      stage_in(p, io->in_y, rin + rowb, ranges[t].first, ranges[t].second);
+      {
+        std::lock_guard<std::mutex> lk(wmu);
+        done[t].store(1);
+      }
+      wcv.notify_all();
+    });
+  }
+  auto before_h2d = [&](int64_t a, int64_t b) {
+    std::unique_lock<std::mutex> lk(wmu);
+    wcv.wait(lk, [&] {
+      for (size_t t = 0; t < ranges.size(); ++t)
+        if (ranges[t].first < b && ranges[t].second > a && !done[t].load()) return false;
+      return true;
+    });
+  };
+  std::vector<std::tuple<int64_t, int64_t, cudaEvent_t>> outs;
+  auto after_d2h = [&](int64_t a, int64_t b, cudaEvent_t ev) { outs.emplace_back(a, b, ev); };
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const cbessfm_status status =
+      host_pipeline(p, rin, rout, n, 1, io->chunks, st, before_h2d, after_d2h);
+  // drain the copy-in tasks even on error (they reference this frame)
+  before_h2d(0, n);
+  if (status != CBESSFM_OK) {
+    cudaStreamSynchronize(st);
+    for (cudaEvent_t ev : p->host_events) cudaEventDestroy(ev);
+    p->host_events.clear();
+    return status;
+  }
+  // copy the kept samples out as their D2H pieces complete
+  e = cudaSuccess;
+  std::atomic<int> pending{0};
+  for (auto& o : outs) {
+    const int64_t a = std::get<0>(o), b = std::get<1>(o);
+    if ((e = cudaEventSynchronize(std::get<2>(o))) != cudaSuccess) break;
+    for (int64_t x0 = a; x0 < b; x0 += piece) {
+      const int64_t x1 = std::min(b, x0 + piece);
+      pending.fetch_add(1);
+      p->pool->submit([&, x0, x1] {
+        stage_out(p, rout, io->out_x, x0, x1);
+        stage_out(p, rout + rowb, io->out_y, x0, x1);
+        {
+          std::lock_guard<std::mutex> lk(wmu);
+          pending.fetch_sub(1);
+        }
+        wcv.notify_all();
+      });
+    }
+  }
+  {
+    std::unique_lock<std::mutex> lk(wmu);
+    wcv.wait(lk, [&] { return pending.load() == 0; });
+  }
+  const cudaError_t e2 = cudaStreamSynchronize(st);
+  for (cudaEvent_t ev : p->host_events) cudaEventDestroy(ev);
+  p->host_events.clear();
+  if (e != cudaSuccess) return cuda_fail(e, "cbessfm_run_dualpol d2h");
+  if (e2 != cudaSuccess) return cuda_fail(e2, "cbessfm_run_dualpol");
   return CBESSFM_OK;
 }
 
