@@ -92,6 +92,8 @@ def build(jobs: int | None = None, verbose: bool = False, profile: bool = False,
                   BUILD / "coeff.log"))
     tasks.append((CSRC / "cbessfm_rx.cu", BUILD / "rx.o", [], HEADERS,
                   BUILD / "rx.log"))
+    tasks.append((CSRC / "cbessfm_wide.cu", BUILD / "wide.o", [], HEADERS,
+                  BUILD / "wide.log"))
     with ThreadPoolExecutor(jobs) as ex:
         results = list(ex.map(_compile, tasks))
     errors = [e for _, e in results if e]

@@ -19,6 +19,13 @@
 #include "../../include/cbessfm.h"
 #include "cbessfm_launch.cuh"
 
+namespace cbessfm {
+cudaError_t wide_run_float(const Params<float>& prm, int P, int Q, int64_t nclusters,
+                           cudaStream_t st);
+cudaError_t wide_run_double(const Params<double>& prm, int P, int Q, int64_t nclusters,
+                            cudaStream_t st);
+}  // namespace cbessfm
+
 namespace {
 
 thread_local std::string g_err;
@@ -36,7 +43,11 @@ bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 
 constexpr int kMaxP = 9;
 
+// largest N' of the fused one-block kernels; wider subbands (up to
+// kMaxWideQ) run the wide path (csrc/cbessfm_wide.cu)
 int max_q(int dtype) { return dtype == CBESSFM_C64 ? 8192 : 4096; }
+constexpr int kMaxWideQ = 65536;
+bool is_wide(const cbessfm_plan* p);
 
 // exp(-2 pi i m / n), m in [0, n), evaluated in long double and rounded once.
 std::vector<double> twiddles(int64_t n) {
@@ -303,7 +314,9 @@ cbessfm_status upload_all(cbessfm_plan* p, const cbessfm_desc* d) {
     return cuda_fail(e, "upload twiddles");
   if ((e = upload_complex<R>(tn.data(), PQ, &p->twN, true)) != cudaSuccess)
     return cuda_fail(e, "upload outer twiddles");
-  const std::vector<double> tp = pass_tables(p->Q, tq, (int)sizeof(R));
+  // per-pass rows of the fused kernels (the wide path reads W_N only)
+  const std::vector<double> tp =
+      p->Q <= max_q(p->dtype) ? pass_tables(p->Q, tq, (int)sizeof(R)) : std::vector<double>(2, 0.0);
   if ((e = upload_complex<R>(tp.data(), tp.size() / 2, &p->twp, true)) != cudaSuccess)
     return cuda_fail(e, "upload pass twiddles");
 #ifdef CB_PHASE_PROFILE
@@ -313,6 +326,8 @@ cbessfm_status upload_all(cbessfm_plan* p, const cbessfm_desc* d) {
 #endif
   return CBESSFM_OK;
 }
+
+bool is_wide(const cbessfm_plan* p) { return p->Q > max_q(p->dtype); }
 
 void free_plan(cbessfm_plan* p) {
   if (!p) return;
@@ -433,7 +448,7 @@ int32_t cbessfm_supported(int32_t dtype, int32_t n_subbands, int32_t block_size)
   if (dtype != CBESSFM_C64 && dtype != CBESSFM_C128) return 0;
   if (n_subbands < 1 || n_subbands > kMaxP || block_size % n_subbands) return 0;
   const int q = block_size / n_subbands;
-  return is_pow2(q) && q >= 256 && q <= max_q(dtype);
+  return is_pow2(q) && q >= 256 && q <= kMaxWideQ;
 }
 
 cbessfm_status cbessfm_plan_create(const cbessfm_desc* d, cbessfm_plan** out) {
@@ -463,7 +478,7 @@ cbessfm_status cbessfm_plan_create(const cbessfm_desc* d, cbessfm_plan** out) {
     snprintf(buf, sizeof buf,
              "unsupported shape for the sm_100a kernel: n_subbands=%d (1..%d), "
              "N'=block_size/n_subbands=%d (power of two in [256, %d])",
-             d->n_subbands, kMaxP, d->block_size / d->n_subbands, max_q(d->dtype));
+             d->n_subbands, kMaxP, d->block_size / d->n_subbands, kMaxWideQ);
     return fail(CBESSFM_ERR_UNSUPPORTED, buf);
   }
   cbessfm_plan* p = new (std::nothrow) cbessfm_plan;
@@ -499,6 +514,16 @@ cbessfm_status cbessfm_plan_info_get(const cbessfm_plan* p, cbessfm_plan_info* i
   if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
   cbessfm::KernelInfo ki{};
   cudaError_t e;
+  if (is_wide(p)) {
+    info->threads_per_cta = 256;
+    info->cluster_size = 1;
+    info->smem_per_cta = 0;
+    info->max_active_clusters = 0;
+    info->q = p->Q;
+    snprintf(info->kernel, sizeof info->kernel, "%s",
+             "cbessfm_wide (Stockham passes, device workspace)");
+    return CBESSFM_OK;
+  }
   if (p->dtype == CBESSFM_C64) {
     cbessfm::Params<float> prm{};
     e = dispatch<float>(p->P, prm, p->Q, 0, nullptr, &ki);
@@ -534,6 +559,14 @@ cbessfm_status cbessfm_run(const cbessfm_plan* p, const cbessfm_io* io, void* st
   if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e;
+  if (is_wide(p)) {
+    if (p->dtype == CBESSFM_C64)
+      e = cbessfm::wide_run_float(make_params<float>(p, io), p->P, p->Q, nclusters, st);
+    else
+      e = cbessfm::wide_run_double(make_params<double>(p, io), p->P, p->Q, nclusters, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cbessfm wide-path launch");
+    return CBESSFM_OK;
+  }
   if (p->dtype == CBESSFM_C64)
     e = dispatch<float>(p->P, make_params<float>(p, io), p->Q, nclusters, st, nullptr);
   else

@@ -1,0 +1,464 @@
+// Wide-subband path of the CB-ESSFM block pipeline: N' = N/N_sb larger than
+// the fused kernels hold in shared memory (c128 N' >= 8192, c64 N' >= 16384;
+// the reference's own full-scale configuration, configs/fullscale.yaml:14-21,
+// runs N = 16384 with N_sb in {1, 2, 4, 8}).
+//
+// Same algorithm and operation order as the fused block kernel
+// (cbessfm_kernel.cuh), staged through a device workspace instead of one
+// CTA's shared memory: every transform is a batched Stockham FFT whose
+// passes (radix 16, leftover radix first) each read and write the chunk's
+// rows once (L2-resident for a chunk of blocks), with the elementwise steps
+// fused into the first / last pass where they touch natural-order samples:
+//
+//   window load ............. dbp.py:473-475          wide_window
+//   outer FFT_N + demux ..... dbp.py:387-389          passes + wide_demux (1/P, first phasor)
+//   per step (dbp.py:394-398):
+//     IFFT_Q, |x|^2+|y|^2 ... dbp.py:396, :193        passes, last one writes I
+//     rfft(I) (half-length FFT of the packed reals)   passes over I viewed as complex
+//     untangle, MIMO, twist . dbp.py:194-195          wide_mimo (fat-kernel formulas)
+//     irfft ................. dbp.py:196               passes -> theta (packed reals)
+//     rotation, FFT_Q ....... dbp.py:208, :398        passes, first one rotates
+//     next phasor ........... dbp.py:395 / :399       last pass multiplies
+//   merge + IFFT_N .......... dbp.py:400-401          wide_merge + passes
+//   keep .................... dbp.py:476-477          wide_store
+//
+// Twiddles of every length L in {N, Q, Q/2} come from the plan's W_N table
+// (L divides N = P * Q) with stride N / L.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "cbessfm_kernel.cuh"
+
+namespace cbessfm {
+namespace wide {
+
+constexpr int kThreads = 256;
+
+enum Hook { kNoHook = 0, kRotate = 1, kPhasor = 2, kIntensity = 3 };
+
+template <typename R>
+struct PassArgs {
+  const Cx<R>* src;
+  Cx<R>* dst;
+  int64_t rows;      // rows of length L (kIntensity: processed in (x, y) pairs)
+  int L, NS;
+  const Cx<R>* twN;  // W_N^m, m < N
+  int tw_stride;     // N / L
+  // hooks
+  const R* theta;    // kRotate: packed reals, row q = row / 2, length L
+  const R* tscale;   // kRotate: per-row-pair scale (theta_scale[set][st])
+  const Cx<R>* phasor;  // kPhasor: [n_tab][P][L] tables, table ph_index[step + 1]
+  const int* ph_index;
+  int P;
+  R* inten;          // kIntensity: row pair q -> I[q][L]
+  int64_t rows_per_wave;  // row pairs (blocks x P) per waveform (set lookup)
+  int64_t q0;             // global index of the chunk's first row pair
+  int n_sets, n_steps, step;
+};
+
+// One Stockham pass of radix RAD and sub-transform size NS on rows of
+// length L: inputs j + r L/RAD twiddled by W_(RAD NS)^(r k), k = j mod NS,
+// outputs (j / NS) NS RAD + k + r NS (natural order after the last pass).
+template <typename R, int RAD, bool INV, int HOOK>
+__global__ void __launch_bounds__(kThreads) wide_pass(const PassArgs<R> a) {
+  const int LR = a.L / RAD;
+  const int64_t units = (HOOK == kIntensity ? a.rows / 2 : a.rows) * LR;
+  for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < units;
+       u += (int64_t)gridDim.x * kThreads) {
+    const int64_t row0 = u / LR;
+    const int j = (int)(u % LR), k = j % a.NS;
+    const int base = (j / a.NS) * a.NS * RAD + k;
+    constexpr int NR = HOOK == kIntensity ? 2 : 1;
+    Cx<R> v[NR][RAD];
+#pragma unroll
+    for (int h = 0; h < NR; ++h) {
+      const int64_t row = HOOK == kIntensity ? 2 * row0 + h : row0;
+      const Cx<R>* s = a.src + row * a.L;
+#pragma unroll
+      for (int r = 0; r < RAD; ++r) v[h][r] = s[j + r * LR];
+      if constexpr (HOOK == kRotate) {
+        // exp(-i theta) on the natural-order inputs (dbp.py:208), the same
+        // sincos and product as the fused kernel's RotationHook
+        const R* th = a.theta + (row >> 1) * (int64_t)a.L;
+        const int64_t q = row >> 1;
+        const int set = a.n_sets > 1 ? (int)(((a.q0 + q) / a.rows_per_wave) % a.n_sets) : 0;
+        const R sc = a.tscale[(int64_t)set * a.n_steps + a.step];
+#pragma unroll
+        for (int r = 0; r < RAD; ++r) {
+          R sn, cs;
+          sincos_acc<R>(th[j + r * LR] * sc, &sn, &cs);
+          v[h][r] = cmul(v[h][r], mk(cs, -sn));
+        }
+      }
+      if (a.NS > 1) {
+        const int e0 = k * (a.L / (a.NS * RAD));
+#pragma unroll
+        for (int r = 1; r < RAD; ++r) {
+          const Cx<R> w = ldg(a.twN + (int64_t)(r * e0) * a.tw_stride);
+          v[h][r] = INV ? cmulc(v[h][r], w) : cmul(v[h][r], w);
+        }
+      }
+      dft_reg<R, RAD, INV>(v[h]);
+      if constexpr (HOOK == kPhasor) {
+        // next dispersion phasor on the natural-order bins (dbp.py:395, :399)
+        const int i = (int)((row >> 1) % a.P);
+        const Cx<R>* ph =
+            a.phasor + ((int64_t)a.ph_index[a.step + 1] * a.P + i) * (int64_t)a.L;
+#pragma unroll
+        for (int r = 0; r < RAD; ++r)
+          v[h][bitrev<RAD>(r)] = cmul(v[h][bitrev<RAD>(r)], ldg(ph + base + r * a.NS));
+      }
+      Cx<R>* d = a.dst + row * a.L;
+#pragma unroll
+      for (int r = 0; r < RAD; ++r) d[base + r * a.NS] = v[h][bitrev<RAD>(r)];
+    }
+    if constexpr (HOOK == kIntensity) {
+      // I = |x|^2 + |y|^2 of the time samples (dbp.py:193)
+      R* I = a.inten + row0 * (int64_t)a.L;
+#pragma unroll
+      for (int r = 0; r < RAD; ++r) {
+        const Cx<R> x = v[0][bitrev<RAD>(r)], y = v[1][bitrev<RAD>(r)];
+        const R ox = x.x * x.x + x.y * x.y;
+        const R oy = y.x * y.x + y.y * y.y;
+        I[base + r * a.NS] = ox + oy;
+      }
+    }
+  }
+}
+
+template <typename R>
+struct StepArgs {
+  Params<R> prm;
+  int P, Q, N;
+  int64_t c0, nc;  // chunk: flattened (waveform, block) indices [c0, c0 + nc)
+};
+
+// Circular window of block b, both polarisations, natural order
+// (dbp.py:473-475): A[c][pol][t] = u[(b keep - half + t) mod n].
+template <typename R>
+__global__ void __launch_bounds__(kThreads) wide_window(const StepArgs<R> s, Cx<R>* A) {
+  const Params<R>& p = s.prm;
+  const int64_t total = s.nc * 2 * s.N;
+  for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < total;
+       u += (int64_t)gridDim.x * kThreads) {
+    const int64_t c = u / (2 * s.N);
+    const int pol = (int)((u / s.N) & 1);
+    const int t = (int)(u % s.N);
+    const int64_t cid = s.c0 + c, wv = cid / p.nb, b = p.b0 + cid % p.nb;
+    int64_t start = (b * p.keep - p.half) % p.n;
+    if (start < 0) start += p.n;
+    start -= p.in_origin;
+    if (start < 0) start += p.n;
+    int64_t idx = start + t;
+    if (idx >= p.n) idx -= p.n;
+    A[u] = p.in[wv * p.in_bstride + pol * p.in_pstride + idx];
+  }
+}
+
+// Subband demux of the FFT_N bins (fftshift / reshape / ifftshift of
+// dbp.py:387-389), x 1/P x first phasor, into rows [c][i][pol][Q].
+template <typename R>
+__global__ void __launch_bounds__(kThreads) wide_demux(const StepArgs<R> s, const Cx<R>* F,
+                                                       Cx<R>* S) {
+  const Params<R>& p = s.prm;
+  const int64_t total = s.nc * 2 * s.N;
+  const R invP = (R)1 / (R)s.P;
+  const Cx<R>* ph0 = p.phasor + (int64_t)p.ph_index[0] * s.N;
+  for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < total;
+       u += (int64_t)gridDim.x * kThreads) {
+    const int m = (int)(u % s.Q);
+    const int pol = (int)((u / s.Q) & 1);
+    const int i = (int)((u / (2 * s.Q)) % s.P);
+    const int64_t c = u / (2 * (int64_t)s.N);
+    int g = i * s.Q + (m + s.Q / 2) % s.Q + s.N / 2;
+    if (g >= s.N) g -= s.N;
+    const Cx<R> v = F[(c * 2 + pol) * s.N + g];
+    S[u] = s.P > 1 ? cmul(scale(v, invP), ldg(ph0 + (int64_t)i * s.Q + m))
+                   : cmul(v, ldg(ph0 + m));
+  }
+}
+
+// Merge (dbp.py:399-401): subband rows back to FFT_N bin order (the merge's
+// x N_sb and the outer IFFT's 1/N are carried by the final phasor's 1/Q).
+template <typename R>
+__global__ void __launch_bounds__(kThreads) wide_merge(const StepArgs<R> s, const Cx<R>* S,
+                                                       Cx<R>* F) {
+  const int64_t total = s.nc * 2 * s.N;
+  for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < total;
+       u += (int64_t)gridDim.x * kThreads) {
+    const int g = (int)(u % s.N);
+    const int pol = (int)((u / s.N) & 1);
+    const int64_t c = u / (2 * (int64_t)s.N);
+    int i, m;
+    int sh = g + s.N / 2;
+    if (sh >= s.N) sh -= s.N;
+    i = sh / s.Q;
+    m = (sh % s.Q + s.Q / 2) % s.Q;
+    F[u] = S[((c * s.P + i) * 2 + pol) * s.Q + m];
+  }
+}
+
+// Keep proc[half : half + span] of every block (dbp.py:476-477).
+template <typename R>
+__global__ void __launch_bounds__(kThreads) wide_store(const StepArgs<R> s, const Cx<R>* F) {
+  const Params<R>& p = s.prm;
+  const int64_t total = s.nc * 2 * p.keep;
+  for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < total;
+       u += (int64_t)gridDim.x * kThreads) {
+    const int64_t c = u / (2 * p.keep);
+    const int pol = (int)((u / p.keep) & 1);
+    const int64_t t = p.half + u % p.keep;
+    const int64_t cid = s.c0 + c, wv = cid / p.nb, b = p.b0 + cid % p.nb;
+    const int64_t span = min(p.keep, p.n - b * p.keep);
+    if (t >= p.half + span) continue;
+    const int64_t obase = b * p.keep - p.half - p.out_origin;
+    p.out[wv * p.out_bstride + pol * p.out_pstride + obase + t] = F[(c * 2 + pol) * s.N + t];
+  }
+}
+
+// r2c untangle of every subband's half-length spectrum, MIMO (dbp.py:195)
+// and c2r pre-twist for one bin pair (k, H - k) of one block: the
+// one-block-per-CTA kernel's fused phase, same operations in the same order.
+template <typename R, int P>
+__global__ void __launch_bounds__(kThreads) wide_mimo(const StepArgs<R> s, const Cx<R>* Z,
+                                                      Cx<R>* T) {
+  const Params<R>& p = s.prm;
+  const int H = s.Q / 2;
+  const int64_t pairs = (int64_t)(H / 2 + 1);
+  const int64_t total = s.nc * pairs;
+  for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < total;
+       u += (int64_t)gridDim.x * kThreads) {
+    const int64_t c = u / pairs;
+    const int kp = (int)(u % pairs), kq = H - kp;
+    const int64_t wv = (s.c0 + c) / p.nb;
+    const int64_t cset = p.n_sets > 1 ? wv % p.n_sets : 0;
+    const Cx<R>* mimo = p.mimo + cset * (int64_t)P * (H + 1);
+    const Cx<R> wk = ldg(p.twN + (int64_t)kp * s.P);  // W_Q^kp
+    Cx<R> ia[P], ib[P];
+#pragma unroll
+    for (int l = 0; l < P; ++l) {
+      const Cx<R>* Il = Z + (c * P + l) * (int64_t)H;
+      if (kp == 0) {
+        const Cx<R> z = Il[0];
+        ia[l] = mk(z.x + z.y, (R)0);
+        ib[l] = mk(z.x - z.y, (R)0);
+      } else {
+        const Cx<R> a = Il[kp];
+        const Cx<R> bq = conj(Il[kq]);
+        const Cx<R> e = scale(a + bq, (R)0.5);
+        const Cx<R> dd = a - bq;
+        const Cx<R> o = mk(dd.y * (R)0.5, -dd.x * (R)0.5);
+        const Cx<R> wo = cmul(o, wk);
+        ia[l] = e + wo;
+        ib[l] = kp == kq ? ia[l] : conj(e - wo);
+      }
+    }
+    Cx<R> ta[P], tb[P];
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int k = half ? kq : kp;
+      const Cx<R>* iv = half ? ib : ia;
+      Cx<R> sv[P];
+#pragma unroll
+      for (int l = 0; l < P; ++l) sv[l] = ldg(mimo + (int64_t)l * (H + 1) + k);
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        Cx<R> acc = mk((R)0, (R)0);
+#pragma unroll
+        for (int l = 0; l < P; ++l)
+          acc = acc + (l >= i ? cmul(sv[l - i], iv[l]) : cmul(conj(sv[i - l]), iv[l]));
+        (half ? tb : ta)[i] = acc;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      Cx<R>* Ti = T + (c * P + i) * (int64_t)H;
+      if (kp == 0) {
+        Ti[0] = mk(ta[i].x + tb[i].x, ta[i].x - tb[i].x);
+      } else {
+        const Cx<R> a = ta[i];
+        const Cx<R> cc = conj(tb[i]);
+        const Cx<R> s2 = a + cc;
+        const Cx<R> dd = cmulc(a - cc, wk);
+        Ti[kp] = mk(s2.x - dd.y, s2.y + dd.x);
+        if (kp != kq) {
+          const Cx<R> a2 = conj(cc);
+          const Cx<R> c2 = conj(a);
+          const Cx<R> s3 = a2 + c2;
+          const Cx<R> w2 = mk(-wk.x, wk.y);
+          const Cx<R> d2 = cmulc(a2 - c2, w2);
+          Ti[kq] = mk(s3.x - d2.y, s3.y + d2.x);
+        }
+      }
+    }
+  }
+}
+
+inline int grid_for(int64_t units) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((units + kThreads - 1) / kThreads, 148 * 16));
+}
+
+// Batched FFT of `rows` rows of length L (src -> result in *cur, ping-pong
+// with *alt); the first pass may rotate, the last may apply a phasor or
+// write the intensity.
+template <typename R, bool INV>
+cudaError_t fft_rows(PassArgs<R> a, Cx<R>** cur, Cx<R>** alt, int first_hook, int last_hook,
+                     cudaStream_t st) {
+  int lg = 0;
+  while ((1 << lg) < a.L) ++lg;
+  const int lead = lg % 4;  // leftover radix first, then radix 16
+  int ns = 1;
+  bool first = true;
+  while (ns < a.L) {
+    const int rad = (first && lead) ? (1 << lead) : 16;
+    const bool last = ns * rad == a.L;
+    const int hook = (first ? first_hook : kNoHook) | (last ? last_hook : kNoHook);
+    a.src = *cur;
+    a.dst = *alt;
+    a.NS = ns;
+    const int64_t units = (hook == kIntensity ? a.rows / 2 : a.rows) * (a.L / rad);
+    const int grid = grid_for(units);
+#define CB_WPASS(RD, HK) wide_pass<R, RD, INV, HK><<<grid, kThreads, 0, st>>>(a)
+#define CB_WHOOK(RD)                                         \
+  switch (hook) {                                            \
+    case kRotate: CB_WPASS(RD, kRotate); break;              \
+    case kPhasor: CB_WPASS(RD, kPhasor); break;              \
+    case kIntensity: CB_WPASS(RD, kIntensity); break;        \
+    default: CB_WPASS(RD, kNoHook); break;                   \
+  }
+    switch (rad) {
+      case 2: CB_WHOOK(2) break;
+      case 4: CB_WHOOK(4) break;
+      case 8: CB_WHOOK(8) break;
+      default: CB_WHOOK(16) break;
+    }
+#undef CB_WHOOK
+#undef CB_WPASS
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    std::swap(*cur, *alt);
+    ns *= rad;
+    first = false;
+  }
+  return cudaSuccess;
+}
+
+template <typename R, int P>
+cudaError_t mimo_launch(const StepArgs<R>& s, const Cx<R>* Z, Cx<R>* T, cudaStream_t st) {
+  const int64_t units = s.nc * (s.Q / 4 + 1);
+  wide_mimo<R, P><<<grid_for(units), kThreads, 0, st>>>(s, Z, T);
+  return cudaGetLastError();
+}
+
+template <typename R>
+cudaError_t mimo_dispatch(const StepArgs<R>& s, const Cx<R>* Z, Cx<R>* T, cudaStream_t st) {
+  switch (s.P) {
+    case 1: return mimo_launch<R, 1>(s, Z, T, st);
+    case 2: return mimo_launch<R, 2>(s, Z, T, st);
+    case 3: return mimo_launch<R, 3>(s, Z, T, st);
+    case 4: return mimo_launch<R, 4>(s, Z, T, st);
+    case 5: return mimo_launch<R, 5>(s, Z, T, st);
+    case 6: return mimo_launch<R, 6>(s, Z, T, st);
+    case 7: return mimo_launch<R, 7>(s, Z, T, st);
+    case 8: return mimo_launch<R, 8>(s, Z, T, st);
+    case 9: return mimo_launch<R, 9>(s, Z, T, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// Bytes of device workspace per (waveform, block) of a chunk.
+template <typename R>
+size_t bytes_per_block(int N) {
+  // two ping-pong field buffers [2][N], two half-length buffers (N reals,
+  // i.e. N/2 complex, each)
+  return sizeof(Cx<R>) * (size_t)(2 * 2 * N + 2 * (N / 2));
+}
+
+template <typename R>
+cudaError_t run(const Params<R>& prm, int P, int Q, int64_t nclusters, cudaStream_t st) {
+  const int N = P * Q, H = Q / 2;
+  // chunk of (waveform, block) pairs: at most ~256 MB of workspace
+  const size_t per = bytes_per_block<R>(N);
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(nclusters, (int64_t)((256u << 20) / per)));
+  void* ws = nullptr;
+  cudaError_t e = cudaMallocAsync(&ws, per * (size_t)chunk, st);
+  if (e != cudaSuccess) return e;
+  Cx<R>* bufA = reinterpret_cast<Cx<R>*>(ws);
+  Cx<R>* bufB = bufA + (size_t)chunk * 2 * N;
+  Cx<R>* hA = bufB + (size_t)chunk * 2 * N;
+  Cx<R>* hB = hA + (size_t)chunk * (N / 2);
+  for (int64_t c0 = 0; c0 < nclusters && e == cudaSuccess; c0 += chunk) {
+    StepArgs<R> s{prm, P, Q, N, c0, std::min<int64_t>(chunk, nclusters - c0)};
+    const int64_t units = s.nc * 2 * N;
+    PassArgs<R> pa{};
+    pa.twN = prm.twN;
+    pa.P = P;
+    pa.n_sets = prm.n_sets;
+    pa.n_steps = prm.n_steps;
+    pa.rows_per_wave = prm.nb * P;
+    pa.q0 = c0 * P;
+    // ---- window, FFT_N per polarisation, demux (+ 1/P, first phasor)
+    wide_window<R><<<grid_for(units), kThreads, 0, st>>>(s, bufA);
+    Cx<R>* cur = bufA;
+    Cx<R>* alt = bufB;
+    pa.rows = s.nc * 2;
+    pa.L = N;
+    pa.tw_stride = 1;
+    if ((e = fft_rows<R, false>(pa, &cur, &alt, kNoHook, kNoHook, st)) != cudaSuccess) break;
+    wide_demux<R><<<grid_for(units), kThreads, 0, st>>>(s, cur, alt);
+    std::swap(cur, alt);  // cur: subband rows [c][i][pol][Q] (spectra)
+    // ---- steps
+    for (int stp = 0; stp < prm.n_steps; ++stp) {
+      pa.rows = s.nc * P * 2;
+      pa.L = Q;
+      pa.tw_stride = P;
+      pa.inten = reinterpret_cast<R*>(hA);
+      if ((e = fft_rows<R, true>(pa, &cur, &alt, kNoHook, kIntensity, st)) != cudaSuccess) break;
+      // rfft of the intensity: half-length FFT of the packed reals
+      PassArgs<R> ph = pa;
+      ph.rows = s.nc * P;
+      ph.L = H;
+      ph.tw_stride = 2 * P;
+      Cx<R>* hc = hA;
+      Cx<R>* ha = hB;
+      if ((e = fft_rows<R, false>(ph, &hc, &ha, kNoHook, kNoHook, st)) != cudaSuccess) break;
+      if ((e = mimo_dispatch<R>(s, hc, ha, st)) != cudaSuccess) break;
+      std::swap(hc, ha);  // hc: twisted theta_hat
+      if ((e = fft_rows<R, true>(ph, &hc, &ha, kNoHook, kNoHook, st)) != cudaSuccess) break;
+      // rotation fused into the first pass of the forward FFT, the next
+      // phasor into its last
+      pa.theta = reinterpret_cast<const R*>(hc);
+      pa.tscale = prm.theta_scale;
+      pa.step = stp;
+      pa.phasor = prm.phasor;
+      pa.ph_index = prm.ph_index;
+      if ((e = fft_rows<R, false>(pa, &cur, &alt, kRotate, kPhasor, st)) != cudaSuccess) break;
+    }
+    if (e != cudaSuccess) break;
+    // ---- merge, IFFT_N, keep
+    wide_merge<R><<<grid_for(units), kThreads, 0, st>>>(s, cur, alt);
+    std::swap(cur, alt);
+    pa.rows = s.nc * 2;
+    pa.L = N;
+    pa.tw_stride = 1;
+    if ((e = fft_rows<R, true>(pa, &cur, &alt, kNoHook, kNoHook, st)) != cudaSuccess) break;
+    wide_store<R><<<grid_for(s.nc * 2 * prm.keep), kThreads, 0, st>>>(s, cur);
+    e = cudaGetLastError();
+  }
+  const cudaError_t ef = cudaFreeAsync(ws, st);
+  return e != cudaSuccess ? e : ef;
+}
+
+}  // namespace wide
+
+cudaError_t wide_run_float(const Params<float>& prm, int P, int Q, int64_t nclusters,
+                           cudaStream_t st) {
+  return wide::run<float>(prm, P, Q, nclusters, st);
+}
+cudaError_t wide_run_double(const Params<double>& prm, int P, int Q, int64_t nclusters,
+                            cudaStream_t st) {
+  return wide::run<double>(prm, P, Q, nclusters, st);
+}
+
+}  // namespace cbessfm

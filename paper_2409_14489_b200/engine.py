@@ -184,8 +184,8 @@ def get_plan(cfg, rate: float, coeffs, dtype: str = "c128",
         raise ValueError(
             f"no sm_100a kernel for n_subbands={n_sb}, "
             f"N'={cfg.block_size // n_sb} ({dtype}); this build supports "
-            "1..9 subbands and power-of-two N' in [256, 4096] (c128) or "
-            "[256, 8192] (c64)")
+            "1..9 subbands and power-of-two N' in [256, 65536]; N' above "
+            "4096 (c128) / 8192 (c64) runs the wide path)")
     with torch.cuda.device(device):
         plan = _native.NativePlan(
             dtype=_DTYPES[dtype], n_subbands=n_sb, block_size=cfg.block_size,

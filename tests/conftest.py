@@ -22,7 +22,8 @@ from paper_2409_14489_b200 import (CoefficientSet, DbpConfig,  # noqa: E402
                                    DualPolWaveform, LinkConfig)
 
 CASES = ("cfg1_nsb1", "cfg1_nsb3_st2", "cfg1_nsb9_st3", "cfg1_nsb2_frac",
-         "cfg1_nst0", "cfg2_nsb5", "cfg4_nsb5_st50", "cfg4_nsb5_st10", "cfg4_nsb5_st1")
+         "cfg1_nst0", "cfg2_nsb5", "cfg4_nsb5_st50", "cfg4_nsb5_st10", "cfg4_nsb5_st1",
+         "wide_nsb2", "wide_nsb1")
 
 
 def pytest_configure(config):

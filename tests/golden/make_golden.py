@@ -201,6 +201,21 @@ def main():
             channel_freq=0.0, channel_bw=100e9))
 
     # --- config-4 layout (50 x 80 km), N' = 4096, 50 steps, n = 32768
+    # --- the reference's full-scale DBP geometry (configs/fullscale.yaml:14-21,
+    #     :32): N = 16384, N_ov = 1800, rho = 0.5, N_sb in {2, 1} -> N' = 8192
+    #     and 16384 (the wide path), on a 5-channel WDM waveform, n = 65536
+    if want("wide_nsb2") or want("wide_nsb1"):
+        wdmw, ww, _ = wave_wdm5(8192, seed=21)
+        ratew = ww.sample_rate
+        for nsb, nst, name in ((2, 15, "wide_nsb2"), (1, 3, "wide_nsb1")):
+            if not want(name):
+                continue
+            cfg = fd.DbpConfig(link=link(15), variant="CB_ESSFM", n_steps=nst,
+                               n_subbands=nsb, splitting_ratio=0.5,
+                               block_size=16384, overlap=1800, oversampling=1.6)
+            c = coeffs_for(cfg, ratew, wdmw.launch_power_w, 31)
+            save_case(name, ww, cfg, c, run(ww, cfg, c), wave="wide")
+
     if want("cfg4_nsb5_st50"):
         wdm4, w4, _ = wave_wdm5(4096, seed=13, spans=50)
         cfg = fd.DbpConfig(link=link(50), variant="CB_ESSFM", n_steps=50,

@@ -18,7 +18,9 @@ def test_num_blocks_matches_reference_framing():
 
 
 @pytest.mark.parametrize("dtype,p,n,ok", [(_native.C64, 5, 10240, True), (_native.C128, 5, 10240, True),
-                                          (_native.C64, 1, 8192, True), (_native.C128, 1, 8192, False),
+                                          (_native.C64, 1, 8192, True), (_native.C128, 1, 8192, True),
+                                          (_native.C128, 2, 16384, True), (_native.C64, 1, 16384, True),
+                                          (_native.C128, 1, 131072, False),
                                           (_native.C64, 10, 20480, False), (_native.C64, 5, 10000, False),
                                           (_native.C64, 3, 3 * 128, False)])
 def test_supported_shapes(dtype, p, n, ok):

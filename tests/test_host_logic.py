@@ -221,7 +221,8 @@ def test_native_library_exports_every_header_symbol():
     assert declared == set(_native.SIGNATURES)
     assert lib.cbessfm_version() == _native.ABI_VERSION
     assert lib.cbessfm_supported(0, 5, 10240) == 1
-    assert lib.cbessfm_supported(1, 5, 10240 * 4) == 0
+    assert lib.cbessfm_supported(1, 5, 10240 * 4) == 1   # N' = 8192: the wide path
+    assert lib.cbessfm_supported(1, 5, 5 * 131072) == 0
     assert lib.cbessfm_supported(0, 3, 3000) == 0
 
 
