@@ -20,7 +20,7 @@ n = 1 << 20
 x = gaussian_wdm(n, RATE, seed=3)
 link = pb.LinkConfig(num_spans=15, span_length_km=80.0, alpha_db_per_km=0.2,
                      dispersion_d_ps_nm_km=17.0, gamma_w_km=1.3)
-for nsb in (1, 2, 4, 8):
+for nsb in (1, 2, 4):   # N_sb = 8 needs overlap % 16 == 0 (the reference rejects 1800)
     cfg = pb.DbpConfig(link=link, variant="CB_ESSFM", n_steps=15, n_subbands=nsb,
                        splitting_ratio=0.5, block_size=16384, overlap=1800, oversampling=1.6)
     with warnings.catch_warnings():
