@@ -76,7 +76,10 @@ __global__ void __launch_bounds__(kThreads) wide_pass(const PassArgs<R> a) {
       const int64_t row = HOOK == kIntensity ? 2 * row0 + h : row0;
       const Cx<R>* s = a.src + row * a.L;
 #pragma unroll
-      for (int r = 0; r < RAD; ++r) v[h][r] = s[j + r * LR];
+      for (int r = 0; r < RAD; ++r) {
+        CB_CHECK(row >= 0 && row < a.rows && j + r * LR < a.L);
+        v[h][r] = s[j + r * LR];
+      }
       if constexpr (HOOK == kRotate) {
         // exp(-i theta) on the natural-order inputs (dbp.py:208), the same
         // sincos and product as the fused kernel's RotationHook
@@ -111,7 +114,10 @@ __global__ void __launch_bounds__(kThreads) wide_pass(const PassArgs<R> a) {
       }
       Cx<R>* d = a.dst + row * a.L;
 #pragma unroll
-      for (int r = 0; r < RAD; ++r) d[base + r * a.NS] = v[h][bitrev<RAD>(r)];
+      for (int r = 0; r < RAD; ++r) {
+        CB_CHECK(base + r * a.NS < a.L);
+        d[base + r * a.NS] = v[h][bitrev<RAD>(r)];
+      }
     }
     if constexpr (HOOK == kIntensity) {
       // I = |x|^2 + |y|^2 of the time samples (dbp.py:193)
@@ -152,6 +158,7 @@ __global__ void __launch_bounds__(kThreads) wide_window(const StepArgs<R> s, Cx<
     if (start < 0) start += p.n;
     int64_t idx = start + t;
     if (idx >= p.n) idx -= p.n;
+    CB_CHECK(idx >= 0 && idx < p.n);
     A[u] = p.in[wv * p.in_bstride + pol * p.in_pstride + idx];
   }
 }
@@ -173,6 +180,7 @@ __global__ void __launch_bounds__(kThreads) wide_demux(const StepArgs<R> s, cons
     const int64_t c = u / (2 * (int64_t)s.N);
     int g = i * s.Q + (m + s.Q / 2) % s.Q + s.N / 2;
     if (g >= s.N) g -= s.N;
+    CB_CHECK(g >= 0 && g < s.N);
     const Cx<R> v = F[(c * 2 + pol) * s.N + g];
     S[u] = s.P > 1 ? cmul(scale(v, invP), ldg(ph0 + (int64_t)i * s.Q + m))
                    : cmul(v, ldg(ph0 + m));
@@ -195,6 +203,7 @@ __global__ void __launch_bounds__(kThreads) wide_merge(const StepArgs<R> s, cons
     if (sh >= s.N) sh -= s.N;
     i = sh / s.Q;
     m = (sh % s.Q + s.Q / 2) % s.Q;
+    CB_CHECK(i >= 0 && i < s.P && m >= 0 && m < s.Q);
     F[u] = S[((c * s.P + i) * 2 + pol) * s.Q + m];
   }
 }
@@ -213,6 +222,7 @@ __global__ void __launch_bounds__(kThreads) wide_store(const StepArgs<R> s, cons
     const int64_t span = min(p.keep, p.n - b * p.keep);
     if (t >= p.half + span) continue;
     const int64_t obase = b * p.keep - p.half - p.out_origin;
+    CB_CHECK(obase + t >= 0 && (p.out_origin != 0 || obase + t < p.n));
     p.out[wv * p.out_bstride + pol * p.out_pstride + obase + t] = F[(c * 2 + pol) * s.N + t];
   }
 }

@@ -21,7 +21,8 @@ from conftest import ROOT
 pytestmark = pytest.mark.gpu
 
 LIB = ROOT / "paper_2409_14489_b200" / "libcbessfm_checked.so"
-CASES = ["fat", "cluster64", "cluster128", "cluster9", "ip", "nlpr", "ssfm", "rx", "coeff"]
+CASES = ["fat", "cluster64", "cluster128", "cluster9", "ip", "wide128", "wide64", "nlpr", "ssfm",
+         "rx", "coeff"]
 
 
 def _checked_lib():

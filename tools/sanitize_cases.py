@@ -5,7 +5,8 @@
 
 Cases: fat (FP32 one-block-per-CTA, P = 5, N' = 2048), cluster64 / cluster128
 (P-CTA cluster kernel, P = 5), cluster9 (P = 9, non-portable cluster, c128),
-ip (in-place-pass c128 kernel, P = 5), nlpr (cbessfm_nlpr), ssfm
+ip (in-place-pass c128 kernel, P = 5), wide128 / wide64 (wide-subband
+path, N' = 8192 c128 / 16384 c64), nlpr (cbessfm_nlpr), ssfm
 (cooperative four-step propagator), rx (receiver symbols + SNR), coeff
 (coefficient grid transform). Each case runs one launch (two blocks for the
 block kernels) and checks the output is finite."""
@@ -56,6 +57,16 @@ def case_cluster9():
 
 def case_ip():
     return _block_kernel("ip", "c128")
+
+
+def case_wide128():
+    # wide-subband path (csrc/cbessfm_wide.cu), N' = 8192 at c128
+    return _block_kernel("cluster", "c128", name="wide_nsb2", blocks=(0, 2))
+
+
+def case_wide64():
+    # wide-subband path, N' = 16384 at c64
+    return _block_kernel("cluster", "c64", name="wide_nsb1", blocks=(0, 2))
 
 
 def case_nlpr():
