@@ -167,7 +167,10 @@ cbessfm_status cbessfm_run_host(const cbessfm_plan* plan, const cbessfm_host_io*
 
 /* One waveform in the reference's layout (cbessfm_dualpol_io), host in,
  * host out, synchronous; `stream` orders the device work. The entry the
- * drop-in run_dbp calls. */
+ * drop-in run_dbp calls. The staging copies also check every input sample
+ * (dbp.py:449 w.require_finite()): a NaN or infinity returns
+ * CBESSFM_ERR_INVALID "waveform contains non-finite samples" (outputs
+ * undefined). */
 cbessfm_status cbessfm_run_dualpol(const cbessfm_plan* plan, const cbessfm_dualpol_io* io,
                                    void* stream);
 

@@ -698,13 +698,30 @@ cbessfm_status host_pipeline(cbessfm_plan* p, const void* in, void* out, int64_t
 }
 
 // c128 -> plan dtype copy of samples [a, b) of one polarisation row
-void stage_in(const cbessfm_plan* p, const double* src, void* row, int64_t a, int64_t b) {
+// Staging copy of samples [a, b) of one polarisation into the page-locked
+// row (cast to float for c64). Returns false if any component is NaN or
+// infinite: the copy reads every sample anyway, so the reference's
+// require_finite check (dbp.py:449) rides along at no extra memory pass.
+bool stage_in(const cbessfm_plan* p, const double* src, void* row, int64_t a, int64_t b) {
+  constexpr uint64_t kExp = 0x7ff0000000000000ull;
+  uint64_t bad = 0;
   if (p->dtype == CBESSFM_C128) {
-    memcpy((double*)row + 2 * a, src + 2 * a, (size_t)(b - a) * 16);
+    const uint64_t* s = reinterpret_cast<const uint64_t*>(src);
+    uint64_t* d = reinterpret_cast<uint64_t*>(row);
+    for (int64_t i = 2 * a; i < 2 * b; ++i) {
+      const uint64_t v = s[i];
+      d[i] = v;
+      bad |= (uint64_t)((v & kExp) == kExp);
+    }
   } else {
+    const uint64_t* s = reinterpret_cast<const uint64_t*>(src);
     float* d = (float*)row;
-    for (int64_t i = 2 * a; i < 2 * b; ++i) d[i] = (float)src[i];
+    for (int64_t i = 2 * a; i < 2 * b; ++i) {
+      d[i] = (float)src[i];
+      bad |= (uint64_t)((s[i] & kExp) == kExp);
+    }
   }
+  return bad == 0;
 }
 void stage_out(const cbessfm_plan* p, const void* row, double* dst, int64_t a, int64_t b) {
   if (p->dtype == CBESSFM_C128) {
@@ -777,12 +794,14 @@ cbessfm_status cbessfm_run_dualpol(const cbessfm_plan* cp, const cbessfm_dualpol
   for (int64_t a = 0; a < wrap; a += piece) ranges.push_back({a, std::min(wrap, a + piece)});
   std::vector<std::atomic<int>> done(ranges.size());
   for (auto& d : done) d.store(0);
+  std::atomic<int> nonfinite{0};
   std::mutex wmu;
   std::condition_variable wcv;
   for (size_t t = 0; t < ranges.size(); ++t) {
     p->pool->submit([&, t] {
-      stage_in(p, io->in_x, rin, ranges[t].first, ranges[t].second);
-      stage_in(p, io->in_y, rin + rowb, ranges[t].first, ranges[t].second);
+      const bool okx = stage_in(p, io->in_x, rin, ranges[t].first, ranges[t].second);
+      const bool oky = stage_in(p, io->in_y, rin + rowb, ranges[t].first, ranges[t].second);
+      if (!(okx && oky)) nonfinite.store(1);
       {
         std::lock_guard<std::mutex> lk(wmu);
         done[t].store(1);
@@ -840,6 +859,8 @@ cbessfm_status cbessfm_run_dualpol(const cbessfm_plan* cp, const cbessfm_dualpol
   p->host_events.clear();
   if (e != cudaSuccess) return cuda_fail(e, "cbessfm_run_dualpol d2h");
   if (e2 != cudaSuccess) return cuda_fail(e2, "cbessfm_run_dualpol");
+  if (nonfinite.load())  // the outputs are left undefined, as after any error
+    return fail(CBESSFM_ERR_INVALID, "waveform contains non-finite samples");
   return CBESSFM_OK;
 }
 

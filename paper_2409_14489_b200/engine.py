@@ -265,7 +265,12 @@ def run_dbp(w, cfg, coeffs=None, counter=None, *, dtype: str = "c128",
     the reference to ~1e-15; "c64" runs the FP32 kernel (tables still built
     in FP64). Returns a new waveform of the input's class."""
     torch = _torch()
-    w.require_finite()
+    # dbp.py:449 w.require_finite(): on the block path the native staging
+    # copies check every sample (cbessfm_run_dualpol, same ValueError) in
+    # the same pass that reads them; it runs here first wherever an earlier
+    # error would otherwise pre-empt it
+    if cfg.variant == "IDEAL_SSFM" or cfg.block_size > w.num_samples:
+        w.require_finite()
     validate_config(cfg)
     if cfg.variant == "IDEAL_SSFM":
         # fine-step inverse propagation of the whole sequence (dbp.py:451-454)
@@ -285,16 +290,11 @@ def run_dbp(w, cfg, coeffs=None, counter=None, *, dtype: str = "c128",
     plan = get_plan(cfg, w.sample_rate, coeffs if cfg.n_steps else None,
                     dtype, device)
     n_blocks = BlockSchedule(n, cfg.block_size, cfg.overlap).n_blocks
-    if cfg.variant == "CB_ESSFM":
-        record_cb_blocks(counter, cfg.block_size, cfg.n_steps, n_sb, n_blocks)
-    else:
-        taps = 1 if not cfg.n_steps else coeffs.coeffs[0].size
-        record_time_domain_blocks(counter, cfg.block_size, cfg.n_steps, taps,
-                                  cfg.variant == "EDC", n_blocks)
     # the reference's layout straight into the native entry: its host
     # threads stage (and, for c64, cast) x and y into the plan's page-locked
-    # buffers chunk by chunk, pipelined with H2D / kernel / D2H, and write
-    # the kept samples into fresh complex128 arrays (cbessfm_run_dualpol)
+    # buffers chunk by chunk, checking finiteness, pipelined with H2D /
+    # kernel / D2H, and write the kept samples into recycled complex128
+    # arrays (cbessfm_run_dualpol)
     x_in = np.ascontiguousarray(w.x, dtype=np.complex128)
     y_in = np.ascontiguousarray(w.y, dtype=np.complex128)
     x_out, y_out = _Lease(n).arrays()
@@ -302,6 +302,14 @@ def run_dbp(w, cfg, coeffs=None, counter=None, *, dtype: str = "c128",
     with torch.cuda.device(dev):
         stream = torch.cuda.current_stream(dev)
         plan.run_dualpol(x_in, y_in, x_out, y_out, chunks=8, stream=stream.cuda_stream)
+    # counted once the call has succeeded (the reference raises on a
+    # non-finite input before any block is counted)
+    if cfg.variant == "CB_ESSFM":
+        record_cb_blocks(counter, cfg.block_size, cfg.n_steps, n_sb, n_blocks)
+    else:
+        taps = 1 if not cfg.n_steps else coeffs.coeffs[0].size
+        record_time_domain_blocks(counter, cfg.block_size, cfg.n_steps, taps,
+                                  cfg.variant == "EDC", n_blocks)
     return type(w)(x_out, y_out, w.sample_rate, w.center_freq)
 
 

@@ -175,6 +175,25 @@ def test_errors_match_reference(cuda):
         pb.run_dbp(g.wave, replace(g.cfg, block_size=3000, overlap=0), g.coeffs)
 
 
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("bad_value", [np.nan, np.inf, -np.inf, complex(0, np.nan)])
+def test_nonfinite_input_raises_before_counting(cuda, dtype, bad_value):
+    # dbp.py:449: require_finite raises before any block is processed or
+    # counted; the drop-in checks in its native staging pass instead, with
+    # the same ValueError and the counter left untouched
+    g = golden("cfg2_nsb5")
+    bad = pb.DualPolWaveform(g.wave.x, g.wave.y.copy(), g.wave.sample_rate)
+    bad.y[g.wave.num_samples - 5] = bad_value           # inside the wrap piece
+    c = pb.CostCounter()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        with pytest.raises(ValueError, match="non-finite"):
+            pb.run_dbp(bad, g.cfg, g.coeffs, counter=c, dtype=dtype)
+        assert c.as_report(g.wave.num_samples, g.cfg.oversampling).rm_per_2d == 0
+        out = pb.run_dbp(g.wave, g.cfg, g.coeffs, dtype=dtype)   # the plan still works
+    assert rel_rms(np.vstack([out.x, out.y]), g.out) < TOL[dtype]
+
+
 def test_counter_hook_matches_reference_cost(cuda):
     # pkg/tests/test_complexity.py:111-121: partial-tile overshoot < 1 %
     g = golden("cfg2_nsb5")
