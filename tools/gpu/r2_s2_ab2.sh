@@ -1,0 +1,10 @@
+# prologue micro-opts (window loads in flight, W_P in registers) vs HEAD
+python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider -k golden > gpurun_out/ab2_tests.log 2>&1; echo "tests rc=$?"; tail -1 gpurun_out/ab2_tests.log
+for rep in 1 2; do
+for lib in libcbessfm_head.so libcbessfm.so; do
+  export CBESSFM_LIB=$PWD/paper_2409_14489_b200/$lib
+  a=$(python bench.py --steps 4 --no-cpu-baseline --no-e2e --no-extras 2>/dev/null | tail -1 | python -c "import json,sys; d=json.load(sys.stdin); print(round(d['ms_per_step'],2), '%.3g'%d['value'])")
+  b=$(python bench.py --workload cfg2 --batch 8 --steps 10 --no-cpu-baseline --no-e2e --no-extras 2>/dev/null | tail -1 | python -c "import json,sys; d=json.load(sys.stdin); print(round(d['ms_per_step'],4))")
+  c=$(python bench.py --workload cfg4s1 --dtype c128 --steps 10 --no-cpu-baseline --no-e2e --no-extras 2>/dev/null | tail -1 | python -c "import json,sys; d=json.load(sys.stdin); print(round(d['ms_per_step'],4))")
+  echo "rep$rep $lib cfg5_c128 $a | cfg2_b8_c128 $b | cfg4s1_c128 $c"
+done; done
