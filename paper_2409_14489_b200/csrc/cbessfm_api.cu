@@ -20,10 +20,11 @@
 #include "cbessfm_launch.cuh"
 
 namespace cbessfm {
+size_t wide_workspace_bytes(int real_bytes, int N, int64_t nclusters);
 cudaError_t wide_run_float(const Params<float>& prm, int P, int Q, int64_t nclusters,
-                           cudaStream_t st);
+                           cudaStream_t st, void* ws, size_t ws_bytes);
 cudaError_t wide_run_double(const Params<double>& prm, int P, int Q, int64_t nclusters,
-                            cudaStream_t st);
+                            cudaStream_t st, void* ws, size_t ws_bytes);
 }  // namespace cbessfm
 
 namespace {
@@ -133,6 +134,12 @@ struct cbessfm_plan {
   void* pin_out = nullptr;
   size_t pin_bytes = 0;
   struct Pool* pool = nullptr;
+  // wide-subband path workspace (csrc/cbessfm_wide.cu), kept across calls;
+  // calls on different streams take turns (wide_done orders them)
+  std::mutex wide_mu;
+  void* wide_ws = nullptr;
+  size_t wide_bytes = 0;
+  cudaEvent_t wide_done = nullptr;
 };
 
 // Host worker threads for cbessfm_run_dualpol's staging copies (FIFO task
@@ -338,6 +345,11 @@ void free_plan(cbessfm_plan* p) {
     if (sl.done) cudaEventDestroy(sl.done);
   }
   for (cudaStream_t st : p->host_streams) cudaStreamDestroy(st);
+  if (p->wide_done) {
+    cudaEventSynchronize(p->wide_done);
+    cudaEventDestroy(p->wide_done);
+  }
+  cudaFree(p->wide_ws);
   delete p->pool;
   if (p->pin_in) cudaFreeHost(p->pin_in);
   if (p->pin_out) cudaFreeHost(p->pin_out);
@@ -560,11 +572,30 @@ cbessfm_status cbessfm_run(const cbessfm_plan* p, const cbessfm_io* io, void* st
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e;
   if (is_wide(p)) {
+    cbessfm_plan* wp = const_cast<cbessfm_plan*>(p);  // only the workspace is touched
+    std::lock_guard<std::mutex> lk(wp->wide_mu);
+    const size_t need =
+        cbessfm::wide_workspace_bytes(p->dtype == CBESSFM_C64 ? 4 : 8, p->N, nclusters);
+    if (!wp->wide_done &&
+        (e = cudaEventCreateWithFlags(&wp->wide_done, cudaEventDisableTiming)) != cudaSuccess)
+      return cuda_fail(e, "event create");
+    if (wp->wide_bytes < need) {
+      cudaEventSynchronize(wp->wide_done);  // its last user has finished
+      cudaFree(wp->wide_ws);
+      wp->wide_ws = nullptr;
+      wp->wide_bytes = 0;
+      if ((e = cudaMalloc(&wp->wide_ws, need)) != cudaSuccess) return cuda_fail(e, "wide workspace");
+      wp->wide_bytes = need;
+    }
+    cudaStreamWaitEvent(st, wp->wide_done, 0);
     if (p->dtype == CBESSFM_C64)
-      e = cbessfm::wide_run_float(make_params<float>(p, io), p->P, p->Q, nclusters, st);
+      e = cbessfm::wide_run_float(make_params<float>(p, io), p->P, p->Q, nclusters, st,
+                                  wp->wide_ws, wp->wide_bytes);
     else
-      e = cbessfm::wide_run_double(make_params<double>(p, io), p->P, p->Q, nclusters, st);
+      e = cbessfm::wide_run_double(make_params<double>(p, io), p->P, p->Q, nclusters, st,
+                                   wp->wide_ws, wp->wide_bytes);
     if (e != cudaSuccess) return cuda_fail(e, "cbessfm wide-path launch");
+    if ((e = cudaEventRecord(wp->wide_done, st)) != cudaSuccess) return cuda_fail(e, "event record");
     return CBESSFM_OK;
   }
   if (p->dtype == CBESSFM_C64)

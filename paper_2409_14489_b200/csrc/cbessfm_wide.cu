@@ -385,15 +385,22 @@ size_t bytes_per_block(int N) {
   return sizeof(Cx<R>) * (size_t)(2 * 2 * N + 2 * (N / 2));
 }
 
+// Workspace a launch of nclusters (waveform, block) pairs uses: chunks of
+// at most ~256 MB.
 template <typename R>
-cudaError_t run(const Params<R>& prm, int P, int Q, int64_t nclusters, cudaStream_t st) {
-  const int N = P * Q, H = Q / 2;
-  // chunk of (waveform, block) pairs: at most ~256 MB of workspace
+size_t workspace_bytes(int N, int64_t nclusters) {
   const size_t per = bytes_per_block<R>(N);
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(nclusters, (int64_t)((256u << 20) / per)));
-  void* ws = nullptr;
-  cudaError_t e = cudaMallocAsync(&ws, per * (size_t)chunk, st);
-  if (e != cudaSuccess) return e;
+  return per * (size_t)chunk;
+}
+
+template <typename R>
+cudaError_t run(const Params<R>& prm, int P, int Q, int64_t nclusters, cudaStream_t st, void* ws,
+                size_t ws_bytes) {
+  const int N = P * Q, H = Q / 2;
+  const size_t per = bytes_per_block<R>(N);
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(nclusters, (int64_t)(ws_bytes / per)));
+  cudaError_t e = cudaSuccess;
   Cx<R>* bufA = reinterpret_cast<Cx<R>*>(ws);
   Cx<R>* bufB = bufA + (size_t)chunk * 2 * N;
   Cx<R>* hA = bufB + (size_t)chunk * 2 * N;
@@ -456,19 +463,22 @@ cudaError_t run(const Params<R>& prm, int P, int Q, int64_t nclusters, cudaStrea
     wide_store<R><<<grid_for(s.nc * 2 * prm.keep), kThreads, 0, st>>>(s, cur);
     e = cudaGetLastError();
   }
-  const cudaError_t ef = cudaFreeAsync(ws, st);
-  return e != cudaSuccess ? e : ef;
+  return e;
 }
 
 }  // namespace wide
 
+size_t wide_workspace_bytes(int real_bytes, int N, int64_t nclusters) {
+  return real_bytes == 4 ? wide::workspace_bytes<float>(N, nclusters)
+                         : wide::workspace_bytes<double>(N, nclusters);
+}
 cudaError_t wide_run_float(const Params<float>& prm, int P, int Q, int64_t nclusters,
-                           cudaStream_t st) {
-  return wide::run<float>(prm, P, Q, nclusters, st);
+                           cudaStream_t st, void* ws, size_t ws_bytes) {
+  return wide::run<float>(prm, P, Q, nclusters, st, ws, ws_bytes);
 }
 cudaError_t wide_run_double(const Params<double>& prm, int P, int Q, int64_t nclusters,
-                            cudaStream_t st) {
-  return wide::run<double>(prm, P, Q, nclusters, st);
+                            cudaStream_t st, void* ws, size_t ws_bytes) {
+  return wide::run<double>(prm, P, Q, nclusters, st, ws, ws_bytes);
 }
 
 }  // namespace cbessfm
