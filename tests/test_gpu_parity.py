@@ -413,3 +413,53 @@ def test_in_place_pass_kernel_matches_oracle(cuda, n_sb, monkeypatch):
         assert rel_rms(np.vstack([out.x, out.y]), ref) < TOL["c128"]
     plan = pb.get_plan(cfg, rate, c, "c128")
     assert plan.info().kernel_name.startswith("cbessfm_ip_kernel")
+
+
+@pytest.mark.parametrize("name,dtype", [("wide_nsb2", "c128"), ("wide_nsb1", "c64")])
+def test_wide_path_launch_forms(cuda, name, dtype):
+    # the wide-subband path (csrc/cbessfm_wide.cu) behind every launch form
+    # the fused kernels serve: batches, block ranges, halo'd time shards,
+    # coefficient sets in one launch and the pinned-host pipeline
+    import torch
+    from paper_2409_14489_b200.planner import gather_slice
+    g = golden(name)
+    rate = g.wave.sample_rate
+    ct = torch.complex128 if dtype == "c128" else torch.complex64
+    tol = TOL[dtype]
+    f0 = np.vstack([g.wave.x, g.wave.y])
+    n = f0.shape[-1]
+    f1 = gaussian_wdm(n, rate, seed=11)
+    plan = pb.get_plan(g.cfg, rate, g.coeffs, dtype)
+    assert plan.info().kernel_name.startswith("cbessfm_wide")
+    x = torch.from_numpy(np.stack([f0, f1])).to(cuda).to(ct)
+    whole = pb.run_dbp_tensor(x, g.cfg, g.coeffs, rate)
+    assert rel_rms(whole[0].to(torch.complex128).cpu().numpy(), g.out) < tol
+    ref1 = orc.run_cb_blocks(f1, g.cfg, rate, g.coeffs)
+    assert rel_rms(whole[1].to(torch.complex128).cpu().numpy(), ref1) < tol
+    sched = pb.BlockSchedule(n, g.cfg.block_size, g.cfg.overlap)
+    parts = torch.zeros_like(x)
+    for rng in ((0, 1), (1, sched.n_blocks)):
+        pb.run_dbp_tensor(x, g.cfg, g.coeffs, rate, out=parts, block_range=rng)
+    assert torch.equal(parts, whole)
+    # time shard from a halo'd slice
+    out = np.zeros_like(f0)
+    for b0, b1 in ((0, 2), (2, sched.n_blocks)):
+        origin, length = sched.input_range(b0, b1)
+        sl = torch.from_numpy(gather_slice(f0, origin, length)[None]).to(cuda).to(ct)
+        o0, o1 = sched.output_range(b0, b1)
+        dst = torch.zeros((1, 2, o1 - o0), dtype=ct, device=cuda)
+        pb.launch(plan, sl, dst, n=n, block_range=(b0, b1), in_origin=origin, out_origin=o0)
+        out[:, o0:o1] = dst[0].to(torch.complex128).cpu().numpy()
+    assert rel_rms(out, g.out) < tol
+    # pinned-host pipeline (cbessfm_run_host: chunked launches on several streams)
+    eng = pb.DbpEngine(g.cfg, g.coeffs, rate, dtype=dtype)
+    hx = x[:1].cpu().pin_memory()
+    ho = eng.run_host(hx, chunks=4)
+    torch.cuda.synchronize()
+    assert torch.equal(ho.to(whole.device), whole[:1])
+    # coefficient sets on one waveform in one launch
+    sets = [g.coeffs, replace(g.coeffs, step_scales=g.coeffs.step_scales * 1.3)]
+    outs = pb.run_dbp_sets(g.wave, g.cfg, sets, dtype=dtype)
+    for c, o in zip(sets, outs):
+        ref = orc.run_cb_blocks(f0, g.cfg, rate, c)
+        assert rel_rms(np.vstack([o.x, o.y]), ref) < tol
