@@ -377,6 +377,184 @@ cudaError_t mimo_dispatch(const StepArgs<R>& s, const Cx<R>* Z, Cx<R>* T, cudaSt
   }
 }
 
+// ------------------------------------------------------------------------
+// Per-row kernels: one CTA holds one length-L row in shared memory (padded,
+// one slot per 16) and runs every pass of the transform in place (load,
+// barrier, store, barrier), so a step reads and writes the field once
+// instead of once per pass. Rows that fit: L <= 8192 at c128, 16384 at c64.
+
+template <typename R>
+constexpr int smem_max_q() {
+  return sizeof(R) == 8 ? 8192 : 16384;
+}
+template <int L>
+constexpr int row_threads() {
+  return L / 16 < 512 ? L / 16 : 512;
+}
+template <int L>
+constexpr int row_padded() {
+  return L + L / 16 + 1;
+}
+
+template <typename R, int L, int RAD, bool INV>
+__device__ __forceinline__ void smem_pass(Cx<R>* F, int NS, const Cx<R>* __restrict__ twN,
+                                          int tws) {
+  constexpr int NT = row_threads<L>();
+  constexpr int NB = L / RAD;
+  static_assert(NB % NT == 0, "butterflies must tile the CTA");
+  constexpr int PER = NB / NT;
+  const int tstep = L / (NS * RAD);
+  Cx<R> v[PER][RAD];
+#pragma unroll
+  for (int p = 0; p < PER; ++p) {
+    const int j = (int)threadIdx.x + p * NT, k = j % NS;
+#pragma unroll
+    for (int r = 0; r < RAD; ++r) v[p][r] = F[pad(j + r * NB)];
+    if (NS > 1) {
+#pragma unroll
+      for (int r = 1; r < RAD; ++r) {
+        const Cx<R> w = ldg(twN + (int64_t)(r * k * tstep) * tws);
+        v[p][r] = INV ? cmulc(v[p][r], w) : cmul(v[p][r], w);
+      }
+    }
+    dft_reg<R, RAD, INV>(v[p]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int p = 0; p < PER; ++p) {
+    const int j = (int)threadIdx.x + p * NT, k = j % NS;
+    const int d0 = (j / NS) * NS * RAD + k;
+#pragma unroll
+    for (int r = 0; r < RAD; ++r) F[pad(d0 + r * NS)] = v[p][bitrev<RAD>(r)];
+  }
+  __syncthreads();
+}
+
+// Unnormalised in-place FFT of the row in F (natural order in and out).
+template <typename R, int L, bool INV>
+__device__ __forceinline__ void row_fft(Cx<R>* F, const Cx<R>* twN, int tws) {
+  constexpr int LG = __builtin_ctz(L), LEAD = LG % 4;
+  int ns = 1;
+  if constexpr (LEAD != 0) {
+    smem_pass<R, L, (1 << LEAD), INV>(F, 1, twN, tws);
+    ns = 1 << LEAD;
+  }
+  for (; ns < L; ns *= 16) smem_pass<R, L, 16, INV>(F, ns, twN, tws);
+}
+
+enum FieldMode { kFirstIfft = 0, kStep = 1, kLastStep = 2 };
+
+// One field row (c, i, pol) per CTA: [rotation, FFT, next phasor,] [IFFT,
+// intensity] -- dbp.py:208, :398, :395 / :399, :396, :193.
+template <typename R, int L>
+__global__ void __launch_bounds__(row_threads<L>()) wide_row_field(const StepArgs<R> s, Cx<R>* rows,
+                                                                  const R* theta, R* Ix, R* Iy,
+                                                                  int step, int mode) {
+  constexpr int NT = row_threads<L>();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Cx<R>* F = reinterpret_cast<Cx<R>*>(smem_raw);
+  const Params<R>& p = s.prm;
+  const int64_t row = blockIdx.x;  // (c * P + i) * 2 + pol
+  const int64_t q = row >> 1;      // (c, i)
+  const int pol = (int)(row & 1), i = (int)(q % s.P);
+  Cx<R>* g = rows + row * L;
+  if (mode == kFirstIfft) {
+    for (int t = threadIdx.x; t < L; t += NT) F[pad(t)] = g[t];
+  } else {
+    // rotation exp(-i theta) of the natural-order time samples
+    const int64_t wv = (s.c0 + q / s.P) / p.nb;
+    const int set = p.n_sets > 1 ? (int)(wv % p.n_sets) : 0;
+    const R sc = p.theta_scale[(int64_t)set * p.n_steps + step];
+    const R* th = theta + q * L;
+    for (int t = threadIdx.x; t < L; t += NT) {
+      R sn, cs;
+      sincos_acc<R>(th[t] * sc, &sn, &cs);
+      F[pad(t)] = cmul(g[t], mk(cs, -sn));
+    }
+  }
+  __syncthreads();
+  if (mode != kFirstIfft) {
+    row_fft<R, L, false>(F, p.twN, s.P);
+    const Cx<R>* ph = p.phasor + ((int64_t)p.ph_index[step + 1] * s.P + i) * (int64_t)L;
+    for (int t = threadIdx.x; t < L; t += NT) F[pad(t)] = cmul(F[pad(t)], ldg(ph + t));
+    __syncthreads();
+  }
+  if (mode == kLastStep) {
+    for (int t = threadIdx.x; t < L; t += NT) g[t] = F[pad(t)];
+    return;
+  }
+  row_fft<R, L, true>(F, p.twN, s.P);
+  R* I = (pol ? Iy : Ix) + q * L;
+  for (int t = threadIdx.x; t < L; t += NT) {
+    const Cx<R> v = F[pad(t)];
+    g[t] = v;
+    I[t] = v.x * v.x + v.y * v.y;
+  }
+}
+
+// Half-length FFT of the packed intensity z[t] = I[2t] + i I[2t+1],
+// I = |x|^2 + |y|^2 (x first, as the reference sums), one (c, i) per CTA.
+template <typename R, int L>
+__global__ void __launch_bounds__(row_threads<L>()) wide_row_rfft(const StepArgs<R> s, const R* Ix,
+                                                                 const R* Iy, Cx<R>* Z) {
+  constexpr int NT = row_threads<L>();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Cx<R>* F = reinterpret_cast<Cx<R>*>(smem_raw);
+  const int64_t q = blockIdx.x;
+  const R* ix = Ix + q * 2 * L;
+  const R* iy = Iy + q * 2 * L;
+  for (int t = threadIdx.x; t < L; t += NT)
+    F[pad(t)] = mk(ix[2 * t] + iy[2 * t], ix[2 * t + 1] + iy[2 * t + 1]);
+  __syncthreads();
+  row_fft<R, L, false>(F, s.prm.twN, 2 * s.P);
+  Cx<R>* z = Z + q * L;
+  for (int t = threadIdx.x; t < L; t += NT) z[t] = F[pad(t)];
+}
+
+// Inverse half-length FFT of the twisted theta_hat, in place (theta packed
+// as reals, dbp.py:196).
+template <typename R, int L>
+__global__ void __launch_bounds__(row_threads<L>()) wide_row_irfft(const StepArgs<R> s, Cx<R>* T) {
+  constexpr int NT = row_threads<L>();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Cx<R>* F = reinterpret_cast<Cx<R>*>(smem_raw);
+  Cx<R>* t_row = T + (int64_t)blockIdx.x * L;
+  for (int t = threadIdx.x; t < L; t += NT) F[pad(t)] = t_row[t];
+  __syncthreads();
+  row_fft<R, L, true>(F, s.prm.twN, 2 * s.P);
+  for (int t = threadIdx.x; t < L; t += NT) t_row[t] = F[pad(t)];
+}
+
+// The steps of one chunk with per-row kernels at subband length Q.
+template <typename R, int Q>
+cudaError_t smem_steps(const StepArgs<R>& s, Cx<R>* cur, R* Ix, R* Iy, Cx<R>* hA, Cx<R>* hB,
+                       cudaStream_t st) {
+  constexpr int H = Q / 2;
+  const Params<R>& prm = s.prm;
+  const int64_t frows = s.nc * s.P * 2, hrows = s.nc * s.P;
+  const size_t fsm = sizeof(Cx<R>) * row_padded<Q>(), hsm = sizeof(Cx<R>) * row_padded<H>();
+  cudaError_t e;
+  auto kf = wide_row_field<R, Q>;
+  auto kh = wide_row_rfft<R, H>;
+  auto ki = wide_row_irfft<R, H>;
+  if ((e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm)) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(kh, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm)) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(ki, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm)) != cudaSuccess)
+    return e;
+  if (prm.n_steps > 0)
+    kf<<<(unsigned)frows, row_threads<Q>(), fsm, st>>>(s, cur, nullptr, Ix, Iy, 0, kFirstIfft);
+  for (int stp = 0; stp < prm.n_steps; ++stp) {
+    kh<<<(unsigned)hrows, row_threads<H>(), hsm, st>>>(s, Ix, Iy, hA);
+    if ((e = mimo_dispatch<R>(s, hA, hB, st)) != cudaSuccess) return e;
+    ki<<<(unsigned)hrows, row_threads<H>(), hsm, st>>>(s, hB);
+    kf<<<(unsigned)frows, row_threads<Q>(), fsm, st>>>(s, cur, reinterpret_cast<const R*>(hB), Ix,
+                                                       Iy, stp,
+                                                       stp + 1 < prm.n_steps ? kStep : kLastStep);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return cudaGetLastError();
+}
+
 // Bytes of device workspace per (waveform, block) of a chunk.
 template <typename R>
 size_t bytes_per_block(int N) {
@@ -425,32 +603,40 @@ cudaError_t run(const Params<R>& prm, int P, int Q, int64_t nclusters, cudaStrea
     if ((e = fft_rows<R, false>(pa, &cur, &alt, kNoHook, kNoHook, st)) != cudaSuccess) break;
     wide_demux<R><<<grid_for(units), kThreads, 0, st>>>(s, cur, alt);
     std::swap(cur, alt);  // cur: subband rows [c][i][pol][Q] (spectra)
-    // ---- steps
-    for (int stp = 0; stp < prm.n_steps; ++stp) {
-      pa.rows = s.nc * P * 2;
-      pa.L = Q;
-      pa.tw_stride = P;
-      pa.inten = reinterpret_cast<R*>(hA);
-      if ((e = fft_rows<R, true>(pa, &cur, &alt, kNoHook, kIntensity, st)) != cudaSuccess) break;
-      // rfft of the intensity: half-length FFT of the packed reals
-      PassArgs<R> ph = pa;
-      ph.rows = s.nc * P;
-      ph.L = H;
-      ph.tw_stride = 2 * P;
-      Cx<R>* hc = hA;
-      Cx<R>* ha = hB;
-      if ((e = fft_rows<R, false>(ph, &hc, &ha, kNoHook, kNoHook, st)) != cudaSuccess) break;
-      if ((e = mimo_dispatch<R>(s, hc, ha, st)) != cudaSuccess) break;
-      std::swap(hc, ha);  // hc: twisted theta_hat
-      if ((e = fft_rows<R, true>(ph, &hc, &ha, kNoHook, kNoHook, st)) != cudaSuccess) break;
-      // rotation fused into the first pass of the forward FFT, the next
-      // phasor into its last
-      pa.theta = reinterpret_cast<const R*>(hc);
-      pa.tscale = prm.theta_scale;
-      pa.step = stp;
-      pa.phasor = prm.phasor;
-      pa.ph_index = prm.ph_index;
-      if ((e = fft_rows<R, false>(pa, &cur, &alt, kRotate, kPhasor, st)) != cudaSuccess) break;
+    // ---- steps: per-row kernels where a row fits one CTA's shared memory
+    if (Q == smem_max_q<R>()) {
+      // intensity of x and y in the idle second field buffer
+      R* Ix = reinterpret_cast<R*>(alt);
+      R* Iy = Ix + (size_t)s.nc * N;
+      // (the wide path starts above the fused kernels' N': 4096 c128, 8192 c64)
+      e = smem_steps<R, smem_max_q<R>()>(s, cur, Ix, Iy, hA, hB, st);
+    } else {
+      for (int stp = 0; stp < prm.n_steps; ++stp) {
+        pa.rows = s.nc * P * 2;
+        pa.L = Q;
+        pa.tw_stride = P;
+        pa.inten = reinterpret_cast<R*>(hA);
+        if ((e = fft_rows<R, true>(pa, &cur, &alt, kNoHook, kIntensity, st)) != cudaSuccess) break;
+        // rfft of the intensity: half-length FFT of the packed reals
+        PassArgs<R> ph = pa;
+        ph.rows = s.nc * P;
+        ph.L = H;
+        ph.tw_stride = 2 * P;
+        Cx<R>* hc = hA;
+        Cx<R>* ha = hB;
+        if ((e = fft_rows<R, false>(ph, &hc, &ha, kNoHook, kNoHook, st)) != cudaSuccess) break;
+        if ((e = mimo_dispatch<R>(s, hc, ha, st)) != cudaSuccess) break;
+        std::swap(hc, ha);  // hc: twisted theta_hat
+        if ((e = fft_rows<R, true>(ph, &hc, &ha, kNoHook, kNoHook, st)) != cudaSuccess) break;
+        // rotation fused into the first pass of the forward FFT, the next
+        // phasor into its last
+        pa.theta = reinterpret_cast<const R*>(hc);
+        pa.tscale = prm.theta_scale;
+        pa.step = stp;
+        pa.phasor = prm.phasor;
+        pa.ph_index = prm.ph_index;
+        if ((e = fft_rows<R, false>(pa, &cur, &alt, kRotate, kPhasor, st)) != cudaSuccess) break;
+      }
     }
     if (e != cudaSuccess) break;
     // ---- merge, IFFT_N, keep
