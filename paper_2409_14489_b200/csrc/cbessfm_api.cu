@@ -851,18 +851,8 @@ cbessfm_status cbessfm_run_dualpol(const cbessfm_plan* cp, const cbessfm_dualpol
   std::vector<std::tuple<int64_t, int64_t, cudaEvent_t>> outs;
   auto after_d2h = [&](int64_t a, int64_t b, cudaEvent_t ev) { outs.emplace_back(a, b, ev); };
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  // c128 output already page-locked and laid out [x | y] (run_dbp's recycled
-  // output buffers): the D2H lands in it directly, no staging copy out
-  bool direct_out = false;
-  if (p->dtype == CBESSFM_C128 && io->out_y == io->out_x + 2 * n) {
-    cudaPointerAttributes pa{};
-    direct_out = cudaPointerGetAttributes(&pa, io->out_x) == cudaSuccess &&
-                 pa.type == cudaMemoryTypeHost;
-    cudaGetLastError();  // a pageable pointer may leave an error behind
-  }
-  if (direct_out) rout = reinterpret_cast<char*>(io->out_x);
-  const cbessfm_status status = host_pipeline(p, rin, rout, n, 1, io->chunks, st, before_h2d,
-                                              direct_out ? nullptr : after_d2h);
+  const cbessfm_status status =
+      host_pipeline(p, rin, rout, n, 1, io->chunks, st, before_h2d, after_d2h);
   // drain the copy-in tasks even on error (they reference this frame)
   before_h2d(0, n);
   if (status != CBESSFM_OK) {

@@ -52,10 +52,7 @@ class _Lease:
             free = _Lease._pool.get(n)
             self.mem = free.pop() if free else None
         if self.mem is None:
-            # page-locked (torch's pinned host allocator): the native c128
-            # path copies the kept samples D2H straight into it
-            t = _torch().empty(2 * n, dtype=_torch().complex128, pin_memory=True)
-            self.mem = t.numpy()
+            self.mem = np.empty(2 * n, dtype=np.complex128)
 
     def __buffer__(self, flags):
         return memoryview(self.mem)
