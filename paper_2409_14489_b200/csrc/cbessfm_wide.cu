@@ -10,8 +10,8 @@
 // rows once (L2-resident for a chunk of blocks), with the elementwise steps
 // fused into the first / last pass where they touch natural-order samples:
 //
-//   window load ............. dbp.py:473-475          wide_window
-//   outer FFT_N + demux ..... dbp.py:387-389          passes + wide_demux (1/P, first phasor)
+//   window load ............. dbp.py:473-475          wide_window (polyphase rows)
+//   outer FFT_N + demux ..... dbp.py:387-389          FFT_Q passes + wide_outer_fwd (radix P, 1/P, first phasor)
 //   per step (dbp.py:394-398):
 //     IFFT_Q, |x|^2+|y|^2 ... dbp.py:396, :193        passes, last one writes I
 //     rfft(I) (half-length FFT of the packed reals)   passes over I viewed as complex
@@ -19,11 +19,11 @@
 //     irfft ................. dbp.py:196               passes -> theta (packed reals)
 //     rotation, FFT_Q ....... dbp.py:208, :398        passes, first one rotates
 //     next phasor ........... dbp.py:395 / :399       last pass multiplies
-//   merge + IFFT_N .......... dbp.py:400-401          wide_merge + passes
+//   merge + IFFT_N .......... dbp.py:400-401          wide_outer_inv (radix P) + IFFT_Q passes
 //   keep .................... dbp.py:476-477          wide_store
 //
-// Twiddles of every length L in {N, Q, Q/2} come from the plan's W_N table
-// (L divides N = P * Q) with stride N / L.
+// Twiddles of every length L in {Q, Q/2} and W_N, W_P come from the plan's
+// W_N table (N = P * Q) with stride N / L.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -140,8 +140,10 @@ struct StepArgs {
   int64_t c0, nc;  // chunk: flattened (waveform, block) indices [c0, c0 + nc)
 };
 
-// Circular window of block b, both polarisations, natural order
-// (dbp.py:473-475): A[c][pol][t] = u[(b keep - half + t) mod n].
+// Circular window of block b, both polarisations, split into its P
+// polyphase components (dbp.py:473-475): A[c][pol][r][t2] = u[(b keep -
+// half + r + P t2) mod n] -- the outer FFT_N is P FFT_Q plus a radix-P stage,
+// as in the fused kernels (N = P Q need not be a power of two).
 template <typename R>
 __global__ void __launch_bounds__(kThreads) wide_window(const StepArgs<R> s, Cx<R>* A) {
   const Params<R>& p = s.prm;
@@ -150,7 +152,8 @@ __global__ void __launch_bounds__(kThreads) wide_window(const StepArgs<R> s, Cx<
        u += (int64_t)gridDim.x * kThreads) {
     const int64_t c = u / (2 * s.N);
     const int pol = (int)((u / s.N) & 1);
-    const int t = (int)(u % s.N);
+    const int rem = (int)(u % s.N);
+    const int t = rem / s.Q + s.P * (rem % s.Q);  // r + P t2
     const int64_t cid = s.c0 + c, wv = cid / p.nb, b = p.b0 + cid % p.nb;
     int64_t start = (b * p.keep - p.half) % p.n;
     if (start < 0) start += p.n;
@@ -163,54 +166,98 @@ __global__ void __launch_bounds__(kThreads) wide_window(const StepArgs<R> s, Cx<
   }
 }
 
-// Subband demux of the FFT_N bins (fftshift / reshape / ifftshift of
-// dbp.py:387-389), x 1/P x first phasor, into rows [c][i][pol][Q].
-template <typename R>
-__global__ void __launch_bounds__(kThreads) wide_demux(const StepArgs<R> s, const Cx<R>* F,
-                                                       Cx<R>* S) {
+// Position of global FFT_N bin g in the subband layout (fftshift / reshape /
+// ifftshift of dbp.py:387-389), as bin_home in the fused kernels.
+__device__ __forceinline__ void wide_bin_home(int g, int P, int Q, int& i, int& m) {
+  const int N = P * Q;
+  int sh = g + N / 2;
+  if (sh >= N) sh -= N;
+  i = sh / Q;
+  m = (sh % Q + Q / 2) % Q;
+}
+
+// Radix-P stage of the outer FFT_N over the polyphase spectra Y_r[k2] (rows
+// [c][pol][r]), x 1/P x first phasor, scattered to the subband rows
+// S[c][i][pol][m] (dbp.py:387-389): the fused kernels' step 3, same order.
+template <typename R, int P>
+__global__ void __launch_bounds__(kThreads) wide_outer_fwd(const StepArgs<R> s, const Cx<R>* Y,
+                                                           Cx<R>* S) {
   const Params<R>& p = s.prm;
-  const int64_t total = s.nc * 2 * s.N;
-  const R invP = (R)1 / (R)s.P;
-  const Cx<R>* ph0 = p.phasor + (int64_t)p.ph_index[0] * s.N;
+  const int Q = s.Q, N = s.N;
+  const int64_t total = s.nc * 2 * Q;
+  const R invP = (R)1 / (R)P;
+  const Cx<R>* ph0 = p.phasor + (int64_t)p.ph_index[0] * N;
+  Cx<R> wP[P];
+#pragma unroll
+  for (int m = 0; m < P; ++m) wP[m] = ldg(p.twN + (int64_t)m * Q);
   for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < total;
        u += (int64_t)gridDim.x * kThreads) {
-    const int m = (int)(u % s.Q);
-    const int pol = (int)((u / s.Q) & 1);
-    const int i = (int)((u / (2 * s.Q)) % s.P);
-    const int64_t c = u / (2 * (int64_t)s.N);
-    int g = i * s.Q + (m + s.Q / 2) % s.Q + s.N / 2;
-    if (g >= s.N) g -= s.N;
-    CB_CHECK(g >= 0 && g < s.N);
-    const Cx<R> v = F[(c * 2 + pol) * s.N + g];
-    S[u] = s.P > 1 ? cmul(scale(v, invP), ldg(ph0 + (int64_t)i * s.Q + m))
-                   : cmul(v, ldg(ph0 + m));
+    const int k2 = (int)(u % Q);
+    const int64_t cp = u / Q;  // c * 2 + pol
+    const int64_t c = cp >> 1;
+    const int pol = (int)(cp & 1);
+    Cx<R> bv[P];
+#pragma unroll
+    for (int r = 0; r < P; ++r) {
+      Cx<R> v = Y[(cp * P + r) * (int64_t)Q + k2];
+      if (r) v = cmul(v, ldg(p.twN + (int64_t)r * k2));
+      bv[r] = v;
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1) {
+      Cx<R> sm = bv[0];
+#pragma unroll
+      for (int r = 1; r < P; ++r) sm = sm + cmul(bv[r], wP[(r * k1) % P]);
+      int i, m;
+      wide_bin_home(Q * k1 + k2, P, Q, i, m);
+      CB_CHECK(i >= 0 && i < P && m >= 0 && m < Q);
+      const Cx<R> w = ldg(ph0 + (int64_t)i * Q + m);
+      S[((c * P + i) * 2 + pol) * (int64_t)Q + m] = P > 1 ? cmul(scale(sm, invP), w) : cmul(sm, w);
+    }
   }
 }
 
-// Merge (dbp.py:399-401): subband rows back to FFT_N bin order (the merge's
-// x N_sb and the outer IFFT's 1/N are carried by the final phasor's 1/Q).
-template <typename R>
-__global__ void __launch_bounds__(kThreads) wide_merge(const StepArgs<R> s, const Cx<R>* S,
-                                                       Cx<R>* F) {
-  const int64_t total = s.nc * 2 * s.N;
+// Merge (dbp.py:399-401): gather the P bins Q k1 + k2 from their subband
+// rows, inverse radix-P stage and W_N^-(n1 k2), polyphase row n1 of the
+// outer IFFT_N (the merge's x N_sb and the outer 1/N are in the final
+// phasor's 1/Q): the fused kernels' step 5, same order.
+template <typename R, int P>
+__global__ void __launch_bounds__(kThreads) wide_outer_inv(const StepArgs<R> s, const Cx<R>* S,
+                                                           Cx<R>* Y) {
+  const Params<R>& p = s.prm;
+  const int Q = s.Q;
+  const int64_t total = s.nc * 2 * Q;
+  Cx<R> wP[P];
+#pragma unroll
+  for (int m = 0; m < P; ++m) wP[m] = ldg(p.twN + (int64_t)m * Q);
   for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < total;
        u += (int64_t)gridDim.x * kThreads) {
-    const int g = (int)(u % s.N);
-    const int pol = (int)((u / s.N) & 1);
-    const int64_t c = u / (2 * (int64_t)s.N);
-    int i, m;
-    int sh = g + s.N / 2;
-    if (sh >= s.N) sh -= s.N;
-    i = sh / s.Q;
-    m = (sh % s.Q + s.Q / 2) % s.Q;
-    CB_CHECK(i >= 0 && i < s.P && m >= 0 && m < s.Q);
-    F[u] = S[((c * s.P + i) * 2 + pol) * s.Q + m];
+    const int k2 = (int)(u % Q);
+    const int64_t cp = u / Q;
+    const int64_t c = cp >> 1;
+    const int pol = (int)(cp & 1);
+    Cx<R> xv[P];
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1) {
+      int i, m;
+      wide_bin_home(Q * k1 + k2, P, Q, i, m);
+      xv[k1] = S[((c * P + i) * 2 + pol) * (int64_t)Q + m];
+    }
+#pragma unroll
+    for (int n1 = 0; n1 < P; ++n1) {
+      Cx<R> sm = xv[0];
+#pragma unroll
+      for (int k1 = 1; k1 < P; ++k1) sm = sm + cmulc(xv[k1], wP[(n1 * k1) % P]);
+      if (n1) sm = cmulc(sm, ldg(p.twN + (int64_t)n1 * k2));
+      Y[(cp * P + n1) * (int64_t)Q + k2] = sm;
+    }
   }
 }
 
-// Keep proc[half : half + span] of every block (dbp.py:476-477).
+// Keep proc[half : half + span] of every block (dbp.py:476-477); sample t
+// of the block is polyphase row t mod P, position t / P.
 template <typename R>
-__global__ void __launch_bounds__(kThreads) wide_store(const StepArgs<R> s, const Cx<R>* F) {
+__global__ void __launch_bounds__(kThreads) wide_store(const StepArgs<R> s, const Cx<R>* Y) {
   const Params<R>& p = s.prm;
   const int64_t total = s.nc * 2 * p.keep;
   for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < total;
@@ -223,7 +270,10 @@ __global__ void __launch_bounds__(kThreads) wide_store(const StepArgs<R> s, cons
     if (t >= p.half + span) continue;
     const int64_t obase = b * p.keep - p.half - p.out_origin;
     CB_CHECK(obase + t >= 0 && (p.out_origin != 0 || obase + t < p.n));
-    p.out[wv * p.out_bstride + pol * p.out_pstride + obase + t] = F[(c * 2 + pol) * s.N + t];
+    const int n1 = (int)(t % s.P);
+    const int64_t t2 = t / s.P;
+    p.out[wv * p.out_bstride + pol * p.out_pstride + obase + t] =
+        Y[((c * 2 + pol) * s.P + n1) * (int64_t)s.Q + t2];
   }
 }
 
@@ -373,6 +423,33 @@ cudaError_t mimo_dispatch(const StepArgs<R>& s, const Cx<R>* Z, Cx<R>* T, cudaSt
     case 7: return mimo_launch<R, 7>(s, Z, T, st);
     case 8: return mimo_launch<R, 8>(s, Z, T, st);
     case 9: return mimo_launch<R, 9>(s, Z, T, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <typename R, int P>
+cudaError_t outer_launch(const StepArgs<R>& s, const Cx<R>* a, Cx<R>* b, bool fwd, cudaStream_t st) {
+  const int64_t units = s.nc * 2 * s.Q;
+  if (fwd)
+    wide_outer_fwd<R, P><<<grid_for(units), kThreads, 0, st>>>(s, a, b);
+  else
+    wide_outer_inv<R, P><<<grid_for(units), kThreads, 0, st>>>(s, a, b);
+  return cudaGetLastError();
+}
+
+template <typename R>
+cudaError_t outer_dispatch(const StepArgs<R>& s, const Cx<R>* a, Cx<R>* b, bool fwd,
+                           cudaStream_t st) {
+  switch (s.P) {
+    case 1: return outer_launch<R, 1>(s, a, b, fwd, st);
+    case 2: return outer_launch<R, 2>(s, a, b, fwd, st);
+    case 3: return outer_launch<R, 3>(s, a, b, fwd, st);
+    case 4: return outer_launch<R, 4>(s, a, b, fwd, st);
+    case 5: return outer_launch<R, 5>(s, a, b, fwd, st);
+    case 6: return outer_launch<R, 6>(s, a, b, fwd, st);
+    case 7: return outer_launch<R, 7>(s, a, b, fwd, st);
+    case 8: return outer_launch<R, 8>(s, a, b, fwd, st);
+    case 9: return outer_launch<R, 9>(s, a, b, fwd, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -593,15 +670,16 @@ cudaError_t run(const Params<R>& prm, int P, int Q, int64_t nclusters, cudaStrea
     pa.n_steps = prm.n_steps;
     pa.rows_per_wave = prm.nb * P;
     pa.q0 = c0 * P;
-    // ---- window, FFT_N per polarisation, demux (+ 1/P, first phasor)
+    // ---- window (polyphase rows), FFT_Q of each, radix-P stage + demux
+    //      (+ 1/P, first phasor)
     wide_window<R><<<grid_for(units), kThreads, 0, st>>>(s, bufA);
     Cx<R>* cur = bufA;
     Cx<R>* alt = bufB;
-    pa.rows = s.nc * 2;
-    pa.L = N;
-    pa.tw_stride = 1;
+    pa.rows = s.nc * 2 * P;
+    pa.L = Q;
+    pa.tw_stride = P;
     if ((e = fft_rows<R, false>(pa, &cur, &alt, kNoHook, kNoHook, st)) != cudaSuccess) break;
-    wide_demux<R><<<grid_for(units), kThreads, 0, st>>>(s, cur, alt);
+    if ((e = outer_dispatch<R>(s, cur, alt, true, st)) != cudaSuccess) break;
     std::swap(cur, alt);  // cur: subband rows [c][i][pol][Q] (spectra)
     // ---- steps: per-row kernels where a row fits one CTA's shared memory
     if (Q == smem_max_q<R>()) {
@@ -639,12 +717,12 @@ cudaError_t run(const Params<R>& prm, int P, int Q, int64_t nclusters, cudaStrea
       }
     }
     if (e != cudaSuccess) break;
-    // ---- merge, IFFT_N, keep
-    wide_merge<R><<<grid_for(units), kThreads, 0, st>>>(s, cur, alt);
+    // ---- merge + inverse radix-P stage, IFFT_Q of each polyphase row, keep
+    if ((e = outer_dispatch<R>(s, cur, alt, false, st)) != cudaSuccess) break;
     std::swap(cur, alt);
-    pa.rows = s.nc * 2;
-    pa.L = N;
-    pa.tw_stride = 1;
+    pa.rows = s.nc * 2 * P;
+    pa.L = Q;
+    pa.tw_stride = P;
     if ((e = fft_rows<R, true>(pa, &cur, &alt, kNoHook, kNoHook, st)) != cudaSuccess) break;
     wide_store<R><<<grid_for(s.nc * 2 * prm.keep), kThreads, 0, st>>>(s, cur);
     e = cudaGetLastError();

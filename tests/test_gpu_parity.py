@@ -463,3 +463,36 @@ def test_wide_path_launch_forms(cuda, name, dtype):
     for c, o in zip(sets, outs):
         ref = orc.run_cb_blocks(f0, g.cfg, rate, c)
         assert rel_rms(np.vstack([o.x, o.y]), ref) < tol
+
+
+@pytest.mark.parametrize("n_sb,n_steps,q", [(1, 0, 8192), (3, 2, 8192), (9, 1, 8192),
+                                             (2, 2, 32768)])
+def test_wide_path_shapes_against_oracle(cuda, n_sb, n_steps, q):
+    # wide-subband shapes the goldens do not cover: zero steps (the EDC-like
+    # linear pass), odd N_sb, the 9-CTA-wide MIMO, and N' = 32768 (the pass-
+    # per-launch form at both dtypes); coefficients from the GPU builder
+    import torch
+    from paper_2409_14489_b200.coefficients import make_dbp_coefficient_set
+    rate = 512e9
+    link = pb.LinkConfig(num_spans=4, span_length_km=80.0, alpha_db_per_km=0.2,
+                         dispersion_d_ps_nm_km=17.0, gamma_w_km=1.3)
+    N = n_sb * q
+    cfg = pb.DbpConfig(link=link, variant="CB_ESSFM", n_steps=n_steps, n_subbands=n_sb,
+                       splitting_ratio=0.5, block_size=N, overlap=2 * n_sb * 180,
+                       oversampling=1.6)
+    coeffs = None
+    if n_steps:
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            coeffs = make_dbp_coefficient_set(cfg, rate, 1e-3, memory=15)
+    field = gaussian_wdm(3 * N + 1000, rate, seed=5 + n_sb)
+    ref = orc.run_cb_blocks(field, cfg, rate, coeffs)
+    for dtype, ct in (("c128", torch.complex128), ("c64", torch.complex64)):
+        assert pb.get_plan(cfg, rate, coeffs, dtype).info().kernel_name.startswith(
+            "cbessfm_wide") or (dtype == "c64" and q <= 8192)
+        x = torch.from_numpy(field[None]).to(cuda).to(ct)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", RuntimeWarning)
+            out = pb.run_dbp_tensor(x, cfg, coeffs, rate)
+        got = out[0].to(torch.complex128).cpu().numpy()
+        assert rel_rms(got, ref) < TOL[dtype], (dtype, rel_rms(got, ref))
