@@ -217,3 +217,23 @@ def test_single_block_covering_the_waveform(cuda):
     field = np.vstack([g.wave.x, g.wave.y])[:, :6144]
     ref = orc.run_cb_blocks(field, cfg, g.wave.sample_rate, g.coeffs)
     assert rel_rms(_gpu(field, cfg, g.coeffs, g.wave.sample_rate, "c128")[0], ref) < 1e-12
+
+
+@pytest.mark.parametrize("n_sb", range(1, 10))
+def test_every_compiled_shape(cuda, n_sb):
+    # every (N_sb, N') the build dispatches -- the fused kernels' 2 x 9 x 6
+    # instantiations (N' = 256 .. 4096 c128, .. 8192 c64) and the wide path
+    # above them (N' = 8192 c128) -- one step each, against the oracle
+    rate = 64e9
+    for q in (256, 512, 1024, 2048, 4096, 8192):
+        n = 2 * n_sb * q + 777                   # partial last block, wrap-around
+        field = gaussian_wdm(n, rate, n_channels=1, spacing=0.0, baud=16e9,
+                             dbm_per_channel=3.0, seed=n_sb + q)
+        cfg = pb.DbpConfig(link=_link(4), variant="CB_ESSFM", n_steps=1, n_subbands=n_sb,
+                           splitting_ratio=0.5, block_size=n_sb * q,
+                           overlap=2 * n_sb * (q // 8), oversampling=2.0)
+        c = _random_coeffs(n_sb, 1, seed=q + 10 * n_sb)
+        ref = orc.run_cb_blocks(field, cfg, rate, c)
+        for dtype in ("c128", "c64"):
+            e = rel_rms(_gpu(field, cfg, c, rate, dtype)[0], ref)
+            assert e < TOL[dtype], (n_sb, q, dtype, e)
