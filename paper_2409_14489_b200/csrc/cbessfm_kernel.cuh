@@ -290,8 +290,43 @@ __device__ __forceinline__ Cx<R> tw16(Cx<R> d, int e16) {
   }
 }
 
+// Radix-4 butterfly on a[0..3] (forward: W_4 = -i), outputs in natural order.
+template <typename R, bool INV>
+__device__ __forceinline__ void dft4_nat(const Cx<R>& a0, const Cx<R>& a1, const Cx<R>& a2,
+                                         const Cx<R>& a3, Cx<R>* y) {
+  const Cx<R> t0 = a0 + a2, t1 = a0 - a2, t2 = a1 + a3, t3 = a1 - a3;
+  y[0] = t0 + t2;
+  y[2] = t0 - t2;
+  y[1] = INV ? mk(t1.x - t3.y, t1.y + t3.x) : mk(t1.x + t3.y, t1.y - t3.x);
+  y[3] = INV ? mk(t1.x + t3.y, t1.y - t3.x) : mk(t1.x - t3.y, t1.y + t3.x);
+}
+
+#ifndef CB_DFT16_4X4  // FP64 radix-16 as 4 x 4 (160 FP64 instructions instead of 168)
+#define CB_DFT16_4X4 1
+#endif
+
 template <typename R, int RAD, bool INV>
 __device__ __forceinline__ void dft_reg(Cx<R>* v) {
+  if constexpr (CB_DFT16_4X4 && RAD == 16 && sizeof(R) == 8) {
+    // X[k1 + 4 k2] = sum_n1 W_4^(n1 k2) W_16^(n1 k1) sum_n2 x[n1 + 4 n2] W_4^(n2 k1);
+    // natural output k goes to v[bitrev(k)] like the radix-2 form below
+    Cx<R> b[4][4];
+#pragma unroll
+    for (int n1 = 0; n1 < 4; ++n1) {
+      dft4_nat<R, INV>(v[n1], v[n1 + 4], v[n1 + 8], v[n1 + 12], b[n1]);
+#pragma unroll
+      for (int k1 = 1; k1 < 4; ++k1)
+        if (n1) b[n1][k1] = tw16<R, INV>(b[n1][k1], n1 * k1);
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      Cx<R> y[4];
+      dft4_nat<R, INV>(b[0][k1], b[1][k1], b[2][k1], b[3][k1], y);
+#pragma unroll
+      for (int k2 = 0; k2 < 4; ++k2) v[bitrev<16>(k1 + 4 * k2)] = y[k2];
+    }
+    return;
+  }
 #pragma unroll
   for (int span = RAD / 2; span >= 1; span >>= 1) {
 #pragma unroll
