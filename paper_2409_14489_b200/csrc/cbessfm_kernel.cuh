@@ -305,23 +305,64 @@ __device__ __forceinline__ void dft4_nat(const Cx<R>& a0, const Cx<R>& a1, const
 #define CB_DFT16_4X4 1
 #endif
 
+// d * W_16^e / sqrt(1/2) for e = 2, 6 (the sqrt(1/2) is applied by the
+// consumer's fused multiply-adds)
+template <typename R, bool INV>
+__device__ __forceinline__ Cx<R> tw16_unscaled(Cx<R> d, int e) {
+  if (e == 2) return INV ? mk(d.x - d.y, d.x + d.y) : mk(d.x + d.y, d.y - d.x);
+  return INV ? mk(-(d.x + d.y), d.x - d.y) : mk(d.y - d.x, -(d.x + d.y));  // e == 6
+}
+
+// Radix-4 butterfly whose input a2 (SC == 2) or inputs a1 and a3 (SC == 13)
+// still carry a missing factor sqrt(1/2): the products fold into the
+// butterfly's additions as fused multiply-adds (FP64 4 x 4 radix-16).
+template <typename R, bool INV, int SC>
+__device__ __forceinline__ void dft4_sc(const Cx<R>& a0, const Cx<R>& a1, const Cx<R>& a2,
+                                        const Cx<R>& a3, Cx<R>* y) {
+  constexpr R h = (R)0.70710678118654752440;
+  if constexpr (SC == 2) {
+    const Cx<R> t0 = mk(fma(h, a2.x, a0.x), fma(h, a2.y, a0.y));
+    const Cx<R> t1 = mk(fma(-h, a2.x, a0.x), fma(-h, a2.y, a0.y));
+    const Cx<R> t2 = a1 + a3, t3 = a1 - a3;
+    y[0] = t0 + t2;
+    y[2] = t0 - t2;
+    y[1] = INV ? mk(t1.x - t3.y, t1.y + t3.x) : mk(t1.x + t3.y, t1.y - t3.x);
+    y[3] = INV ? mk(t1.x + t3.y, t1.y - t3.x) : mk(t1.x - t3.y, t1.y + t3.x);
+  } else {  // SC == 13: t2 = h p, t3 = h m
+    const Cx<R> t0 = a0 + a2, t1 = a0 - a2;
+    const Cx<R> p = a1 + a3, m = a1 - a3;
+    y[0] = mk(fma(h, p.x, t0.x), fma(h, p.y, t0.y));
+    y[2] = mk(fma(-h, p.x, t0.x), fma(-h, p.y, t0.y));
+    y[1] = INV ? mk(fma(-h, m.y, t1.x), fma(h, m.x, t1.y)) : mk(fma(h, m.y, t1.x), fma(-h, m.x, t1.y));
+    y[3] = INV ? mk(fma(h, m.y, t1.x), fma(-h, m.x, t1.y)) : mk(fma(-h, m.y, t1.x), fma(h, m.x, t1.y));
+  }
+}
+
 template <typename R, int RAD, bool INV>
 __device__ __forceinline__ void dft_reg(Cx<R>* v) {
   if constexpr (CB_DFT16_4X4 && RAD == 16 && sizeof(R) == 8) {
     // X[k1 + 4 k2] = sum_n1 W_4^(n1 k2) W_16^(n1 k1) sum_n2 x[n1 + 4 n2] W_4^(n2 k1);
-    // natural output k goes to v[bitrev(k)] like the radix-2 form below
+    // natural output k goes to v[bitrev(k)] like the radix-2 form below.
+    // The four sqrt(1/2)-type twiddles (n1 k1 = 2, 6) are left unscaled and
+    // folded into the second radix-4 stage (dft4_sc): 152 FP64 instructions.
     Cx<R> b[4][4];
 #pragma unroll
     for (int n1 = 0; n1 < 4; ++n1) {
       dft4_nat<R, INV>(v[n1], v[n1 + 4], v[n1 + 8], v[n1 + 12], b[n1]);
 #pragma unroll
-      for (int k1 = 1; k1 < 4; ++k1)
-        if (n1) b[n1][k1] = tw16<R, INV>(b[n1][k1], n1 * k1);
+      for (int k1 = 1; k1 < 4; ++k1) {
+        if (!n1) continue;
+        const int e = n1 * k1;
+        b[n1][k1] = (e == 2 || e == 6) ? tw16_unscaled<R, INV>(b[n1][k1], e)
+                                       : tw16<R, INV>(b[n1][k1], e);
+      }
     }
 #pragma unroll
     for (int k1 = 0; k1 < 4; ++k1) {
       Cx<R> y[4];
-      dft4_nat<R, INV>(b[0][k1], b[1][k1], b[2][k1], b[3][k1], y);
+      if (k1 == 0) dft4_nat<R, INV>(b[0][0], b[1][0], b[2][0], b[3][0], y);
+      else if (k1 == 2) dft4_sc<R, INV, 13>(b[0][2], b[1][2], b[2][2], b[3][2], y);
+      else dft4_sc<R, INV, 2>(b[0][k1], b[1][k1], b[2][k1], b[3][k1], y);
 #pragma unroll
       for (int k2 = 0; k2 < 4; ++k2) v[bitrev<16>(k1 + 4 * k2)] = y[k2];
     }
