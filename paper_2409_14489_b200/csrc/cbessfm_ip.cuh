@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(256, 2) cbessfm_ip_kernel(const Params<R> prm)
           Cx<R> acc = mk((R)0, (R)0);
 #pragma unroll
           for (int l = 0; l < P; ++l)
-            acc = acc + (l >= i ? cmul(sv[l - i], iv[l]) : cmul(conj(sv[i - l]), iv[l]));
+            acc = l >= i ? cmac(acc, sv[l - i], iv[l]) : cmacc(acc, sv[i - l], iv[l]);
           push(cluster_addr(ts_local + (uint32_t)(pad(k) * sizeof(Cx<R>)), i), acc,
                cluster_addr(bar_t, i));
         }

@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kThreads) wide_mimo(const StepArgs<R> s, const
         Cx<R> acc = mk((R)0, (R)0);
 #pragma unroll
         for (int l = 0; l < P; ++l)
-          acc = acc + (l >= i ? cmul(sv[l - i], iv[l]) : cmul(conj(sv[i - l]), iv[l]));
+          acc = l >= i ? cmac(acc, sv[l - i], iv[l]) : cmacc(acc, sv[i - l], iv[l]);
         (half ? tb : ta)[i] = acc;
       }
     }
