@@ -111,6 +111,12 @@ struct cbessfm_plan {
   void* twN = nullptr;     // [P*Q]
   void* twp = nullptr;     // per-pass twiddle rows
   long long* dbg = nullptr;  // phase clocks (CB_PHASE_PROFILE builds)
+  // block counters of persistent cluster-kernel launches: each launch takes
+  // the next slot of the ring (zeroed on its stream), so launches in flight
+  // on different streams do not share one
+  static constexpr int kWorkSlots = 64;
+  unsigned long long* work = nullptr;
+  mutable std::atomic<unsigned> work_next{0};
   // host-buffer pipeline (cbessfm_run_host): streams created on first use
   std::mutex host_mu;
   std::vector<cudaStream_t> host_streams;  // [0] copy in, [1] copy out, [2..] compute
@@ -326,6 +332,9 @@ cbessfm_status upload_all(cbessfm_plan* p, const cbessfm_desc* d) {
       p->Q <= max_q(p->dtype) ? pass_tables(p->Q, tq, (int)sizeof(R)) : std::vector<double>(2, 0.0);
   if ((e = upload_complex<R>(tp.data(), tp.size() / 2, &p->twp, true)) != cudaSuccess)
     return cuda_fail(e, "upload pass twiddles");
+  if ((e = cudaMalloc((void**)&p->work, sizeof(unsigned long long) * cbessfm_plan::kWorkSlots)) !=
+      cudaSuccess)
+    return cuda_fail(e, "alloc block counters");
 #ifdef CB_PHASE_PROFILE
   if ((e = cudaMalloc((void**)&p->dbg, kDbgSlots * sizeof(long long))) != cudaSuccess)
     return cuda_fail(e, "alloc phase clocks");
@@ -362,6 +371,7 @@ void free_plan(cbessfm_plan* p) {
   cudaFree(p->twN);
   cudaFree(p->twp);
   cudaFree(p->dbg);
+  cudaFree(p->work);
   delete p;
 }
 
@@ -440,6 +450,8 @@ cbessfm::Params<R> make_params(const cbessfm_plan* p, const cbessfm_io* io) {
   prm.n_steps = p->n_steps;
   prm.n_sets = p->n_sets;
   prm.cid0 = 0;
+  prm.work = p->work ? p->work + p->work_next.fetch_add(1) % cbessfm_plan::kWorkSlots : nullptr;
+  prm.total = 0;
   prm.dbg = p->dbg;
   return prm;
 }

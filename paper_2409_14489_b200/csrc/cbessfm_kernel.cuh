@@ -1531,6 +1531,10 @@ struct Params {
   const Cx<R>* twp;        // per-pass rows, layout twp_base()
   int n_steps;
   int64_t cid0;            // first cluster index of this launch chunk
+  // persistent launches of the cluster kernel (null: one block per cluster):
+  // each cluster claims blocks cid0 + atomicAdd(work, 1) until `total`
+  unsigned long long* work;
+  int64_t total;
   int kernel_pref;         // 0: choose by grid size, 1: cluster kernel (several
                            // launches in flight, cbessfm_run_host)
   long long* dbg;          // phase clocks of CTA 0 (CB_PHASE_PROFILE builds only)
@@ -1672,313 +1676,356 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
   }
   const int tid = threadIdx.x;
   const int rank = (P > 1) ? (int)(blockIdx.x % P) : 0;
-  const int64_t cid = prm.cid0 + blockIdx.x / P;
-  const int64_t wv = cid / prm.nb;
-  const int64_t b = prm.b0 + cid % prm.nb;
-  const int64_t n = prm.n;
-  const int64_t cset = prm.n_sets > 1 ? wv % prm.n_sets : 0;
-  const Cx<R>* __restrict__ mimo = prm.mimo + cset * (int64_t)P * (H + 1);
-  const R* __restrict__ theta_scale = prm.theta_scale + cset * prm.n_steps;
-
-  const Cx<R>* __restrict__ twQ = prm.twQ;
-  const Cx<R>* __restrict__ twN = prm.twN;
-  const Cx<R>* __restrict__ twpT = prm.twp + twp_base(Q, FI);  // field IFFT / outer
-  const Cx<R>* __restrict__ twpF = prm.twp + twp_base(Q, FF);  // in-step field FFT
-  const Cx<R>* __restrict__ twpH = prm.twp + twp_base(Q, HS);  // half-length FFTs
-
-  CB_MARK(0);
-  CB_TIMELINE(0);
-  // ---- 1. load the polyphase component u[rank + P*t2] of the circular
-  //         window starting at (b*keep - half) mod n (dbp.py:473-475)
-  {
-    int64_t start = (b * prm.keep - prm.half) % n;
-    if (start < 0) start += n;
-    start -= prm.in_origin;
-    if (start < 0) start += n;
-    const Cx<R>* src = prm.in + wv * prm.in_bstride;
-    for (int t2 = tid; t2 < Q; t2 += NT) {
-      int64_t idx = start + rank + (int64_t)P * t2;
-      if (idx >= n) idx -= n;
-      CB_CHECK(idx >= 0 && idx < n);
-      F[pad(t2)] = src[idx];
-      F[SF + pad(t2)] = src[prm.in_pstride + idx];
-    }
-  }
-  __syncthreads();
-  if constexpr (TMON) asm volatile("tcgen05.fence::after_thread_sync;");
-
-  const size_t ph_tab = (size_t)P * Q;
-  CB_MARK(1);
-
-  // ---- 2. outer transform, polyphase part: FFT_Q of both polarisations.
-  //         For P == 1 the subband layout is the natural FFT order
-  //         (bin_home is the identity) and the first phasor is fused in.
-  if constexpr (P == 1) {
-    PhasorHook<R> ph0;
-    ph0.ph = prm.phasor + (size_t)prm.ph_index[0] * ph_tab;
-    fft2<R, Q, NT, FI, false, NoHook, PhasorHook<R>>(F, twpT, &s_zero, NoHook(), ph0);
-  } else {
-    fft2<R, Q, NT, FI, false>(F, twpT, &s_zero);
-    // ---- 3. cross-subband radix-P stage over DSMEM: CTA c produces bins
-    //         Q*k1 + k2 for k2 in its slice and every k1, and writes each to
-    //         the CTA that owns it in the fftshift'd subband layout. Row 0's
-    //         results are staged in the owner's idle IS/RB region and row 1's
-    //         land in the owner's row 0 once every CTA has read it, so no CTA
-    //         overwrites fields another CTA still reads (3 cluster barriers).
-    //         The polarisation rows come out swapped; everything in the step
-    //         loop is symmetric in x and y, and step 5 swaps them back.
-    cg::cluster_group cluster = cg::this_cluster();
-    const int lo = (rank * Q) / P, hi = ((rank + 1) * Q) / P;
-    const R invP = (R)1 / (R)P;
-    const Cx<R>* ph0 = prm.phasor + (size_t)prm.ph_index[0] * ph_tab;
-    Cx<R>* S = IS;  // staging: padded_len(Q) entries fit in IS + RB
-    cluster.sync();
-    for (int pol = 0; pol < 2; ++pol) {
-      for (int k2 = lo + tid; k2 < hi; k2 += NT) {
-        Cx<R> bv[P];
-#pragma unroll
-        for (int r = 0; r < P; ++r) {
-          const Cx<R>* rf = cluster.map_shared_rank(F, r);
-          Cx<R> v = rf[pol * SF + pad(k2)];
-          if (r) v = cmul(v, ldg(twN + r * k2));
-          bv[r] = v;
-        }
-#pragma unroll
-        for (int k1 = 0; k1 < P; ++k1) {
-          Cx<R> s = bv[0];
-#pragma unroll
-          for (int r = 1; r < P; ++r) s = s + cmul(bv[r], ldg(twN + ((r * k1) % P) * Q));
-          int i, m;
-          bin_home<P, Q>(Q * k1 + k2, i, m);
-          const Cx<R> w = ldg(ph0 + (size_t)i * Q + m);
-          // row 0 results go to the staging area, row 1 results into the
-          // owner's row 0 (consumed by then): the rows come out swapped
-          Cx<R>* dst = cluster.map_shared_rank(pol ? F : S, i);
-          dst[pad(m)] = cmul(scale(s, invP), w);
-        }
-      }
-      cluster.sync();
-    }
-    // every remote read of row 1 is done: move the staged row-0 results in
-    for (int t = tid; t < Q; t += NT) F[SF + pad(t)] = S[pad(t)];
-    __syncthreads();
-  }
-
-  CB_MARK(2);
-  const Cx<R>* ph_rank = prm.phasor + (size_t)rank * Q;  // this CTA's subband rows
-  R* Ireal = reinterpret_cast<R*>(IS);
-  const R* Treal = reinterpret_cast<const R*>(TS);
-
-  // ---- 4. nonlinear steps (dbp.py:394-398). The subband IFFT
-  //         (normalisation folded into the phasor) also writes, in its last
-  //         pass, I = |x|^2 + |y|^2 packed as z[t] = I[2t] + i I[2t+1]. The
-  //         first step's IFFT runs here; later steps' IFFTs start inside
-  //         the previous step's fft2_boundary.
-  IntensityHook<R> ih;
-  ih.I = Ireal;
-  if (prm.n_steps > 0)
-    fft2<R, Q, NT, FI, true, NoHook, IntensityHook<R>>(F, twpT, &s_zero, NoHook(), ih);
-  CB_MARK(3);
-  constexpr int KU = (H / 2 + 1 + NT - 1) / NT;  // untangle/twist bins per thread
-  for (int st = 0; st < prm.n_steps; ++st) {
-    // per-step scalars issued at the top of the step: their L2 latency
-    // overlaps the intensity transforms instead of stalling the rotation
-    // FFT and the boundary pass
-    const R tsc_st = theta_scale[st];
-    const int phi_next = prm.ph_index[st + 1];  // n_steps + 1 entries
-    // W_Q^k of this thread's untangle/twist bins, issued before the FFT so
-    // the L2 latency hides behind it (the same k serve both)
-    Cx<R> twk[KU];
-#pragma unroll
-    for (int u = 0; u < KU; ++u) {
-      const int k = tid + u * NT;
-      twk[u] = (k <= H / 2) ? ldg(twQ + k) : mk((R)1, (R)0);
-    }
-    fft1<R, Q, H, NT, false, HS>(IS, twpH, &s_zero);
-    CB_MARK(8 + 8 * st + 0);
-
-    // r2c untangle: I_hat[k], k = 0..H (numpy rfft, dbp.py:194). For P > 1
-    // each bin goes straight from registers to the CTA whose MIMO slice
-    // holds it (st.async into its RB, completing on its mbarrier); for
-    // P == 1 it is written back in place.
+  // Persistent launches (prm.work set): the grid holds about as many
+  // clusters as fit the GPU at once and each claims block after block from
+  // a launch-wide counter -- rank 0 claims, the others read its slot over
+  // DSMEM. The TMEM twiddle rows are filled once per CTA instead of once per
+  // block, and no cluster waits on the scheduler between blocks. Clusters
+  // the GPU starts late find the counter spent and exit.
+  __shared__ long long s_cid[3];  // [it & 1]: claimed by rank 0, [2]: this CTA's block
+  const bool persist = prm.work != nullptr;
+  if (persist) {
+    if (rank == 0 && tid == 0) s_cid[0] = (long long)atomicAdd(prm.work, 1ull);
     if constexpr (P > 1) {
+      cg::this_cluster().sync();
+    } else {
+      __syncthreads();
+    }
+  }
+  for (int it = 0;; ++it) {
+    int64_t cid;
+    if (persist) {
       if (tid == 0) {
-        const int len = mimo_lo(rank + 1, P, H) - mimo_lo(rank, P, H);
-        mbar_expect(&s_bar[0], (uint32_t)(P * len * sizeof(Cx<R>)));
-        mbar_expect(&s_bar[1], (uint32_t)((H + 1) * sizeof(Cx<R>)));
-      }
-    }
-    auto emit = [&](int k, Cx<R> v) {
-      if constexpr (P > 1) {
-        int c = (k * P) / (H + 1);
-        if (mimo_lo(c + 1, P, H) <= k) ++c;
-        const uint32_t dst = cluster_addr(smem_addr(RB + rank * SLM + (k - mimo_lo(c, P, H))), c);
-        push(dst, v, cluster_addr(smem_addr(&s_bar[0]), c));
-      } else {
-        IS[pad(k)] = v;
-      }
-    };
-#pragma unroll
-    for (int u = 0; u < KU; ++u) {
-      const int k = tid + u * NT;
-      if (k > H / 2) break;
-      if (k == 0) {
-        const Cx<R> z = IS[pad(0)];
-        emit(0, mk(z.x + z.y, (R)0));
-        emit(H, mk(z.x - z.y, (R)0));
-      } else {
-        const Cx<R> a = IS[pad(k)];
-        const Cx<R> bq = conj(IS[pad(H - k)]);
-        const Cx<R> e = scale(a + bq, (R)0.5);
-        const Cx<R> dd = a - bq;                           // 2i * O[k]
-        const Cx<R> o = mk(dd.y * (R)0.5, -dd.x * (R)0.5); // O[k]
-        const Cx<R> wo = cmul(o, twk[u]);
-        emit(k, e + wo);
-        if (k != H - k) emit(H - k, conj(e - wo));
-      }
-    }
-
-    CB_MARK(8 + 8 * st + 1);
-    // MIMO coupling (dbp.py:195): theta_hat_i[k] = sum_l T[i,l,k] I_hat_l[k]
-    if constexpr (P > 1) {
-      const int lo = mimo_lo(rank, P, H), hi = mimo_lo(rank + 1, P, H);
-      const uint32_t ts_local = smem_addr(TS);
-      const uint32_t bar_t = smem_addr(&s_bar[1]);
-      for (int k = lo + tid; k < hi; k += NT) {
-        Cx<R> sv[P];
-#pragma unroll
-        for (int l = 0; l < P; ++l) sv[l] = ldg_na(mimo + (size_t)l * (H + 1) + k);
-        mbar_wait(&s_bar[0], st & 1);
-        Cx<R> iv[P];
-#pragma unroll
-        for (int l = 0; l < P; ++l) iv[l] = RB[l * SLM + (k - lo)];
-#pragma unroll
-        for (int i = 0; i < P; ++i) {
-          Cx<R> acc = mk((R)0, (R)0);
-#pragma unroll
-          for (int l = 0; l < P; ++l) {
-            acc = l >= i ? cmac(acc, sv[l - i], iv[l]) : cmacc(acc, sv[i - l], iv[l]);
-          }
-          push(cluster_addr(ts_local + (uint32_t)(pad(k) * sizeof(Cx<R>)), i), acc,
-               cluster_addr(bar_t, i));
+        long long c = s_cid[it & 1];
+        if constexpr (P > 1) {
+          if (rank != 0) c = *cg::this_cluster().map_shared_rank(&s_cid[it & 1], 0);
         }
+        s_cid[2] = c;
       }
-      CB_MARK(8 + 8 * st + 2);
-      mbar_wait(&s_bar[1], st & 1);
+      __syncthreads();
+      cid = s_cid[2];
+      if (cid >= prm.total) break;
+      // claim the next block now; the other CTAs read it after this block's
+      // last cluster barrier (step 5), which orders the store before them
+      if (rank == 0 && tid == 0) s_cid[(it + 1) & 1] = (long long)atomicAdd(prm.work, 1ull);
+      cid += prm.cid0;
     } else {
-      __syncthreads();
-      for (int k = tid; k <= H; k += NT) TS[pad(k)] = cmul(ldg(mimo + k), IS[pad(k)]);
-      __syncthreads();
+      if (it) break;
+      cid = prm.cid0 + blockIdx.x / P;
     }
+    // mbarrier phase parity continues across the blocks of a CTA
+    const int ph0 = (int)(((int64_t)it * prm.n_steps) & 1);
+    const int64_t wv = cid / prm.nb;
+    const int64_t b = prm.b0 + cid % prm.nb;
+    const int64_t n = prm.n;
+    const int64_t cset = prm.n_sets > 1 ? wv % prm.n_sets : 0;
+    const Cx<R>* __restrict__ mimo = prm.mimo + cset * (int64_t)P * (H + 1);
+    const R* __restrict__ theta_scale = prm.theta_scale + cset * prm.n_steps;
 
-    CB_MARK(8 + 8 * st + 3);
-    // c2r pre-twist in place (numpy irfft ignores Im of bins 0 and H)
-#pragma unroll
-    for (int u = 0; u < KU; ++u) {
-      const int k = tid + u * NT;
-      if (k > H / 2) break;
-      if (k == 0) {
-        const R x0 = TS[pad(0)].x, xh = TS[pad(H)].x;
-        TS[pad(0)] = mk(x0 + xh, x0 - xh);
-      } else {
-        const Cx<R> a = TS[pad(k)];                 // X[k]
-        const Cx<R> c = conj(TS[pad(H - k)]);       // X[k + H]
-        const Cx<R> wk = twk[u];                    // W^k
-        const Cx<R> s = a + c;
-        const Cx<R> dd = cmulc(a - c, wk);          // W^-k (a - c)
-        TS[pad(k)] = mk(s.x - dd.y, s.y + dd.x);    // s + i dd
-        if (k != H - k) {
-          // Z[H-k] = (X[H-k] + X[Q-k]) + i W^-(H-k) (X[H-k] - X[Q-k])
-          const Cx<R> a2 = conj(c);                 // X[H-k]
-          const Cx<R> c2 = conj(a);                 // X[Q-k]
-          const Cx<R> s2 = a2 + c2;
-          const Cx<R> w2 = mk(-wk.x, wk.y);         // W^(H-k) = -conj(W^k)
-          const Cx<R> d2 = cmulc(a2 - c2, w2);
-          TS[pad(H - k)] = mk(s2.x - d2.y, s2.y + d2.x);
-        }
+    const Cx<R>* __restrict__ twQ = prm.twQ;
+    const Cx<R>* __restrict__ twN = prm.twN;
+    const Cx<R>* __restrict__ twpT = prm.twp + twp_base(Q, FI);  // field IFFT / outer
+    const Cx<R>* __restrict__ twpF = prm.twp + twp_base(Q, FF);  // in-step field FFT
+    const Cx<R>* __restrict__ twpH = prm.twp + twp_base(Q, HS);  // half-length FFTs
+
+    CB_MARK(0);
+    CB_TIMELINE(0);
+    // ---- 1. load the polyphase component u[rank + P*t2] of the circular
+    //         window starting at (b*keep - half) mod n (dbp.py:473-475)
+    {
+      int64_t start = (b * prm.keep - prm.half) % n;
+      if (start < 0) start += n;
+      start -= prm.in_origin;
+      if (start < 0) start += n;
+      const Cx<R>* src = prm.in + wv * prm.in_bstride;
+      for (int t2 = tid; t2 < Q; t2 += NT) {
+        int64_t idx = start + rank + (int64_t)P * t2;
+        if (idx >= n) idx -= n;
+        CB_CHECK(idx >= 0 && idx < n);
+        F[pad(t2)] = src[idx];
+        F[SF + pad(t2)] = src[prm.in_pstride + idx];
       }
     }
     __syncthreads();
-    CB_MARK(8 + 8 * st + 4);
-    fft1<R, Q, H, NT, true, HS>(TS, twpH, &s_zero);
-    CB_MARK(8 + 8 * st + 5);
+    if constexpr (TMON) asm volatile("tcgen05.fence::after_thread_sync;");
 
-    // rotation exp(-i theta) fused into the first pass of the subband FFT
-    // (dbp.py:208, :398); its last pass either fuses with the next phasor
-    // and the next step's IFFT (dbp.py:395-396) or, after the last step,
-    // applies the final phasor (dbp.py:399)
-    RotationHook<R> rot;
-    rot.th = Treal;
-    rot.scale = tsc_st;
-    const Cx<R>* ph_next = ph_rank + (size_t)phi_next * ph_tab;
-    if (st + 1 < prm.n_steps) {
-      fft2<R, Q, NT, FF, false, RotationHook<R>, NoHook, 1, Q / sched_radix(Q, 1, FI)>(
-          F, twpF, &s_zero, rot);
-      CB_MARK(8 + 8 * st + 6);
-      fft2_boundary<R, Q, NT, FI, FF>(F, twpF, ph_next, &s_zero);
-      CB_MARK(8 + 8 * st + 7);
-      fft2<R, Q, NT, FI, true, NoHook, IntensityHook<R>, sched_radix(Q, 1, FI)>(
-          F, twpT, &s_zero, NoHook(), ih);
+    const size_t ph_tab = (size_t)P * Q;
+    CB_MARK(1);
+
+    // ---- 2. outer transform, polyphase part: FFT_Q of both polarisations.
+    //         For P == 1 the subband layout is the natural FFT order
+    //         (bin_home is the identity) and the first phasor is fused in.
+    if constexpr (P == 1) {
+      PhasorHook<R> ph0;
+      ph0.ph = prm.phasor + (size_t)prm.ph_index[0] * ph_tab;
+      fft2<R, Q, NT, FI, false, NoHook, PhasorHook<R>>(F, twpT, &s_zero, NoHook(), ph0);
     } else {
-      PhasorHook<R> ph1;
-      ph1.ph = ph_next;
-      fft2<R, Q, NT, FF, false, RotationHook<R>, PhasorHook<R>>(F, twpF, &s_zero, rot, ph1);
-    }
-  }
-
-  CB_MARK(4);
-  // ---- 5. merge + outer IFFT (dbp.py:400-401): CTA c gathers, for k2 in
-  //         its slice, the P bins Q*k1 + k2 from their owners, applies the
-  //         inverse radix-P stage and the twiddle, and hands polyphase
-  //         component n1 to CTA n1 (staged as in step 3, which swaps the
-  //         rows back).
-  if constexpr (P > 1) {
-    cg::cluster_group cluster = cg::this_cluster();
-    const int lo = (rank * Q) / P, hi = ((rank + 1) * Q) / P;
-    Cx<R>* S = IS;
-    cluster.sync();
-    for (int pol = 0; pol < 2; ++pol) {
-      for (int k2 = lo + tid; k2 < hi; k2 += NT) {
-        Cx<R> xv[P];
-#pragma unroll
-        for (int k1 = 0; k1 < P; ++k1) {
-          int i, m;
-          bin_home<P, Q>(Q * k1 + k2, i, m);
-          const Cx<R>* rf = cluster.map_shared_rank(F, i);
-          xv[k1] = rf[pol * SF + pad(m)];
-        }
-#pragma unroll
-        for (int n1 = 0; n1 < P; ++n1) {
-          Cx<R> s = xv[0];
-#pragma unroll
-          for (int k1 = 1; k1 < P; ++k1) s = s + cmulc(xv[k1], ldg(twN + ((n1 * k1) % P) * Q));
-          if (n1) s = cmulc(s, ldg(twN + n1 * k2));
-          Cx<R>* dst = cluster.map_shared_rank(pol ? F : S, n1);
-          dst[pad(k2)] = s;
-        }
-      }
+      fft2<R, Q, NT, FI, false>(F, twpT, &s_zero);
+      // ---- 3. cross-subband radix-P stage over DSMEM: CTA c produces bins
+      //         Q*k1 + k2 for k2 in its slice and every k1, and writes each to
+      //         the CTA that owns it in the fftshift'd subband layout. Row 0's
+      //         results are staged in the owner's idle IS/RB region and row 1's
+      //         land in the owner's row 0 once every CTA has read it, so no CTA
+      //         overwrites fields another CTA still reads (3 cluster barriers).
+      //         The polarisation rows come out swapped; everything in the step
+      //         loop is symmetric in x and y, and step 5 swaps them back.
+      cg::cluster_group cluster = cg::this_cluster();
+      const int lo = (rank * Q) / P, hi = ((rank + 1) * Q) / P;
+      const R invP = (R)1 / (R)P;
+      const Cx<R>* ph0 = prm.phasor + (size_t)prm.ph_index[0] * ph_tab;
+      Cx<R>* S = IS;  // staging: padded_len(Q) entries fit in IS + RB
       cluster.sync();
+      for (int pol = 0; pol < 2; ++pol) {
+        for (int k2 = lo + tid; k2 < hi; k2 += NT) {
+          Cx<R> bv[P];
+  #pragma unroll
+          for (int r = 0; r < P; ++r) {
+            const Cx<R>* rf = cluster.map_shared_rank(F, r);
+            Cx<R> v = rf[pol * SF + pad(k2)];
+            if (r) v = cmul(v, ldg(twN + r * k2));
+            bv[r] = v;
+          }
+  #pragma unroll
+          for (int k1 = 0; k1 < P; ++k1) {
+            Cx<R> s = bv[0];
+  #pragma unroll
+            for (int r = 1; r < P; ++r) s = s + cmul(bv[r], ldg(twN + ((r * k1) % P) * Q));
+            int i, m;
+            bin_home<P, Q>(Q * k1 + k2, i, m);
+            const Cx<R> w = ldg(ph0 + (size_t)i * Q + m);
+            // row 0 results go to the staging area, row 1 results into the
+            // owner's row 0 (consumed by then): the rows come out swapped
+            Cx<R>* dst = cluster.map_shared_rank(pol ? F : S, i);
+            dst[pad(m)] = cmul(scale(s, invP), w);
+          }
+        }
+        cluster.sync();
+      }
+      // every remote read of row 1 is done: move the staged row-0 results in
+      for (int t = tid; t < Q; t += NT) F[SF + pad(t)] = S[pad(t)];
+      __syncthreads();
     }
-    for (int t = tid; t < Q; t += NT) F[SF + pad(t)] = S[pad(t)];
-    __syncthreads();
-  }
-  fft2<R, Q, NT, FI, true>(F, twpT, &s_zero);
 
-  CB_MARK(5);
-  CB_TIMELINE(1);
-  // ---- 6. keep proc[half : half + span] (dbp.py:476-477)
-  {
-    const int64_t span = min(prm.keep, n - b * prm.keep);
-    Cx<R>* dst = prm.out + wv * prm.out_bstride;
-    const int64_t obase = b * prm.keep - prm.half - prm.out_origin;
-    for (int t2 = tid; t2 < Q; t2 += NT) {
-      const int64_t t = rank + (int64_t)P * t2;
-      if (t >= prm.half && t < prm.half + span) {
-        CB_CHECK(obase + t >= 0 && (prm.out_origin != 0 || obase + t < n));
-        dst[obase + t] = F[pad(t2)];
-        dst[prm.out_pstride + obase + t] = F[SF + pad(t2)];
+    CB_MARK(2);
+    const Cx<R>* ph_rank = prm.phasor + (size_t)rank * Q;  // this CTA's subband rows
+    R* Ireal = reinterpret_cast<R*>(IS);
+    const R* Treal = reinterpret_cast<const R*>(TS);
+
+    // ---- 4. nonlinear steps (dbp.py:394-398). The subband IFFT
+    //         (normalisation folded into the phasor) also writes, in its last
+    //         pass, I = |x|^2 + |y|^2 packed as z[t] = I[2t] + i I[2t+1]. The
+    //         first step's IFFT runs here; later steps' IFFTs start inside
+    //         the previous step's fft2_boundary.
+    IntensityHook<R> ih;
+    ih.I = Ireal;
+    if (prm.n_steps > 0)
+      fft2<R, Q, NT, FI, true, NoHook, IntensityHook<R>>(F, twpT, &s_zero, NoHook(), ih);
+    CB_MARK(3);
+    constexpr int KU = (H / 2 + 1 + NT - 1) / NT;  // untangle/twist bins per thread
+    for (int st = 0; st < prm.n_steps; ++st) {
+      // per-step scalars issued at the top of the step: their L2 latency
+      // overlaps the intensity transforms instead of stalling the rotation
+      // FFT and the boundary pass
+      const R tsc_st = theta_scale[st];
+      const int phi_next = prm.ph_index[st + 1];  // n_steps + 1 entries
+      // W_Q^k of this thread's untangle/twist bins, issued before the FFT so
+      // the L2 latency hides behind it (the same k serve both)
+      Cx<R> twk[KU];
+  #pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        const int k = tid + u * NT;
+        twk[u] = (k <= H / 2) ? ldg(twQ + k) : mk((R)1, (R)0);
+      }
+      fft1<R, Q, H, NT, false, HS>(IS, twpH, &s_zero);
+      CB_MARK(8 + 8 * st + 0);
+
+      // r2c untangle: I_hat[k], k = 0..H (numpy rfft, dbp.py:194). For P > 1
+      // each bin goes straight from registers to the CTA whose MIMO slice
+      // holds it (st.async into its RB, completing on its mbarrier); for
+      // P == 1 it is written back in place.
+      if constexpr (P > 1) {
+        if (tid == 0) {
+          const int len = mimo_lo(rank + 1, P, H) - mimo_lo(rank, P, H);
+          mbar_expect(&s_bar[0], (uint32_t)(P * len * sizeof(Cx<R>)));
+          mbar_expect(&s_bar[1], (uint32_t)((H + 1) * sizeof(Cx<R>)));
+        }
+      }
+      auto emit = [&](int k, Cx<R> v) {
+        if constexpr (P > 1) {
+          int c = (k * P) / (H + 1);
+          if (mimo_lo(c + 1, P, H) <= k) ++c;
+          const uint32_t dst = cluster_addr(smem_addr(RB + rank * SLM + (k - mimo_lo(c, P, H))), c);
+          push(dst, v, cluster_addr(smem_addr(&s_bar[0]), c));
+        } else {
+          IS[pad(k)] = v;
+        }
+      };
+  #pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        const int k = tid + u * NT;
+        if (k > H / 2) break;
+        if (k == 0) {
+          const Cx<R> z = IS[pad(0)];
+          emit(0, mk(z.x + z.y, (R)0));
+          emit(H, mk(z.x - z.y, (R)0));
+        } else {
+          const Cx<R> a = IS[pad(k)];
+          const Cx<R> bq = conj(IS[pad(H - k)]);
+          const Cx<R> e = scale(a + bq, (R)0.5);
+          const Cx<R> dd = a - bq;                           // 2i * O[k]
+          const Cx<R> o = mk(dd.y * (R)0.5, -dd.x * (R)0.5); // O[k]
+          const Cx<R> wo = cmul(o, twk[u]);
+          emit(k, e + wo);
+          if (k != H - k) emit(H - k, conj(e - wo));
+        }
+      }
+
+      CB_MARK(8 + 8 * st + 1);
+      // MIMO coupling (dbp.py:195): theta_hat_i[k] = sum_l T[i,l,k] I_hat_l[k]
+      if constexpr (P > 1) {
+        const int lo = mimo_lo(rank, P, H), hi = mimo_lo(rank + 1, P, H);
+        const uint32_t ts_local = smem_addr(TS);
+        const uint32_t bar_t = smem_addr(&s_bar[1]);
+        for (int k = lo + tid; k < hi; k += NT) {
+          Cx<R> sv[P];
+  #pragma unroll
+          for (int l = 0; l < P; ++l) sv[l] = ldg_na(mimo + (size_t)l * (H + 1) + k);
+          mbar_wait(&s_bar[0], (st + ph0) & 1);
+          Cx<R> iv[P];
+  #pragma unroll
+          for (int l = 0; l < P; ++l) iv[l] = RB[l * SLM + (k - lo)];
+  #pragma unroll
+          for (int i = 0; i < P; ++i) {
+            Cx<R> acc = mk((R)0, (R)0);
+  #pragma unroll
+            for (int l = 0; l < P; ++l) {
+              acc = l >= i ? cmac(acc, sv[l - i], iv[l]) : cmacc(acc, sv[i - l], iv[l]);
+            }
+            push(cluster_addr(ts_local + (uint32_t)(pad(k) * sizeof(Cx<R>)), i), acc,
+                 cluster_addr(bar_t, i));
+          }
+        }
+        CB_MARK(8 + 8 * st + 2);
+        mbar_wait(&s_bar[1], (st + ph0) & 1);
+      } else {
+        __syncthreads();
+        for (int k = tid; k <= H; k += NT) TS[pad(k)] = cmul(ldg(mimo + k), IS[pad(k)]);
+        __syncthreads();
+      }
+
+      CB_MARK(8 + 8 * st + 3);
+      // c2r pre-twist in place (numpy irfft ignores Im of bins 0 and H)
+  #pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        const int k = tid + u * NT;
+        if (k > H / 2) break;
+        if (k == 0) {
+          const R x0 = TS[pad(0)].x, xh = TS[pad(H)].x;
+          TS[pad(0)] = mk(x0 + xh, x0 - xh);
+        } else {
+          const Cx<R> a = TS[pad(k)];                 // X[k]
+          const Cx<R> c = conj(TS[pad(H - k)]);       // X[k + H]
+          const Cx<R> wk = twk[u];                    // W^k
+          const Cx<R> s = a + c;
+          const Cx<R> dd = cmulc(a - c, wk);          // W^-k (a - c)
+          TS[pad(k)] = mk(s.x - dd.y, s.y + dd.x);    // s + i dd
+          if (k != H - k) {
+            // Z[H-k] = (X[H-k] + X[Q-k]) + i W^-(H-k) (X[H-k] - X[Q-k])
+            const Cx<R> a2 = conj(c);                 // X[H-k]
+            const Cx<R> c2 = conj(a);                 // X[Q-k]
+            const Cx<R> s2 = a2 + c2;
+            const Cx<R> w2 = mk(-wk.x, wk.y);         // W^(H-k) = -conj(W^k)
+            const Cx<R> d2 = cmulc(a2 - c2, w2);
+            TS[pad(H - k)] = mk(s2.x - d2.y, s2.y + d2.x);
+          }
+        }
+      }
+      __syncthreads();
+      CB_MARK(8 + 8 * st + 4);
+      fft1<R, Q, H, NT, true, HS>(TS, twpH, &s_zero);
+      CB_MARK(8 + 8 * st + 5);
+
+      // rotation exp(-i theta) fused into the first pass of the subband FFT
+      // (dbp.py:208, :398); its last pass either fuses with the next phasor
+      // and the next step's IFFT (dbp.py:395-396) or, after the last step,
+      // applies the final phasor (dbp.py:399)
+      RotationHook<R> rot;
+      rot.th = Treal;
+      rot.scale = tsc_st;
+      const Cx<R>* ph_next = ph_rank + (size_t)phi_next * ph_tab;
+      if (st + 1 < prm.n_steps) {
+        fft2<R, Q, NT, FF, false, RotationHook<R>, NoHook, 1, Q / sched_radix(Q, 1, FI)>(
+            F, twpF, &s_zero, rot);
+        CB_MARK(8 + 8 * st + 6);
+        fft2_boundary<R, Q, NT, FI, FF>(F, twpF, ph_next, &s_zero);
+        CB_MARK(8 + 8 * st + 7);
+        fft2<R, Q, NT, FI, true, NoHook, IntensityHook<R>, sched_radix(Q, 1, FI)>(
+            F, twpT, &s_zero, NoHook(), ih);
+      } else {
+        PhasorHook<R> ph1;
+        ph1.ph = ph_next;
+        fft2<R, Q, NT, FF, false, RotationHook<R>, PhasorHook<R>>(F, twpF, &s_zero, rot, ph1);
       }
     }
+
+    CB_MARK(4);
+    // ---- 5. merge + outer IFFT (dbp.py:400-401): CTA c gathers, for k2 in
+    //         its slice, the P bins Q*k1 + k2 from their owners, applies the
+    //         inverse radix-P stage and the twiddle, and hands polyphase
+    //         component n1 to CTA n1 (staged as in step 3, which swaps the
+    //         rows back).
+    if constexpr (P > 1) {
+      cg::cluster_group cluster = cg::this_cluster();
+      const int lo = (rank * Q) / P, hi = ((rank + 1) * Q) / P;
+      Cx<R>* S = IS;
+      cluster.sync();
+      for (int pol = 0; pol < 2; ++pol) {
+        for (int k2 = lo + tid; k2 < hi; k2 += NT) {
+          Cx<R> xv[P];
+  #pragma unroll
+          for (int k1 = 0; k1 < P; ++k1) {
+            int i, m;
+            bin_home<P, Q>(Q * k1 + k2, i, m);
+            const Cx<R>* rf = cluster.map_shared_rank(F, i);
+            xv[k1] = rf[pol * SF + pad(m)];
+          }
+  #pragma unroll
+          for (int n1 = 0; n1 < P; ++n1) {
+            Cx<R> s = xv[0];
+  #pragma unroll
+            for (int k1 = 1; k1 < P; ++k1) s = s + cmulc(xv[k1], ldg(twN + ((n1 * k1) % P) * Q));
+            if (n1) s = cmulc(s, ldg(twN + n1 * k2));
+            Cx<R>* dst = cluster.map_shared_rank(pol ? F : S, n1);
+            dst[pad(k2)] = s;
+          }
+        }
+        cluster.sync();
+      }
+      for (int t = tid; t < Q; t += NT) F[SF + pad(t)] = S[pad(t)];
+      __syncthreads();
+    }
+    fft2<R, Q, NT, FI, true>(F, twpT, &s_zero);
+
+    CB_MARK(5);
+    CB_TIMELINE(1);
+    // ---- 6. keep proc[half : half + span] (dbp.py:476-477)
+    {
+      const int64_t span = min(prm.keep, n - b * prm.keep);
+      Cx<R>* dst = prm.out + wv * prm.out_bstride;
+      const int64_t obase = b * prm.keep - prm.half - prm.out_origin;
+      for (int t2 = tid; t2 < Q; t2 += NT) {
+        const int64_t t = rank + (int64_t)P * t2;
+        if (t >= prm.half && t < prm.half + span) {
+          CB_CHECK(obase + t >= 0 && (prm.out_origin != 0 || obase + t < n));
+          dst[obase + t] = F[pad(t2)];
+          dst[prm.out_pstride + obase + t] = F[SF + pad(t2)];
+        }
+      }
+    }
+  }
+  if constexpr (P > 1) {
+    // rank 0's claim slots are read over DSMEM up to the last iteration
+    if (persist) cg::this_cluster().sync();
   }
   if constexpr (TMON) {
     asm volatile("tcgen05.fence::before_thread_sync;");

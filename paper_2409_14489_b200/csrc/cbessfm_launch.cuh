@@ -93,7 +93,7 @@ inline bool use_fat_kernel(int64_t nblocks, int pref) {
 // block): dynamic shared memory opt-in and sizing, non-portable clusters,
 // occupancy query for `info`. KERN is cbessfm_block_kernel<R, P, Q> or
 // cbessfm_ip_kernel<R, P> (same Params, threads, shared memory and TMEM).
-template <typename R, int P, int Q, void (*KERN)(const Params<R>)>
+template <typename R, int P, int Q, void (*KERN)(const Params<R>), bool PERSIST = false>
 cudaError_t launch_cluster(const char* kname, const Params<R>& prm, int64_t nclusters,
                            cudaStream_t stream, KernelInfo* info) {
   auto kern = KERN;
@@ -176,9 +176,32 @@ cudaError_t launch_cluster(const char* kname, const Params<R>& prm, int64_t nclu
     info->max_active_clusters = nc;
     if (nclusters == 0) return cudaSuccess;
   }
+  Params<R> p = prm;
+  if (PERSIST && p.work) {
+    // persistent launch (cbessfm_block_kernel): twice as many clusters as
+    // the register budget lets the SMs hold -- those beyond what the GPU
+    // actually co-schedules start late, find the counter spent and exit --
+    // each claiming blocks until all nclusters are done. CBESSFM_PERSIST=0
+    // launches one cluster per block (A/B); CBESSFM_PERSIST=k > 0 sets the
+    // grid to k clusters (tests: every block count takes the loop).
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t g = (int64_t)2 * sms * min_blocks<R, Q>() / P > 1
+                    ? (int64_t)2 * sms * min_blocks<R, Q>() / P
+                    : 1;
+    const char* env = getenv("CBESSFM_PERSIST");
+    if (env && atoi(env) > 0) g = atoi(env);
+    if (nclusters > g && !(env && env[0] == '0')) {
+      cudaError_t e = cudaMemsetAsync(p.work, 0, sizeof(unsigned long long), stream);
+      if (e != cudaSuccess) return e;
+      p.total = nclusters;
+      cfg.gridDim = dim3((unsigned)(g * P), 1, 1);
+      return cudaLaunchKernelEx(&cfg, kern, p);
+    }
+  }
+  p.work = nullptr;
   // grid.x is limited to 2^31-1 CTAs: launch in chunks of whole clusters
   const int64_t max_clusters = (int64_t)(0x7fffffff / P);
-  Params<R> p = prm;
   for (int64_t c0 = 0; c0 < nclusters; c0 += max_clusters) {
     const int64_t nc = nclusters - c0 < max_clusters ? nclusters - c0 : max_clusters;
     p.cid0 = prm.cid0 + c0;
@@ -215,8 +238,8 @@ cudaError_t launch_one(const Params<R>& prm, int64_t nclusters, cudaStream_t str
       return launch_cluster<R, P, Q, cbessfm_ip_kernel<R, P>>("cbessfm_ip_kernel", prm, nclusters,
                                                               stream, info);
   }
-  return launch_cluster<R, P, Q, cbessfm_block_kernel<R, P, Q>>("cbessfm_block_kernel", prm,
-                                                                nclusters, stream, info);
+  return launch_cluster<R, P, Q, cbessfm_block_kernel<R, P, Q>, true>("cbessfm_block_kernel", prm,
+                                                                      nclusters, stream, info);
 }
 
 template <typename R, int P>

@@ -496,3 +496,31 @@ def test_wide_path_shapes_against_oracle(cuda, n_sb, n_steps, q):
             out = pb.run_dbp_tensor(x, cfg, coeffs, rate)
         got = out[0].to(torch.complex128).cpu().numpy()
         assert rel_rms(got, ref) < TOL[dtype], (dtype, rel_rms(got, ref))
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_persistent_cluster_launch_is_bit_identical(cuda, dtype, monkeypatch):
+    # csrc/cbessfm_launch.cuh: large cluster-kernel launches run a grid of
+    # about two clusters per SM pair that claim blocks from a counter (TMEM
+    # rows filled once, mbarrier phases continuing across blocks). Forcing
+    # tiny grids (CBESSFM_PERSIST=k clusters) makes every golden case take
+    # the loop -- 1 cluster walks all blocks in order, 2/3/7 interleave --
+    # and each must equal one cluster per block bit for bit (and the
+    # reference within the bar); a batch of 3 waveforms covers the
+    # waveform / block index split of the claimed ids
+    import torch
+    monkeypatch.setenv("CBESSFM_KERNEL", "cluster")
+    for name in CASES:
+        g = golden(name)
+        if name.startswith("wide"):  # N' > 4096: the wide-subband path
+            continue
+        rate = g.wave.sample_rate
+        ct = torch.complex128 if dtype == "c128" else torch.complex64
+        x = torch.from_numpy(np.stack([np.vstack([g.wave.x, g.wave.y])] * 3)).to(cuda).to(ct)
+        monkeypatch.setenv("CBESSFM_PERSIST", "0")
+        ref = pb.run_dbp_tensor(x, g.cfg, g.coeffs, rate)
+        assert rel_rms(ref[1].cpu().numpy(), g.out) < TOL[dtype], name
+        for k in ("1", "2", "3", "7"):
+            monkeypatch.setenv("CBESSFM_PERSIST", k)
+            out = pb.run_dbp_tensor(x, g.cfg, g.coeffs, rate)
+            assert torch.equal(out, ref), f"{name} {dtype} persist={k}"
