@@ -665,7 +665,7 @@ def main():
             # slot w mod R -- every byte of every waveform is copied in and
             # out each step, only the content repeats
             ring = min(3, args.batch * max(1, args.steps)) if args.batch > 1 else 3
-            chunks = int(os.environ.get("BENCH_E2E_CHUNKS", "3"))
+            chunks = int(os.environ.get("BENCH_E2E_CHUNKS", "4"))
             hx = [x[r % args.batch:r % args.batch + 1].cpu().pin_memory() for r in range(ring)]
             hout = [torch.empty_like(h).pin_memory() for h in hx]
             sides = [torch.cuda.Stream(dev) for _ in range(ring)]
