@@ -299,6 +299,9 @@ __global__ void __launch_bounds__(256, 2) cbessfm_ip_kernel(const Params<R> prm)
     // the staged row-0 results (pos() layout, same padding) move in
     for (int t = tid; t < Q; t += NT) F[SF + pad(t)] = S[pad(t)];
     __syncthreads();
+    // as in cbessfm_block_kernel: no step-0 push may land in IS / RB (which
+    // S spans) before every CTA has read its staged row out
+    cluster_arrive();
   }
   CB_MARK(2);
 
@@ -321,6 +324,7 @@ __global__ void __launch_bounds__(256, 2) cbessfm_ip_kernel(const Params<R> prm)
     __syncthreads();
   }
   CB_MARK(3);
+  cluster_wait();
   constexpr int KU = (H / 2 + 1 + NT - 1) / NT;
   for (int st = 0; st < prm.n_steps; ++st) {
     const R tsc_st = theta_scale[st];

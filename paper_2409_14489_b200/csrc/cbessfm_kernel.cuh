@@ -780,6 +780,13 @@ __device__ __forceinline__ uint32_t cluster_addr(uint32_t local, uint32_t rank) 
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
   return r;
 }
+// split cluster barrier (release / acquire at cluster scope)
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
                : "memory");
@@ -1804,6 +1811,13 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
       // every remote read of row 1 is done: move the staged row-0 results in
       for (int t = tid; t < Q; t += NT) F[SF + pad(t)] = S[pad(t)];
       __syncthreads();
+      // S spans IS and RB, where the other CTAs' st.async pushes of step 0
+      // land: they may not start before every CTA of the cluster has read
+      // its staged row out. Split cluster barrier: arrive here, wait before
+      // the step loop (behind the first IFFT, so nobody actually waits). A
+      // CTA running a few microseconds ahead of a descheduled one did
+      // overwrite it: 1-2 corrupted blocks per 72 768-block launch.
+      cluster_arrive();
     }
 
     CB_MARK(2);
@@ -1821,6 +1835,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
     if (prm.n_steps > 0)
       fft2<R, Q, NT, FI, true, NoHook, IntensityHook<R>>(F, twpT, &s_zero, NoHook(), ih);
     CB_MARK(3);
+    if constexpr (P > 1) cluster_wait();  // pairs with the arrive after step 3's copy
     constexpr int KU = (H / 2 + 1 + NT - 1) / NT;  // untangle/twist bins per thread
     for (int st = 0; st < prm.n_steps; ++st) {
       // per-step scalars issued at the top of the step: their L2 latency

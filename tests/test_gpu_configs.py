@@ -7,6 +7,7 @@ smaller sizes); coefficient sets were built by the reference
 """
 
 import math
+import os
 import warnings
 from dataclasses import replace
 
@@ -163,6 +164,29 @@ def test_config4_full_batch_subset(cuda):
             warnings.simplefilter("ignore", RuntimeWarning)
             out = pb.run_dbp_tensor(xx, g.cfg, g.coeffs, rate)
         got = out[subset].to(torch.complex128).cpu().numpy()
+        if dtype == "c128":
+            # the persistent cluster kernel (this launch: ~118 clusters claiming
+            # 72 768 blocks) against one cluster per block, bit for bit over the
+            # WHOLE batch: a cross-block race in a CTA that works through
+            # hundreds of blocks shows up as a corrupted block somewhere in
+            # the launch, not necessarily in the oracle-checked subset
+            os.environ["CBESSFM_PERSIST"] = "0"
+            try:
+                with warnings.catch_warnings():
+                    warnings.simplefilter("ignore", RuntimeWarning)
+                    one = pb.run_dbp_tensor(xx, g.cfg, g.coeffs, rate)
+            finally:
+                os.environ.pop("CBESSFM_PERSIST", None)
+            for rep in range(3):
+                if rep:
+                    with warnings.catch_warnings():
+                        warnings.simplefilter("ignore", RuntimeWarning)
+                        out = pb.run_dbp_tensor(xx, g.cfg, g.coeffs, rate)
+                a = torch.view_as_real(out).view(torch.int64)
+                b = torch.view_as_real(one).view(torch.int64)
+                nbad = int((a != b).sum())
+                assert nbad == 0, f"persistent launch {rep}: {nbad} words differ"
+            del one, a, b
         del out, xx
         torch.cuda.empty_cache()
         for i, w in enumerate(subset):
