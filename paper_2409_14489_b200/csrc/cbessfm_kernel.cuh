@@ -1714,7 +1714,40 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
       if (cid >= prm.total) break;
       // claim the next block now; the other CTAs read it after this block's
       // last cluster barrier (step 5), which orders the store before them
+#ifndef CB_NO_PREFETCH_NEXT
+      // ... and pull its window towards L2 while this block computes (warp 0
+      // of rank 0; whole waveforms only: shards index a shorter slice).
+      // configs[4] c128 361.4 -> 359.1 ms per step (tools/gpu/r2_s4_pf.sh).
+      if (rank == 0 && tid < 32) {
+        long long nxt = 0;
+        if (tid == 0) {
+          nxt = (long long)atomicAdd(prm.work, 1ull);
+          s_cid[(it + 1) & 1] = nxt;
+        }
+        nxt = __shfl_sync(0xffffffffu, nxt, 0);
+        if (nxt < prm.total && prm.in_origin == 0) {
+          const int64_t c2 = nxt + prm.cid0;
+          const int64_t wv2 = c2 / prm.nb, b2 = prm.b0 + c2 % prm.nb;
+          int64_t st2 = (b2 * prm.keep - prm.half) % prm.n;
+          if (st2 < 0) st2 += prm.n;
+          if (st2 + (int64_t)P * Q <= prm.n) {
+            constexpr uint32_t piece = (uint32_t)((size_t)P * Q * sizeof(Cx<R>) / 32);
+            // (the bulk prefetch wants 16-byte aligned addresses: complex64
+            // windows may start on an odd sample, so round down)
+            static_assert(piece % 16 == 0, "prefetch pieces are whole 16-byte units");
+            const uintptr_t a0 =
+                reinterpret_cast<uintptr_t>(prm.in + wv2 * prm.in_bstride + st2) + (size_t)tid * piece;
+            const uintptr_t a1 = a0 + (size_t)prm.in_pstride * sizeof(Cx<R>);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0 & ~(uintptr_t)15),
+                         "r"(piece) : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a1 & ~(uintptr_t)15),
+                         "r"(piece) : "memory");
+          }
+        }
+      }
+#else
       if (rank == 0 && tid == 0) s_cid[(it + 1) & 1] = (long long)atomicAdd(prm.work, 1ull);
+#endif
       cid += prm.cid0;
     } else {
       if (it) break;
