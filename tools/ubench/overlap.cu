@@ -67,8 +67,11 @@ __global__ void __launch_bounds__(NT, 2) k(double2* out, int passes, double seed
 
 template <int MODE>
 float run(int ctas, int passes, double2* out) {
-  const size_t smem = 110 * 1024;
+  const size_t smem = 100 * 1024;
   cudaFuncSetAttribute(k<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k<MODE>, NT, smem);
+  if (MODE == 0 && passes == 2000) printf("  (occupancy query: %d CTAs per SM)\n", occ);
   k<MODE><<<ctas, NT, smem>>>(out, 10, 1e-9);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
