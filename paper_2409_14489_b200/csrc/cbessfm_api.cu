@@ -110,6 +110,7 @@ struct cbessfm_plan {
   void* twQ = nullptr;     // [Q]
   void* twN = nullptr;     // [P*Q]
   void* twp = nullptr;     // per-pass twiddle rows
+  void* rot_tab = nullptr; // complex128: exp(i k / kRotDen), k = -kRotTab/2 .. kRotTab/2 - 1
   long long* dbg = nullptr;  // phase clocks (CB_PHASE_PROFILE builds)
   // block counters of persistent cluster-kernel launches: each launch takes
   // the next slot of the ring (zeroed on its stream), so launches in flight
@@ -332,6 +333,17 @@ cbessfm_status upload_all(cbessfm_plan* p, const cbessfm_desc* d) {
       p->Q <= max_q(p->dtype) ? pass_tables(p->Q, tq, (int)sizeof(R)) : std::vector<double>(2, 0.0);
   if ((e = upload_complex<R>(tp.data(), tp.size() / 2, &p->twp, true)) != cudaSuccess)
     return cuda_fail(e, "upload pass twiddles");
+  if (sizeof(R) == sizeof(double)) {
+    // rotation table of the complex128 cluster kernel (RotationTabHook)
+    std::vector<double> rt(2 * (size_t)cbessfm::kRotTab);
+    for (int i = 0; i < cbessfm::kRotTab; ++i) {
+      const double a = (double)(i - cbessfm::kRotTab / 2) / cbessfm::kRotDen;
+      rt[2 * i] = std::cos(a);
+      rt[2 * i + 1] = std::sin(a);
+    }
+    if ((e = upload_complex<R>(rt.data(), (size_t)cbessfm::kRotTab, &p->rot_tab)) != cudaSuccess)
+      return cuda_fail(e, "upload rotation table");
+  }
   if ((e = cudaMalloc((void**)&p->work, sizeof(unsigned long long) * cbessfm_plan::kWorkSlots)) !=
       cudaSuccess)
     return cuda_fail(e, "alloc block counters");
@@ -370,6 +382,7 @@ void free_plan(cbessfm_plan* p) {
   cudaFree(p->twQ);
   cudaFree(p->twN);
   cudaFree(p->twp);
+  cudaFree(p->rot_tab);
   cudaFree(p->dbg);
   cudaFree(p->work);
   delete p;
@@ -447,6 +460,7 @@ cbessfm::Params<R> make_params(const cbessfm_plan* p, const cbessfm_io* io) {
   prm.twQ = reinterpret_cast<const C*>(p->twQ);
   prm.twN = reinterpret_cast<const C*>(p->twN);
   prm.twp = reinterpret_cast<const C*>(p->twp);
+  prm.rot_tab = reinterpret_cast<const C*>(p->rot_tab);
   prm.n_steps = p->n_steps;
   prm.n_sets = p->n_sets;
   prm.cid0 = 0;

@@ -987,6 +987,11 @@ __device__ __forceinline__ void sincos_acc<float>(float a, float* s, float* c) {
 #ifndef CB_LIBDEVICE_SINCOS
 template <>
 __device__ __forceinline__ void sincos_acc<double>(double a, double* s, double* c) {
+#ifdef CB_SINCOS_STUB  // timing experiment only (wrong results): what the sincos costs
+  *s = a;
+  *c = fma(a, -0.5 * a, 1.0);
+  return;
+#endif
   if (fabs(a) > 1048576.0) {
     sincos(a, s, c);
     return;
@@ -1044,6 +1049,72 @@ struct RotationHook : NoHook {
       const Cx<R> mine = mk(c, -s), theirs = mk(co, -so);
       v[2 * h] = cmul(v[2 * h], pol ? theirs : mine);
       v[2 * h + 1] = cmul(v[2 * h + 1], pol ? mine : theirs);
+    }
+  }
+};
+
+// complex128 cluster kernel with a rotation table in shared memory
+// (kRotTab entries exp(i k / kRotDen), k = -kRotTab/2 .. kRotTab/2 - 1, copied
+// from Params::rot_tab at kernel start): theta = k/32 + r with |r| <= 1/64,
+// the table gives (cos, sin)(k/32), degree-5 / degree-6 Taylor polynomials
+// give (sin, cos)(r) to < 5e-17, one complex product combines them -- 15
+// FP64 instructions per angle instead of 23 and no quadrant selects. Angles
+// of 7.9375 rad or more anywhere in the warp (never reached by a per-step
+// nonlinear phase, but legal) take sincos_acc for the whole pass: one
+// warp-uniform branch per pass, so each side keeps its eight angles
+// interleaved.
+constexpr int kRotTab = 512;
+constexpr int kRotDen = 32;
+template <typename R>
+struct RotationTabHook : NoHook {
+  const R* th;
+  R scale;
+  const Cx<R>* tab;  // shared memory, entry k + kRotTab/2
+  template <typename, int RAD, int LR>
+  __device__ __forceinline__ void pre(int j, Cx<R>* v) {
+    static_assert(sizeof(R) == 8, "the rotation table is built for complex128");
+    const R* base = th + fpos(j);
+    const int pol = (threadIdx.x >> 4) & 1;
+    static_assert(RAD % 2 == 0, "rotation split needs an even radix");
+    double a[RAD / 2];
+    bool small = true;
+#pragma unroll
+    for (int h = 0; h < RAD / 2; ++h) {
+      a[h] = base[2 * pad((2 * h + pol) * LR / 2)] * scale;
+      // |a| < 7.9375 (0x401FC000...): |k| <= 254
+      small = small && (unsigned)(__double2hiint(a[h]) & 0x7fffffff) < 0x401fc000u;
+    }
+    if (__all_sync(0xffffffffu, small)) {
+#pragma unroll
+      for (int h = 0; h < RAD / 2; ++h) {
+        const double t = fma(a[h], (double)kRotDen, 6755399441055744.0);  // 1.5 * 2^52
+        const int k = __double2loint(t);                                  // rint(32 a)
+        const double r = fma(t - 6755399441055744.0, -1.0 / kRotDen, a[h]);
+        const Cx<R> e = tab[k + kRotTab / 2];
+        const double r2 = r * r;
+        const double sn = fma(r * r2, fma(r2, 8.33333333333333333e-03, -1.66666666666666667e-01), r);
+        double pc = fma(r2, -1.38888888888888889e-03, 4.16666666666666667e-02);
+        pc = fma(r2, pc, -0.5);
+        const double cs = fma(r2, pc, 1.0);
+        const double c = fma(e.x, cs, -(e.y * sn));
+        const double s = fma(e.y, cs, e.x * sn);
+        const R so = __shfl_xor_sync(0xffffffffu, s, 16);
+        const R co = __shfl_xor_sync(0xffffffffu, c, 16);
+        const Cx<R> mine = mk(c, -s), theirs = mk(co, -so);
+        v[2 * h] = cmul(v[2 * h], pol ? theirs : mine);
+        v[2 * h + 1] = cmul(v[2 * h + 1], pol ? mine : theirs);
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < RAD / 2; ++h) {
+        R s, c;
+        sincos_acc<R>(a[h], &s, &c);
+        const R so = __shfl_xor_sync(0xffffffffu, s, 16);
+        const R co = __shfl_xor_sync(0xffffffffu, c, 16);
+        const Cx<R> mine = mk(c, -s), theirs = mk(co, -so);
+        v[2 * h] = cmul(v[2 * h], pol ? theirs : mine);
+        v[2 * h + 1] = cmul(v[2 * h + 1], pol ? mine : theirs);
+      }
     }
   }
 };
@@ -1536,6 +1607,7 @@ struct Params {
   const Cx<R>* twQ;        // [Q]   exp(-2 pi i m / Q)
   const Cx<R>* twN;        // [P*Q] exp(-2 pi i m / (P Q))
   const Cx<R>* twp;        // per-pass rows, layout twp_base()
+  const Cx<R>* rot_tab;    // [kRotTab] exp(i k / kRotDen) (complex128 plans), else null
   int n_steps;
   int64_t cid0;            // first cluster index of this launch chunk
   // persistent launches of the cluster kernel (null: one block per cluster):
@@ -1594,6 +1666,17 @@ template <typename R, int Q>
 __host__ __device__ constexpr bool tm_on() { return false; }
 #endif
 
+// The rotation table (RotationTabHook) rides in the shared memory the TMEM
+// kernels claim anyway (1/min_blocks of the SM, csrc/cbessfm_launch.cuh):
+// complex128 with TMEM rows, i.e. N' = 2048 and 4096.
+#ifndef CB_ROT_TAB
+#define CB_ROT_TAB 1
+#endif
+template <typename R, int Q>
+__host__ __device__ constexpr bool rot_tab_on() {
+  return CB_ROT_TAB && sizeof(R) == 8 && tm_on<R, Q>();
+}
+
 // MIMO slice of CTA c: bins [mimo_lo(c), mimo_lo(c+1)) of the H+1 rfft bins.
 __host__ __device__ constexpr int mimo_lo(int c, int P, int H) { return (c * (H + 1)) / P; }
 __host__ __device__ constexpr int mimo_slice_max(int P, int H) { return (H + 1 + P - 1) / P; }
@@ -1611,7 +1694,8 @@ template <typename R, int Q>
 __host__ __device__ constexpr size_t smem_bytes(int P) {
   // F: 2 padded polarisation rows; IS: padded spectrum (Q/2+1 bins)
   return sizeof(Cx<R>) *
-         (size_t)(2 * padded_len(Q) + padded_len(Q / 2 + 1) + (P > 1 ? rb_len<Q>(P) : 0));
+         (size_t)(2 * padded_len(Q) + padded_len(Q / 2 + 1) + (P > 1 ? rb_len<Q>(P) : 0) +
+                  (rot_tab_on<R, Q>() ? kRotTab : 0));
 }
 
 // Position of global FFT bin g (of N = P*Q) in the subband layout:
@@ -1644,6 +1728,12 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
   Cx<R>* TS = IS;
   Cx<R>* RB = IS + padded_len(H + 1);  // P > 1 only
   constexpr int SLM = mimo_slice_max(P, H);
+  constexpr bool ROTTAB = rot_tab_on<R, Q>();
+  Cx<R>* RT = RB + (P > 1 ? rb_len<Q>(P) : 0);  // rotation table (ROTTAB only)
+  if constexpr (ROTTAB) {
+    // (ordered before its first use by the barrier after the block load)
+    for (int i = threadIdx.x; i < kRotTab; i += threads_for<R, Q>()) RT[i] = ldg(prm.rot_tab + i);
+  }
 
   __shared__ int s_zero;
   __shared__ uint64_t s_bar[2];  // [0]: intensity slices in RB, [1]: theta_hat in TS
@@ -1997,12 +2087,14 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
       // (dbp.py:208, :398); its last pass either fuses with the next phasor
       // and the next step's IFFT (dbp.py:395-396) or, after the last step,
       // applies the final phasor (dbp.py:399)
-      RotationHook<R> rot;
+      using Rot = typename std::conditional<ROTTAB, RotationTabHook<R>, RotationHook<R>>::type;
+      Rot rot;
       rot.th = Treal;
       rot.scale = tsc_st;
+      if constexpr (ROTTAB) rot.tab = RT;
       const Cx<R>* ph_next = ph_rank + (size_t)phi_next * ph_tab;
       if (st + 1 < prm.n_steps) {
-        fft2<R, Q, NT, FF, false, RotationHook<R>, NoHook, 1, Q / sched_radix(Q, 1, FI)>(
+        fft2<R, Q, NT, FF, false, Rot, NoHook, 1, Q / sched_radix(Q, 1, FI)>(
             F, twpF, &s_zero, rot);
         CB_MARK(8 + 8 * st + 6);
         fft2_boundary<R, Q, NT, FI, FF>(F, twpF, ph_next, &s_zero);
@@ -2012,7 +2104,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
       } else {
         PhasorHook<R> ph1;
         ph1.ph = ph_next;
-        fft2<R, Q, NT, FF, false, RotationHook<R>, PhasorHook<R>>(F, twpF, &s_zero, rot, ph1);
+        fft2<R, Q, NT, FF, false, Rot, PhasorHook<R>>(F, twpF, &s_zero, rot, ph1);
       }
     }
 

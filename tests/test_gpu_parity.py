@@ -524,3 +524,25 @@ def test_persistent_cluster_launch_is_bit_identical(cuda, dtype, monkeypatch):
             monkeypatch.setenv("CBESSFM_PERSIST", k)
             out = pb.run_dbp_tensor(x, g.cfg, g.coeffs, rate)
             assert torch.equal(out, ref), f"{name} {dtype} persist={k}"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("amp", [1.0, 6.0, 7.0, 12.0])
+@pytest.mark.parametrize("name", ["cfg2_nsb5", "cfg4_nsb5_st10"])
+def test_rotation_table_and_large_angle_fallback(cuda, name, amp):
+    # the complex128 cluster kernel at N' = 2048 / 4096 rotates by exp(-i theta)
+    # through a shared-memory table for |theta| < 7.9375 rad and through the
+    # polynomial sincos for any warp that holds a larger angle
+    # (csrc/cbessfm_kernel.cuh RotationTabHook). Scaling the waveform by amp
+    # scales every theta by amp^2 (max |theta| is 0.19 rad at amp 1 in both
+    # cases): 6 uses the whole table (max 6.9 rad), 7 mixes both paths (mean
+    # 5.7, max 9.4), 12 is all fallback (mean 17 rad). Each against the
+    # oracle on the same scaled input, at the complex128 bar.
+    g = golden(name)
+    w = pb.DualPolWaveform(g.wave.x * amp, g.wave.y * amp, g.wave.sample_rate)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        out = pb.run_dbp(w, g.cfg, g.coeffs, dtype="c128")
+        ref = orc.run_cb(w.x, w.y, w.sample_rate, g.cfg, g.coeffs)
+    e = rel_rms(np.vstack([out.x, out.y]), np.vstack(ref))
+    assert e < TOL["c128"], (name, amp, e)
