@@ -931,6 +931,11 @@ __device__ __forceinline__ void sincos_acc(R a, R* s, R* c);
 // step, but legal) take the libdevice path.
 template <>
 __device__ __forceinline__ void sincos_acc<float>(float a, float* s, float* c) {
+#ifdef CB_SINCOS_STUB  // timing experiment only (wrong results): what the sincos costs
+  *s = a;
+  *c = __fmaf_rn(a, -0.5f * a, 1.0f);
+  return;
+#endif
   float r;
   int q;
   if (fabsf(a) > 8192.0f) {
