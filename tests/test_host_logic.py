@@ -361,3 +361,32 @@ def test_sim_settings_xor():
         ch.SimSettings(step_km=0.1, max_phase_rad=1e-3)
     s = ch.SimSettings()
     assert s.step_km == 0.1 and s.max_phase_rad is None
+
+
+def test_rotation_table_arithmetic_is_accurate_to_an_ulp():
+    # csrc/cbessfm_kernel.cuh RotationTabHook, restated in numpy float64 with
+    # the kernel's operations in the kernel's order (the FMAs become separate
+    # multiply / add here, which only loosens the bound): exp(i a) from the
+    # 512-entry table exp(i k / 32) and the degree-5 / degree-6 Taylor
+    # remainders, for every |a| < 7.9375 the table path accepts.
+    rng = np.random.default_rng(11)
+    a = np.concatenate([rng.uniform(-7.9374, 7.9374, 200000), [0.0, -0.0, 7.9374, -7.9374, 1 / 64, -1 / 64]])
+    magic = 6755399441055744.0          # 1.5 * 2^52
+    t = a * 32.0 + magic
+    k = (t.view(np.int64) & 0xFFFFFFFF).astype(np.int64)
+    k = np.where(k >= 2 ** 31, k - 2 ** 32, k)       # the low word, two's complement
+    assert np.array_equal(k, np.rint(a * 32.0).astype(np.int64))
+    assert np.abs(k).max() <= 254                     # inside the 512 entries
+    r = (t - magic) * (-1.0 / 32) + a
+    assert np.abs(r).max() <= 1 / 64
+    tab_c, tab_s = np.cos((np.arange(512) - 256) / 32.0), np.sin((np.arange(512) - 256) / 32.0)
+    ec, es = tab_c[k + 256], tab_s[k + 256]
+    r2 = r * r
+    sn = (r * r2) * (r2 * 8.33333333333333333e-03 - 1.66666666666666667e-01) + r
+    pc = r2 * -1.38888888888888889e-03 + 4.16666666666666667e-02
+    pc = r2 * pc - 0.5
+    cs = r2 * pc + 1.0
+    c = ec * cs - es * sn
+    s = es * cs + ec * sn
+    err = np.hypot(c - np.cos(a), s - np.sin(a)).max()
+    assert err < 4e-16, err
