@@ -37,15 +37,31 @@ __global__ void __launch_bounds__(NT, 2) k(double2* out, int passes, double seed
         }
     }
     if (fp) {
+      // (accumulators and multipliers in registers of their own: operands
+      // taken straight from the 4-aligned quads an LDS.128 fills collide on
+      // the register banks and cost a third cycle per DFMA)
+      double ax[8], ay[8], mx[8], my[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        ax[r] = v[r].x;
+        ay[r] = v[r].y;
+        mx[r] = v[r + 8].x + 1.0;
+        my[r] = v[r + 8].y + 1.0;
+      }
 #pragma unroll
       for (int q = 0; q < reps; ++q)
 #pragma unroll
         for (int f = 0; f < NF / 16; ++f)
 #pragma unroll
           for (int r = 0; r < 8; ++r) {
-            v[r].x = fma(v[r].x, v[r + 8].y, v[r].y);
-            v[r].y = fma(v[r].y, v[r + 8].x, v[r].x);
+            ax[r] = fma(ax[r], my[r], ay[r]);
+            ay[r] = fma(ay[r], mx[r], ax[r]);
           }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        v[r].x = ax[r];
+        v[r].y = ay[r];
+      }
     }
     if (MODE == 3) __syncthreads();
     if (ls) {
