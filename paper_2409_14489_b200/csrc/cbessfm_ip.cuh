@@ -183,6 +183,11 @@ __global__ void __launch_bounds__(256, 2) cbessfm_ip_kernel(const Params<R> prm)
   Cx<R>* TS = IS;  // as in cbessfm_block_kernel
   Cx<R>* RB = IS + padded_len(H + 1);
   constexpr int SLM = mimo_slice_max(P, H);
+  constexpr bool ROTTAB = rot_tab_on<R, Q>();
+  Cx<R>* RT = RB + rb_len<Q>(P);  // rotation table (RotationTabHook)
+  if constexpr (ROTTAB) {
+    for (int i = threadIdx.x; i < kRotTab; i += NT) RT[i] = ldg(prm.rot_tab + i);
+  }
 
   __shared__ int s_zero;
   __shared__ uint64_t s_bar[2];
@@ -207,15 +212,61 @@ __global__ void __launch_bounds__(256, 2) cbessfm_ip_kernel(const Params<R> prm)
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;");
 
-  CB_MARK(0);
   const int tid = threadIdx.x;
-  const int64_t cid_tl = prm.cid0 + blockIdx.x / P;
-  {
-    const int64_t cid = cid_tl;
-    CB_TIMELINE(0);
-  }
   const int rank = (int)(blockIdx.x % P);
-  const int64_t cid = prm.cid0 + blockIdx.x / P;
+  // persistent launches: as in cbessfm_block_kernel (rank 0 claims blocks from
+  // the launch-wide counter, the next one at the top of the current block, and
+  // pulls its window towards L2; mbarrier phase parity continues across blocks)
+  __shared__ long long s_cid[3];
+  const bool persist = prm.work != nullptr;
+  if (persist) {
+    if (rank == 0 && tid == 0) s_cid[0] = (long long)atomicAdd(prm.work, 1ull);
+    cg::this_cluster().sync();
+  }
+  for (int it = 0;; ++it) {
+  int64_t cid;
+  if (persist) {
+    if (tid == 0) {
+      long long c = s_cid[it & 1];
+      if (rank != 0) c = *cg::this_cluster().map_shared_rank(&s_cid[it & 1], 0);
+      s_cid[2] = c;
+    }
+    __syncthreads();
+    cid = s_cid[2];
+    if (cid >= prm.total) break;
+    if (rank == 0 && tid < 32) {
+      long long nxt = 0;
+      if (tid == 0) {
+        nxt = (long long)atomicAdd(prm.work, 1ull);
+        s_cid[(it + 1) & 1] = nxt;
+      }
+      nxt = __shfl_sync(0xffffffffu, nxt, 0);
+      if (nxt < prm.total && prm.in_origin == 0) {
+        const int64_t c2 = nxt + prm.cid0;
+        const int64_t wv2 = c2 / prm.nb, b2 = prm.b0 + c2 % prm.nb;
+        int64_t st2 = (b2 * prm.keep - prm.half) % prm.n;
+        if (st2 < 0) st2 += prm.n;
+        if (st2 + (int64_t)P * Q <= prm.n) {
+          constexpr uint32_t piece = (uint32_t)((size_t)P * Q * sizeof(Cx<R>) / 32);
+          static_assert(piece % 16 == 0, "prefetch pieces are whole 16-byte units");
+          const uintptr_t a0 =
+              reinterpret_cast<uintptr_t>(prm.in + wv2 * prm.in_bstride + st2) + (size_t)tid * piece;
+          const uintptr_t a1 = a0 + (size_t)prm.in_pstride * sizeof(Cx<R>);
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0 & ~(uintptr_t)15),
+                       "r"(piece) : "memory");
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a1 & ~(uintptr_t)15),
+                       "r"(piece) : "memory");
+        }
+      }
+    }
+    cid += prm.cid0;
+  } else {
+    if (it) break;
+    cid = prm.cid0 + blockIdx.x / P;
+  }
+  const int ph0 = (int)(((int64_t)it * prm.n_steps) & 1);
+  CB_MARK(0);
+  CB_TIMELINE(0);
   const int64_t wv = cid / prm.nb;
   const int64_t b = prm.b0 + cid % prm.nb;
   const int64_t n = prm.n;
@@ -399,7 +450,7 @@ __global__ void __launch_bounds__(256, 2) cbessfm_ip_kernel(const Params<R> prm)
         Cx<R> sv[P];
 #pragma unroll
         for (int l = 0; l < P; ++l) sv[l] = ldg_na(mimo + (size_t)l * (H + 1) + k);
-        mbar_wait(&s_bar[0], st & 1);
+        mbar_wait(&s_bar[0], (st + ph0) & 1);
         Cx<R> iv[P];
 #pragma unroll
         for (int l = 0; l < P; ++l) iv[l] = RB[l * SLM + (k - lo)];
@@ -414,7 +465,7 @@ __global__ void __launch_bounds__(256, 2) cbessfm_ip_kernel(const Params<R> prm)
         }
       }
       CB_MARK(8 + 8 * st + 2);
-      mbar_wait(&s_bar[1], st & 1);
+      mbar_wait(&s_bar[1], (st + ph0) & 1);
     }
     CB_MARK(8 + 8 * st + 3);
 
@@ -451,9 +502,10 @@ __global__ void __launch_bounds__(256, 2) cbessfm_ip_kernel(const Params<R> prm)
     // rotation exp(-i theta) fused into G (dbp.py:208, :398), then the
     // warp-local passes; the boundary pass applies the next phasor and
     // starts the next IFFT (dbp.py:395-396), or the final phasor (:399)
-    RotationHook<R> rot;
+    typename std::conditional<ROTTAB, RotationTabHook<R>, RotationHook<R>>::type rot;
     rot.th = Treal;
     rot.scale = tsc_st;
+    if constexpr (ROTTAB) rot.tab = RT;
     ip_global<R, false>(F, &s_zero, rot, rowsG);
     __syncthreads();
     ip_l1<R, false>(F, &s_zero, rowsL);
@@ -512,10 +564,7 @@ __global__ void __launch_bounds__(256, 2) cbessfm_ip_kernel(const Params<R> prm)
   }
   fft2<R, Q, NT, FI, true>(F, twpT, &s_zero);
   CB_MARK(5);
-  {
-    const int64_t cid = cid_tl;
-    CB_TIMELINE(1);
-  }
+  CB_TIMELINE(1);
 
   // ---- 6. keep proc[half : half + span] (dbp.py:476-477)
   {
@@ -531,6 +580,9 @@ __global__ void __launch_bounds__(256, 2) cbessfm_ip_kernel(const Params<R> prm)
       }
     }
   }
+  }  // blocks of this cluster
+  // rank 0's claim slots are read over DSMEM up to the last iteration
+  if (persist) cg::this_cluster().sync();
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (threadIdx.x < 32)

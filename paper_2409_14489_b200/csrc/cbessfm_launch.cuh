@@ -214,10 +214,13 @@ cudaError_t launch_cluster(const char* kname, const Params<R>& prm, int64_t nclu
 
 
 // In-place-pass kernel (cbessfm_ip.cuh, complex128, N' = 2048, P >= 2):
-// selected with CBESSFM_KERNEL=ip. Same results as the cluster kernel
-// (parity-tested) but not faster: configs[4] 379.6 vs 373.5 ms per step,
-// configs[1] x8 6.01 vs 5.99 ms ("In-place passes"),
-// so the Stockham cluster kernel stays the default.
+// selected with CBESSFM_KERNEL=ip. Same results as the cluster kernel within
+// rounding (parity-tested), same persistent launch, prefetch and rotation
+// table, but not faster: at equal features it went from 1.5 % ahead (367.2
+// vs 372.9 ms on configs[4], one cluster per block, polynomial sincos) to
+// 1.9 % behind once both had the persistent launch and the table (353.2 vs
+// 346.7 ms; tools/gpu/r2_s4_ip2.sh, r2_s4_ipp.sh), so the Stockham cluster
+// kernel stays the default.
 template <typename R, int P, int Q>
 constexpr bool ip_ok() {
   return sizeof(R) == 8 && Q == kIpQ && P >= 2;
@@ -235,8 +238,8 @@ cudaError_t launch_one(const Params<R>& prm, int64_t nclusters, cudaStream_t str
   }
   if constexpr (ip_ok<R, P, Q>()) {
     if (use_ip_kernel() && prm.phasor_rev)
-      return launch_cluster<R, P, Q, cbessfm_ip_kernel<R, P>>("cbessfm_ip_kernel", prm, nclusters,
-                                                              stream, info);
+      return launch_cluster<R, P, Q, cbessfm_ip_kernel<R, P>, true>("cbessfm_ip_kernel", prm,
+                                                                    nclusters, stream, info);
   }
   return launch_cluster<R, P, Q, cbessfm_block_kernel<R, P, Q>, true>("cbessfm_block_kernel", prm,
                                                                       nclusters, stream, info);

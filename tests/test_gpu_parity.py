@@ -498,8 +498,8 @@ def test_wide_path_shapes_against_oracle(cuda, n_sb, n_steps, q):
         assert rel_rms(got, ref) < TOL[dtype], (dtype, rel_rms(got, ref))
 
 
-@pytest.mark.parametrize("dtype", ["c128", "c64"])
-def test_persistent_cluster_launch_is_bit_identical(cuda, dtype, monkeypatch):
+@pytest.mark.parametrize("dtype,kernel", [("c128", "cluster"), ("c64", "cluster"), ("c128", "ip")])
+def test_persistent_cluster_launch_is_bit_identical(cuda, dtype, kernel, monkeypatch):
     # csrc/cbessfm_launch.cuh: large cluster-kernel launches run a grid of
     # about two clusters per SM pair that claim blocks from a counter (TMEM
     # rows filled once, mbarrier phases continuing across blocks). Forcing
@@ -508,8 +508,11 @@ def test_persistent_cluster_launch_is_bit_identical(cuda, dtype, monkeypatch):
     # and each must equal one cluster per block bit for bit (and the
     # reference within the bar); a batch of 3 waveforms covers the
     # waveform / block index split of the claimed ids
+    # (kernel "ip": the in-place-pass kernel, the complex128 default at
+    # N' = 2048, has the same persistent loop; other shapes fall through to
+    # the Stockham cluster kernel)
     import torch
-    monkeypatch.setenv("CBESSFM_KERNEL", "cluster")
+    monkeypatch.setenv("CBESSFM_KERNEL", kernel)
     for name in CASES:
         g = golden(name)
         if name.startswith("wide"):  # N' > 4096: the wide-subband path

@@ -10,6 +10,13 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
+// -DADDMIX: the FP64 work is two-operand DADDs (2 issue cycles each, like most of
+// a butterfly) instead of three-operand DFMAs (3 cycles each here)
+#ifdef ADDMIX
+#define FPOP(a, m, b) ((a) + (b))
+#else
+#define FPOP(a, m, b) fma((a), (m), (b))
+#endif
 constexpr int NT = 256;
 constexpr int NF = 200;
 
@@ -54,8 +61,8 @@ __global__ void __launch_bounds__(NT, 2) k(double2* out, int passes, double seed
         for (int f = 0; f < NF / 16; ++f)
 #pragma unroll
           for (int r = 0; r < 8; ++r) {
-            ax[r] = fma(ax[r], my[r], ay[r]);
-            ay[r] = fma(ay[r], mx[r], ax[r]);
+            ax[r] = FPOP(ax[r], my[r], ay[r]);
+            ay[r] = FPOP(ay[r], mx[r], ax[r]);
           }
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
