@@ -664,8 +664,15 @@ def main():
             # samples (read back from HBM once); waveform w of a step uses
             # slot w mod R -- every byte of every waveform is copied in and
             # out each step, only the content repeats
-            ring = min(3, args.batch * max(1, args.steps)) if args.batch > 1 else 3
-            chunks = int(os.environ.get("BENCH_E2E_CHUNKS", "4"))
+            # (ring of 4 slots, one chunk per waveform: the kernel now takes less
+            # than the H2D of a waveform, so what matters is that the copy-in
+            # engine never waits for a slot -- tools/gpu/r2_s4_e2e2.sh: 379.5 ms
+            # with 3 slots x 4 chunks, 367.3 ms with 4 x 1 on a box whose host
+            # link floors the step at 363 ms)
+            big = args.batch > 1   # single-waveform steps keep 3 slots x 4 chunks
+            ring_max = int(os.environ.get("BENCH_E2E_RING", "4" if big else "3"))
+            ring = min(ring_max, args.batch * max(1, args.steps)) if args.batch > 1 else ring_max
+            chunks = int(os.environ.get("BENCH_E2E_CHUNKS", "1" if big else "4"))
             hx = [x[r % args.batch:r % args.batch + 1].cpu().pin_memory() for r in range(ring)]
             hout = [torch.empty_like(h).pin_memory() for h in hx]
             sides = [torch.cuda.Stream(dev) for _ in range(ring)]
