@@ -1758,7 +1758,10 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
   // radix-8 half-length passes from Q = 2048 (measured: c64 -1.3 %, c128
   // -2.5 % per step at Q = 2048 vs radix 4, though a pass then keeps only
   // half the CTA's threads busy)
-  constexpr int HS = kHalf | (TMON ? kTM : 0) | (Q >= 2048 ? kWide : 0);
+#ifndef CB_HALF_R4  // experiment knob: 1 = radix-4 half-length passes at every Q
+#define CB_HALF_R4 0
+#endif
+  constexpr int HS = kHalf | (TMON ? kTM : 0) | (Q >= 2048 && !CB_HALF_R4 ? kWide : 0);
   if constexpr (TMON) {
     // allocate this CTA's TMEM columns (warp 0) and copy the twiddle rows in
     if (threadIdx.x < 32) {
