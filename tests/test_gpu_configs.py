@@ -187,6 +187,13 @@ def test_config4_full_batch_subset(cuda):
                 nbad = int((a != b).sum())
                 assert nbad == 0, f"persistent launch {rep}: {nbad} words differ"
             del one, a, b
+        else:
+            # the one-block kernel at the same scale: two launches, bit for bit
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore", RuntimeWarning)
+                again = pb.run_dbp_tensor(xx, g.cfg, g.coeffs, rate)
+            assert torch.equal(out, again), "c64 launches differ"
+            del again
         del out, xx
         torch.cuda.empty_cache()
         for i, w in enumerate(subset):
