@@ -148,13 +148,21 @@ cudaError_t launch_cluster(const char* kname, const Params<R>& prm, int64_t nclu
   cfg.blockDim = dim3(NT, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = P;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = P > 1 ? 1 : 0;
+  if (const char* env = getenv("CBESSFM_CLUSTER_POLICY")) {  // experiment hook: 1 spread, 2 load balancing
+    if (P > 1 && atoi(env) > 0) {
+      attr[1].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+      attr[1].val.clusterSchedulingPolicyPreference =
+          atoi(env) == 1 ? cudaClusterSchedulingPolicySpread : cudaClusterSchedulingPolicyLoadBalancing;
+      cfg.numAttrs = 2;
+    }
+  }
   if (info) {
     info->threads = NT;
     info->cluster = P;
