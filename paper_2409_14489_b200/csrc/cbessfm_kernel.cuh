@@ -1480,7 +1480,13 @@ __device__ __forceinline__ void fft2_boundary(Cx<R>* __restrict__ F,
     // and hand it to the inverse butterfly as its input r
     Cx<R> u[RAD];
 #pragma unroll
-    for (int r = 0; r < RAD; ++r) u[r] = cmul(v[p][bitrev<RAD>(r)], ldg_na(ph + j + r * LR));
+    for (int r = 0; r < RAD; ++r) {
+#ifdef CB_PHASOR_STUB  // timing experiment only (wrong results): what the phasor loads cost
+      u[r] = cmul(v[p][bitrev<RAD>(r)], mk((R)(1.0 / Q), (R)(1e-3 * r / Q)));
+#else
+      u[r] = cmul(v[p][bitrev<RAD>(r)], ldg_na(ph + j + r * LR));
+#endif
+    }
     dft_reg<R, RAD, true>(u);
 #pragma unroll
     for (int r = 0; r < RAD; ++r) v[p][r] = u[r];
