@@ -1988,8 +1988,14 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
         const int k = tid + u * NT;
         twk[u] = (k <= H / 2) ? ldg(twQ + k) : mk((R)1, (R)0);
       }
-      fft1<R, Q, H, NT, false, HS>(IS, twpH, &s_zero);
+      // CB_STUB_NLPR (timing experiments only, wrong results): 1 skips the two
+      // half-length transforms, 2 also the untangle / MIMO exchange / twist
+#ifndef CB_STUB_NLPR
+#define CB_STUB_NLPR 0
+#endif
+      if (CB_STUB_NLPR < 1) fft1<R, Q, H, NT, false, HS>(IS, twpH, &s_zero);
       CB_MARK(8 + 8 * st + 0);
+      if (CB_STUB_NLPR < 2) {
 
       // r2c untangle: I_hat[k], k = 0..H (numpy rfft, dbp.py:194). For P > 1
       // each bin goes straight from registers to the CTA whose MIMO slice
@@ -2092,9 +2098,10 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
           }
         }
       }
+      }  // CB_STUB_NLPR < 2
       __syncthreads();
       CB_MARK(8 + 8 * st + 4);
-      fft1<R, Q, H, NT, true, HS>(TS, twpH, &s_zero);
+      if (CB_STUB_NLPR < 1) fft1<R, Q, H, NT, true, HS>(TS, twpH, &s_zero);
       CB_MARK(8 + 8 * st + 5);
 
       // rotation exp(-i theta) fused into the first pass of the subband FFT
@@ -2104,7 +2111,7 @@ __global__ void __launch_bounds__(threads_for<R, Q>(), min_blocks<R, Q>())
       using Rot = typename std::conditional<ROTTAB, RotationTabHook<R>, RotationHook<R>>::type;
       Rot rot;
       rot.th = Treal;
-      rot.scale = tsc_st;
+      rot.scale = CB_STUB_NLPR ? (R)0 : tsc_st;
       if constexpr (ROTTAB) rot.tab = RT;
       const Cx<R>* ph_next = ph_rank + (size_t)phi_next * ph_tab;
       if (st + 1 < prm.n_steps) {
